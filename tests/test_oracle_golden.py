@@ -1,0 +1,119 @@
+"""Pin the C oracle against fixtures produced by the reference itself.
+
+Fixtures: tests/golden/make_golden.py (runs fifield 0.1.0, numba backend).
+Bar: bit-exact where the reference's arithmetic is plain scalar code (quad build,
+PC FIM + mask, queries, centres, indexing); <=1e-13 relative where the reference
+goes through BLAS/LAPACK (GP build kernels.py:505-519, det/lmin kernels.py:604-607).
+"""
+import numpy as np
+import pytest
+
+MODELS = ("quad", "gp30", "gp70")
+
+
+def model_tuple(g_models, name):
+    if name == "quad":
+        _, k2, k1, k0 = g_models["quad_k"]
+        return ("quad", k2, k1, k0)
+    par = g_models[f"{name}_par"]
+    return ("gp", g_models[f"{name}_zs"], par[2], par[3])
+
+
+def test_centers_bit_exact(oracle, g_small):
+    c = oracle.centers(g_small["origin"], g_small["voxel_size"][0], g_small["dims"])
+    assert np.array_equal(c, g_small["centers"])
+
+
+@pytest.mark.parametrize("kind", ["trace", "info"])
+def test_quad_build_bit_exact(oracle, g_small, g_models, kind):
+    _, k2, k1, k0 = g_models["quad_k"]
+    f = oracle.build_quad_factors(g_small["centers"], g_small["points"], 1.0, k2, k1, k0, kind == "trace")
+    assert np.array_equal(f, g_small[f"factors_quad_{kind}"])
+
+
+def test_quad_build_sigma(oracle, g_small, g_models):
+    _, k2, k1, k0 = g_models["quad_k"]
+    f = oracle.build_quad_factors(g_small["centers"], g_small["points"], 0.7, k2, k1, k0, False)
+    assert np.array_equal(f, g_small["factors_quad_info_sigma07"])
+
+
+@pytest.mark.parametrize("ns", [30, 70])
+@pytest.mark.parametrize("kind", ["trace", "info"])
+def test_gp_build(oracle, g_small, g_models, ns, kind):
+    par = g_models[f"gp{ns}_par"]
+    f = oracle.build_gp_factors(g_small["centers"], g_small["points"], 1.0, g_models[f"gp{ns}_zs"],
+                                g_models[f"gp{ns}_kinv"], par[1], np.cos(par[0]), kind == "trace")
+    ref = g_small[f"factors_gp{ns}_{kind}"]
+    assert np.abs(f - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_config1_rows(oracle, g_cfg1, g_models):
+    """Full config-1 landmark set (2 000, seed 0) on 24 sampled voxels."""
+    pts, cs = g_cfg1["points"], g_cfg1["centers"]
+    _, k2, k1, k0 = g_models["quad_k"]
+    par = g_models["gp70_par"]
+    for kind in ("trace", "info"):
+        q = oracle.build_quad_factors(cs, pts, 1.0, k2, k1, k0, kind == "trace")
+        assert np.array_equal(q, g_cfg1[f"quad_{kind}"])
+        gp = oracle.build_gp_factors(cs, pts, 1.0, g_models["gp70_zs"], g_models["gp70_kinv"], par[1],
+                                     np.cos(par[0]), kind == "trace")
+        ref = g_cfg1[f"gp70_{kind}"]
+        rel = np.linalg.norm(gp - ref, axis=1) / np.linalg.norm(ref, axis=1)
+        assert rel.max() <= 1e-12
+
+
+def test_pc_fim_and_mask_bit_exact(oracle, g_pc):
+    out = oracle.exact_fim_batch(g_pc["rotations"], g_pc["translations"], g_pc["points"], g_pc["camera"])
+    assert np.array_equal(out, g_pc["fims"])
+    mask = oracle.pc_mask(g_pc["rotations"], g_pc["translations"], g_pc["points"], g_pc["camera"])
+    assert np.array_equal(mask, g_pc["visible_kernel"])
+    # the Python helper exact_visible (fim.py:103-111) projects through a BLAS matmul and
+    # disagrees with the kernel on at most a handful of exact-border pairs
+    assert (mask != g_pc["visible"]).sum() <= 2
+
+
+@pytest.mark.parametrize("mname", MODELS)
+@pytest.mark.parametrize("kind", ["trace", "info"])
+@pytest.mark.parametrize("mode", ["nearest", "trilinear"])
+def test_queries_bit_exact(oracle, g_small, g_models, mname, kind, mode):
+    dims = g_small["dims"]
+    slots = np.arange(int(np.prod(dims)), dtype=np.int32)
+    pos, rots = g_small["positions"], g_small["rotations"]
+    axes = np.ascontiguousarray(rots[:, :, 2])
+    F = g_small[f"factors_{mname}_{kind}"]
+    mod = model_tuple(g_models, mname)
+    tri = mode == "trilinear"
+    v, st = oracle.metric_batch(slots, F, g_small["origin"], g_small["voxel_size"][0], dims, pos, axes, mod,
+                                "trace", kind == "trace", tri)
+    assert np.array_equal(st == 0, g_small[f"ok_{mname}_{kind}_{mode}"])
+    assert np.array_equal(v, g_small[f"trace_{mname}_{kind}_{mode}"])
+    if kind == "info":
+        f, st = oracle.query_fim_batch(slots, F, g_small["origin"], g_small["voxel_size"][0], dims, pos, axes, mod,
+                                       tri)
+        assert np.array_equal(f, g_small[f"fim_{mname}_{mode}"])
+        for metric in ("det", "lmin"):
+            mv, _ = oracle.metric_batch(slots, F, g_small["origin"], g_small["voxel_size"][0], dims, pos, axes, mod,
+                                        metric, False, tri)
+            ref = g_small[f"{metric}_{mname}_{mode}"]
+            assert np.abs(mv - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_indexing_bit_exact(oracle, g_small):
+    dims, o, vs = g_small["dims"], g_small["origin"], g_small["voxel_size"][0]
+    near = np.array([oracle.locate_nearest(o, vs, dims, p) for p in g_small["positions"]])
+    assert np.array_equal(near, g_small["nearest_index"])
+    ref = g_small["trilinear_idx_w"]
+    for i, p in enumerate(g_small["positions"]):
+        r = oracle.trilinear(o, vs, dims, p)
+        if r is None:
+            assert np.isnan(ref[i, 0])
+        else:
+            assert np.array_equal(r[0].astype(np.float64), ref[i, :8])
+            assert np.array_equal(r[1], ref[i, 8:])
+
+
+def test_landmark_fim_kats(oracle, g_kats):
+    for i in range(g_kats["t"].shape[0]):
+        f, tr = oracle.fim_flat(g_kats["p"][i], g_kats["t"][i], 1.0 / g_kats["sigma"][i] ** 2)
+        np.testing.assert_allclose(f, g_kats["fim"][i], rtol=1e-13, atol=1e-15)
+        assert tr == pytest.approx(np.trace(f), rel=1e-14)
