@@ -1,0 +1,669 @@
+// fif_build.cu — field build (positional information factors), sm_100a.
+//
+// Replaces the voxel x landmark loops of the reference:
+//   _nb_build_quad / _nb_build_quad_par  kernels.py:427-468, 527-568
+//   _nb_build_gp                         kernels.py:471-524
+//   per-pair 6x6 information             _nb_fim_flat_into kernels.py:363-424
+//
+// N-body structure: a CTA owns a tile of voxels; landmark tiles stream through
+// shared memory and are broadcast to every thread.  Per-pair arithmetic is FP32
+// on a difference d = p - c that is exact to ~1 ulp (landmarks and centres are
+// pre-split into float hi/lo pairs), partial sums over short landmark runs are
+// FP32 and are flushed into FP64 / double-float accumulators so the final
+// factors carry ~1e-9 relative error (the query-parity budget).
+// GP trace evaluates the sigmoid's cosine in FP64 (FP64 pipe is otherwise idle)
+// because the kinv epilogue amplifies S errors ~200x.
+#include <cstdarg>
+#include <mutex>
+
+#include "fif_common.cuh"
+
+namespace fif {
+
+// ─────────────────────────── landmark table ────────────────────────────
+// Per landmark 2 x float4: {ph.x, ph.y, ph.z, |p|^2}, {pl.x, pl.y, pl.z, valid}
+// with p = ph + pl.  Rows past n are zero with valid = 0 (zero contribution).
+constexpr int kLmPad = 256;
+
+__global__ void k_prep_landmarks(const double* __restrict__ pts, int64_t n, int64_t n_pad, float4* __restrict__ tab) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n) {
+    double px = pts[3 * i], py = pts[3 * i + 1], pz = pts[3 * i + 2];
+    split_f32(px, a.x, b.x);
+    split_f32(py, a.y, b.y);
+    split_f32(pz, a.z, b.z);
+    a.w = __double2float_rn(px * px + py * py + pz * pz);
+    b.w = 1.0f;
+  }
+  tab[2 * i] = a;
+  tab[2 * i + 1] = b;
+}
+
+// Per-pair prologue shared by the quad kernels and GP-info phase A.
+struct PairF {
+  float ux, uy, uz, w;  // unit bearing c->p and w = 1/(sigma^2 n^2) (0 if skipped)
+};
+
+__device__ __forceinline__ PairF pair_prologue(float4 a, float4 b, const float ch[3], const float cl[3], float inv_s2) {
+  float dx = __fadd_rn(__fsub_rn(a.x, ch[0]), __fsub_rn(b.x, cl[0]));
+  float dy = __fadd_rn(__fsub_rn(a.y, ch[1]), __fsub_rn(b.y, cl[1]));
+  float dz = __fadd_rn(__fsub_rn(a.z, ch[2]), __fsub_rn(b.z, cl[2]));
+  float n2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  // the reference skips n2 < 1e-300 (kernels.py:444); in FP32 a coincident
+  // landmark gives n2 == 0 and is skipped through rn = 0
+  bool ok = n2 > 1e-30f && b.w != 0.f;
+  float rn = ok ? rsqrtf(n2) : 0.f;
+  // one Newton step: rsqrt to ~1 ulp
+  rn = fmaf(0.5f * rn, fmaf(-n2 * rn, rn, 1.0f), rn);
+  PairF q;
+  q.ux = dx * rn;
+  q.uy = dy * rn;
+  q.uz = dz * rn;
+  q.w = inv_s2 * rn * rn;
+  return q;
+}
+
+__device__ __forceinline__ void voxel_split(const VoxSrc& src, int64_t v, float ch[3], float cl[3]) {
+  double cx, cy, cz;
+  voxel_center(src, v, cx, cy, cz);
+  split_f32(cx, ch[0], cl[0]);
+  split_f32(cy, ch[1], cl[1]);
+  split_f32(cz, ch[2], cl[2]);
+}
+
+// ─────────────────────────── quad, trace ───────────────────────────────
+// One thread per voxel; out (rows,10) f64: sum_i vp_i[k] * tr_i.
+constexpr int QT_THREADS = 128;
+constexpr int QT_TILE = 128;   // landmarks per smem tile
+constexpr int QT_FLUSH = 16;   // FP32 partial run length before the FP64 flush
+
+template <bool HAS_MASK>
+__global__ void __launch_bounds__(QT_THREADS) k_quad_trace(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real,
+                                                           VoxSrc src, int64_t v0, int64_t v1,
+                                                           const uint8_t* __restrict__ mask, float inv_s2,
+                                                           double* __restrict__ out) {
+  __shared__ float4 tile[QT_TILE * 2];
+  const int64_t v = v0 + blockIdx.x * (int64_t)QT_THREADS + threadIdx.x;
+  const bool active = v < v1;
+  float ch[3], cl[3];
+  voxel_split(src, active ? v : v0, ch, cl);
+  double acc[10];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) acc[k] = 0.0;
+  for (int64_t base = 0; base < n_pad; base += QT_TILE) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < QT_TILE * 2; j += QT_THREADS) tile[j] = lm[2 * base + j];
+    __syncthreads();
+#pragma unroll 1
+    for (int j0 = 0; j0 < QT_TILE; j0 += QT_FLUSH) {
+      float part[10];
+#pragma unroll
+      for (int k = 0; k < 10; ++k) part[k] = 0.f;
+#pragma unroll 4
+      for (int j = j0; j < j0 + QT_FLUSH; ++j) {
+        float4 a = tile[2 * j], b = tile[2 * j + 1];
+        if (HAS_MASK) {
+          int64_t i = base + j;
+          if (i < n_real && active && mask[(v - v0) * n_real + i] == 0) b.w = 0.f;
+        }
+        PairF q = pair_prologue(a, b, ch, cl, inv_s2);
+        // tr = w (2 + |p|^2 + (p.u)^2) = sum of the six diagonal entries (kernels.py:424)
+        float pu = fmaf(a.x, q.ux, fmaf(a.y, q.uy, a.z * q.uz));
+        float tr = q.w * fmaf(pu, pu, 2.0f + a.w);
+        float tx = tr * q.ux, ty = tr * q.uy, tz = tr * q.uz;
+        part[0] = fmaf(tx, q.ux, part[0]);
+        part[1] = fmaf(ty, q.uy, part[1]);
+        part[2] = fmaf(tz, q.uz, part[2]);
+        part[3] = fmaf(tx, q.uy, part[3]);
+        part[4] = fmaf(tx, q.uz, part[4]);
+        part[5] = fmaf(ty, q.uz, part[5]);
+        part[6] += tx;
+        part[7] += ty;
+        part[8] += tz;
+        part[9] += tr;
+      }
+#pragma unroll
+      for (int k = 0; k < 10; ++k) acc[k] += (double)part[k];
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) out[(v - v0) * 10 + k] = acc[k];
+  }
+}
+
+// ─────────────────────────── quad, info ────────────────────────────────
+// Warp-uniform entry groups: warp (w % 4) of a CTA owns a subset of the 21
+// unique entries of the symmetric 6x6 for the CTA's 32 voxels (one per lane).
+// G0: TL {0,1,2,6,7,11}  G1: TR {3,4,5,8,9}  G2: {10,12,13,14,15}  G3: BR {16..20}
+constexpr int QI_THREADS = 128;
+constexpr int QI_TILE = 128;
+constexpr int QI_FLUSH = 32;
+template <int G> struct QGroup { static constexpr int NE = G == 0 ? 6 : 5; };
+// packed index of entry t of group G
+__host__ __device__ constexpr int qidx(int G, int t) {
+  return G == 0 ? (t < 3 ? t : (t < 5 ? t + 3 : 11))
+       : G == 1 ? (t < 3 ? 3 + t : 5 + t)
+       : G == 2 ? (t == 0 ? 10 : 11 + t)
+       : 16 + t;
+}
+
+// Entries of w * block (kernels.py:385-423), world-frame p (global perturbation).
+template <int G>
+__device__ __forceinline__ void group_entries(const PairF& q, float4 a, float* e) {
+  const float w = q.w, ux = q.ux, uy = q.uy, uz = q.uz;
+  const float px = a.x, py = a.y, pz = a.z, pp = a.w;
+  if (G == 0) {
+    float wx = w * ux, wy = w * uy, wz = w * uz;
+    e[0] = fmaf(-wx, ux, w);
+    e[1] = -wx * uy;
+    e[2] = -wx * uz;
+    e[3] = fmaf(-wy, uy, w);
+    e[4] = -wy * uz;
+    e[5] = fmaf(-wz, uz, w);
+  } else {
+    float c2x = fmaf(py, uz, -pz * uy);
+    float c2y = fmaf(pz, ux, -px * uz);
+    float c2z = fmaf(px, uy, -py * ux);
+    if (G == 1) {
+      e[0] = -w * (ux * c2x);            // (0,3)
+      e[1] = -w * fmaf(ux, c2y, -pz);    // (0,4)
+      e[2] = -w * fmaf(ux, c2z, py);     // (0,5)
+      e[3] = -w * fmaf(uy, c2x, pz);     // (1,3)
+      e[4] = -w * (uy * c2y);            // (1,4)
+    } else if (G == 2) {
+      e[0] = -w * fmaf(uy, c2z, -px);    // (1,5)
+      e[1] = -w * fmaf(uz, c2x, -py);    // (2,3)
+      e[2] = -w * fmaf(uz, c2y, px);     // (2,4)
+      e[3] = -w * (uz * c2z);            // (2,5)
+      e[4] = w * fmaf(-c2x, c2x, fmaf(-px, px, pp));  // (3,3)
+    } else {
+      e[0] = w * fmaf(-c2x, c2y, -px * py);          // (3,4)
+      e[1] = w * fmaf(-c2x, c2z, -px * pz);          // (3,5)
+      e[2] = w * fmaf(-c2y, c2y, fmaf(-py, py, pp));  // (4,4)
+      e[3] = w * fmaf(-c2y, c2z, -py * pz);          // (4,5)
+      e[4] = w * fmaf(-c2z, c2z, fmaf(-pz, pz, pp));  // (5,5)
+    }
+  }
+}
+
+template <int G, bool HAS_MASK>
+__device__ __forceinline__ void quad_info_body(const float4* __restrict__ lm, float4* tile, double* accs, int64_t n_pad,
+                                               int64_t n_real, const VoxSrc& src, int64_t v, int64_t v0, bool active,
+                                               const uint8_t* __restrict__ mask, float inv_s2,
+                                               double* __restrict__ out) {
+  constexpr int NE = QGroup<G>::NE;
+  const int lane = threadIdx.x & 31;
+  float ch[3], cl[3];
+  voxel_split(src, active ? v : v0, ch, cl);
+  // FP64 accumulators live in shared memory: [k*NE + j][lane]
+#pragma unroll
+  for (int t = 0; t < 10 * NE; ++t) accs[t * 32 + lane] = 0.0;
+  for (int64_t base = 0; base < n_pad; base += QI_TILE) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < QI_TILE * 2; j += QI_THREADS) tile[j] = lm[2 * base + j];
+    __syncthreads();
+#pragma unroll 1
+    for (int j0 = 0; j0 < QI_TILE; j0 += QI_FLUSH) {
+      float part[10 * NE];
+#pragma unroll
+      for (int t = 0; t < 10 * NE; ++t) part[t] = 0.f;
+#pragma unroll 2
+      for (int j = j0; j < j0 + QI_FLUSH; ++j) {
+        float4 a = tile[2 * j], b = tile[2 * j + 1];
+        if (HAS_MASK) {
+          int64_t i = base + j;
+          if (i < n_real && active && mask[(v - v0) * n_real + i] == 0) b.w = 0.f;
+        }
+        PairF q = pair_prologue(a, b, ch, cl, inv_s2);
+        float e[NE];
+        group_entries<G>(q, a, e);
+        const float vp[10] = {q.ux * q.ux, q.uy * q.uy, q.uz * q.uz, q.ux * q.uy, q.ux * q.uz,
+                              q.uy * q.uz, q.ux, q.uy, q.uz, 1.0f};
+#pragma unroll
+        for (int k = 0; k < 10; ++k)
+#pragma unroll
+          for (int t = 0; t < NE; ++t) part[k * NE + t] = fmaf(vp[k], e[t], part[k * NE + t]);
+      }
+#pragma unroll
+      for (int t = 0; t < 10 * NE; ++t) accs[t * 32 + lane] += (double)part[t];
+    }
+  }
+  if (active) {
+    double* o = out + (v - v0) * 210;
+#pragma unroll
+    for (int k = 0; k < 10; ++k)
+#pragma unroll
+      for (int t = 0; t < NE; ++t) o[k * 21 + qidx(G, t)] = accs[(k * NE + t) * 32 + lane];
+  }
+}
+
+template <bool HAS_MASK>
+__global__ void __launch_bounds__(QI_THREADS) k_quad_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real,
+                                                          VoxSrc src, int64_t v0, int64_t v1,
+                                                          const uint8_t* __restrict__ mask, float inv_s2,
+                                                          double* __restrict__ out) {
+  __shared__ float4 tile[QI_TILE * 2];
+  extern __shared__ double accs_all[];  // 4 warps x 60 x 32 doubles
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t v = v0 + blockIdx.x * (int64_t)32 + lane;
+  const bool active = v < v1;
+  double* accs = accs_all + warp * 60 * 32;
+  switch (warp) {
+    case 0: quad_info_body<0, HAS_MASK>(lm, tile, accs, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
+    case 1: quad_info_body<1, HAS_MASK>(lm, tile, accs, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
+    case 2: quad_info_body<2, HAS_MASK>(lm, tile, accs, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
+    default: quad_info_body<3, HAS_MASK>(lm, tile, accs, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
+  }
+}
+
+// ─────────────────────────── GP, trace ─────────────────────────────────
+// CTA = VB voxels x N_s samples (thread (v, g)).  Phase A: per (voxel, landmark)
+// pair, FP64 bearing u and FP32 trace tr into smem.  Phase B: thread (v, g)
+// evaluates vs = sigmoid(k_s (u.z_g - cos a)) with the cosine in FP64 and the
+// exponent/reciprocal on MUFU, and accumulates tr * vs.
+constexpr int GT_TILE = 64;
+constexpr int GT_FLUSH = 8;
+struct __align__(16) PairT {
+  double ux, uy, uz;
+  float tr, pad;
+};
+
+template <bool HAS_MASK>
+__global__ void k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1, int vb,
+                           int ns, const double* __restrict__ zs, const uint8_t* __restrict__ mask, double inv_s2,
+                           double ax, double bx, double* __restrict__ out64, float* __restrict__ out32) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairT* pairs = reinterpret_cast<PairT*>(smem_raw);                     // [vb][GT_TILE]
+  double* cen = reinterpret_cast<double*>(pairs + vb * GT_TILE);         // [vb][3]
+  double* lp = cen + 3 * vb;                                             // [GT_TILE][3] landmark tile
+  const int t = threadIdx.x;
+  const int64_t vbase = v0 + blockIdx.x * (int64_t)vb;
+  if (t < vb) {
+    int64_t v = vbase + t;
+    double cx = 0, cy = 0, cz = 0;
+    if (v < v1) voxel_center(src, v, cx, cy, cz);
+    cen[3 * t] = cx;
+    cen[3 * t + 1] = cy;
+    cen[3 * t + 2] = cz;
+  }
+  const int vl = t / ns, g = t - vl * ns;
+  const bool worker = vl < vb;
+  const bool active = worker && (vbase + vl) < v1;
+  double zx = 0, zy = 0, zz = 0;
+  if (worker) {
+    zx = zs[3 * g];
+    zy = zs[3 * g + 1];
+    zz = zs[3 * g + 2];
+  }
+  DF acc;
+  acc.init();
+  const int npairs = vb * GT_TILE;
+  for (int64_t base = 0; base < n_real; base += GT_TILE) {
+    __syncthreads();
+    for (int j = t; j < GT_TILE * 3; j += blockDim.x) {
+      int64_t i = base + j / 3;
+      lp[j] = i < n_real ? pts[3 * base + j] : 0.0;
+    }
+    __syncthreads();
+    // phase A: FP64 per-pair quantities (exactly the reference's d, n2, skip rule)
+    for (int pidx = t; pidx < npairs; pidx += blockDim.x) {
+      int pv = pidx / GT_TILE, pj = pidx - pv * GT_TILE;
+      int64_t i = base + pj;
+      double px = lp[3 * pj], py = lp[3 * pj + 1], pz = lp[3 * pj + 2];
+      double dx = px - cen[3 * pv], dy = py - cen[3 * pv + 1], dz = pz - cen[3 * pv + 2];
+      double n2 = dx * dx + dy * dy + dz * dz;
+      bool ok = i < n_real && n2 >= 1e-300 && (vbase + pv) < v1;
+      if (HAS_MASK && ok) ok = mask[(vbase + pv - v0) * n_real + i] != 0;
+      PairT pr;
+      if (ok) {
+        double rn = rsqrt(n2);
+        double ux = dx * rn, uy = dy * rn, uz = dz * rn;
+        double w = inv_s2 * rn * rn;
+        double pu = px * ux + py * uy + pz * uz;
+        double pp = px * px + py * py + pz * pz;
+        pr.ux = ux;
+        pr.uy = uy;
+        pr.uz = uz;
+        pr.tr = (float)(w * (2.0 + pp + pu * pu));
+      } else {
+        pr.ux = pr.uy = pr.uz = 0.0;
+        pr.tr = 0.f;
+      }
+      pr.pad = 0.f;
+      pairs[pidx] = pr;
+    }
+    __syncthreads();
+    if (worker) {
+      const PairT* pv = pairs + vl * GT_TILE;
+#pragma unroll 1
+      for (int j0 = 0; j0 < GT_TILE; j0 += GT_FLUSH) {
+        float part = 0.f;
+#pragma unroll
+        for (int j = j0; j < j0 + GT_FLUSH; ++j) {
+          PairT pr = pv[j];
+          double c = fma(pr.ux, zx, fma(pr.uy, zy, pr.uz * zz));
+          float x = f64_to_f32_alu(fma(c, ax, bx));  // -k_s (c - cos a) log2(e)
+          float vs = rcp_approx(1.0f + ex2_approx(x));
+          part = fmaf(pr.tr, vs, part);
+        }
+        acc.add(part);
+      }
+    }
+  }
+  if (active) {
+    int64_t r = vbase + vl - v0;
+    double s = acc.value();
+    out64[r * ns + g] = s;
+    if (out32) out32[r * ns + g] = (float)s;
+  }
+}
+
+// ─────────────────────────── GP, info ──────────────────────────────────
+// Phase A: per pair, u and the 21 unique entries of w*block in FP32 (24 floats);
+// phase B: thread (v, g) accumulates vs_g * entries into 21 FP32 partials,
+// flushed every GI_FLUSH landmarks into double-float accumulators.
+constexpr int GI_TILE = 32;
+constexpr int GI_FLUSH = 16;
+
+__device__ __forceinline__ void all_entries(const PairF& q, float4 a, float* e) {
+  group_entries<0>(q, a, e + 0);   // slots 0,1,2,6,7,11
+  group_entries<1>(q, a, e + 6);   // 3,4,5,8,9
+  group_entries<2>(q, a, e + 11);  // 10,12,13,14,15
+  group_entries<3>(q, a, e + 16);  // 16..20
+}
+// position in the e[] order above of each packed index 0..20
+__constant__ int kEntryPerm[21] = {0, 1, 2, 6, 7, 8, 3, 4, 9, 10, 11, 5, 12, 13, 14, 15, 16, 17, 18, 19, 20};
+
+template <bool HAS_MASK>
+__global__ void k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0,
+                          int64_t v1, int vb, int ns, const double* __restrict__ zs, const uint8_t* __restrict__ mask,
+                          float inv_s2, float ax, float bx, double* __restrict__ out64, float* __restrict__ out32) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4* pairs = reinterpret_cast<float4*>(smem_raw);          // [vb][GI_TILE][6]
+  float4* tile = pairs + vb * GI_TILE * 6;                      // [GI_TILE][2]
+  float* cs = reinterpret_cast<float*>(tile + GI_TILE * 2);     // [vb][6] centre hi/lo
+  const int t = threadIdx.x;
+  const int64_t vbase = v0 + blockIdx.x * (int64_t)vb;
+  if (t < vb) {
+    int64_t v = vbase + t;
+    float ch[3], cl[3];
+    voxel_split(src, v < v1 ? v : v0, ch, cl);
+    for (int a = 0; a < 3; ++a) {
+      cs[6 * t + a] = ch[a];
+      cs[6 * t + 3 + a] = cl[a];
+    }
+  }
+  const int vl = t / ns, g = t - vl * ns;
+  const bool worker = vl < vb;
+  const bool active = worker && (vbase + vl) < v1;
+  float zx = 0.f, zy = 0.f, zz = 0.f;
+  if (worker) {
+    zx = (float)zs[3 * g];
+    zy = (float)zs[3 * g + 1];
+    zz = (float)zs[3 * g + 2];
+  }
+  DF acc[21];
+#pragma unroll
+  for (int e = 0; e < 21; ++e) acc[e].init();
+  const int npairs = vb * GI_TILE;
+  for (int64_t base = 0; base < n_pad; base += GI_TILE) {
+    __syncthreads();
+    for (int j = t; j < GI_TILE * 2; j += blockDim.x) tile[j] = lm[2 * base + j];
+    __syncthreads();
+    for (int pidx = t; pidx < npairs; pidx += blockDim.x) {
+      int pv = pidx / GI_TILE, pj = pidx - pv * GI_TILE;
+      float4 a = tile[2 * pj], b = tile[2 * pj + 1];
+      if ((vbase + pv) >= v1) b.w = 0.f;
+      if (HAS_MASK) {
+        int64_t i = base + pj;
+        if (b.w != 0.f && mask[(vbase + pv - v0) * n_real + i] == 0) b.w = 0.f;
+      }
+      const float* c = cs + 6 * pv;
+      float ch[3] = {c[0], c[1], c[2]}, cl[3] = {c[3], c[4], c[5]};
+      PairF q = pair_prologue(a, b, ch, cl, inv_s2);
+      float e[21];
+      all_entries(q, a, e);
+      float4* dst = pairs + pidx * 6;
+      dst[0] = make_float4(q.ux, q.uy, q.uz, e[kEntryPerm[0]]);
+      dst[1] = make_float4(e[kEntryPerm[1]], e[kEntryPerm[2]], e[kEntryPerm[3]], e[kEntryPerm[4]]);
+      dst[2] = make_float4(e[kEntryPerm[5]], e[kEntryPerm[6]], e[kEntryPerm[7]], e[kEntryPerm[8]]);
+      dst[3] = make_float4(e[kEntryPerm[9]], e[kEntryPerm[10]], e[kEntryPerm[11]], e[kEntryPerm[12]]);
+      dst[4] = make_float4(e[kEntryPerm[13]], e[kEntryPerm[14]], e[kEntryPerm[15]], e[kEntryPerm[16]]);
+      dst[5] = make_float4(e[kEntryPerm[17]], e[kEntryPerm[18]], e[kEntryPerm[19]], e[kEntryPerm[20]]);
+    }
+    __syncthreads();
+    if (worker) {
+      const float4* pv = pairs + vl * GI_TILE * 6;
+#pragma unroll 1
+      for (int j0 = 0; j0 < GI_TILE; j0 += GI_FLUSH) {
+        float part[21];
+#pragma unroll
+        for (int e = 0; e < 21; ++e) part[e] = 0.f;
+#pragma unroll 2
+        for (int j = j0; j < j0 + GI_FLUSH; ++j) {
+          const float4* p = pv + 6 * j;
+          float4 r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3], r4 = p[4], r5 = p[5];
+          float c = fmaf(r0.x, zx, fmaf(r0.y, zy, r0.z * zz));
+          float vs = rcp_approx(1.0f + ex2_approx(fmaf(c, ax, bx)));
+          const float ent[21] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w, r3.x, r3.y,
+                                 r3.z, r3.w, r4.x, r4.y, r4.z, r4.w, r5.x, r5.y, r5.z, r5.w};
+#pragma unroll
+          for (int e = 0; e < 21; ++e) part[e] = fmaf(vs, ent[e], part[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 21; ++e) acc[e].add(part[e]);
+      }
+    }
+  }
+  if (active) {
+    int64_t r = vbase + vl - v0;
+    double* o = out64 + (r * ns + g) * 21;
+#pragma unroll
+    for (int e = 0; e < 21; ++e) o[e] = acc[e].value();
+    if (out32) {
+      float* o32 = out32 + (r * ns + g) * 21;
+#pragma unroll
+      for (int e = 0; e < 21; ++e) o32[e] = (float)acc[e].value();
+    }
+  }
+}
+
+// ─────────────────────────── exports ───────────────────────────────────
+// Expand packed (rows, nv, 21) to the reference's (rows, nv*36).
+__global__ void k_expand36(const double* __restrict__ in, int64_t blocks, double* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= blocks * 36) return;
+  int64_t b = i / 36;
+  int rc = (int)(i - b * 36), r = rc / 6, c = rc - r * 6;
+  int lo = r < c ? r : c, hi = r < c ? c : r;
+  out[i] = in[b * 21 + packed_index(lo, hi)];
+}
+
+// F = kinv @ S per voxel (kinv symmetric; reference factor of kernels.py:511-523).
+// S (rows, ns, W), W = 1 (trace) or 21 (info); out (rows, ns, W) f64.
+__global__ void k_gp_apply_kinv(const double* __restrict__ S, int64_t rows, int ns, int W,
+                                const double* __restrict__ kinv, double* __restrict__ out) {
+  extern __shared__ double sm[];  // S row [ns*W]
+  const int64_t r = blockIdx.x;
+  const int n = ns * W;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) sm[j] = S[r * n + j];
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    int k = j / W, e = j - k * W;
+    double s = 0.0;
+    for (int gidx = 0; gidx < ns; ++gidx) s = fma(kinv[(int64_t)k * ns + gidx], sm[gidx * W + e], s);
+    out[r * n + j] = s;
+  }
+}
+
+}  // namespace fif
+
+using namespace fif;
+
+extern "C" int64_t fif_build_scratch_bytes(int64_t n_points) {
+  int64_t n_pad = ((n_points + kLmPad - 1) / kLmPad) * kLmPad;
+  if (n_pad == 0) n_pad = kLmPad;
+  return n_pad * 2 * (int64_t)sizeof(float4);
+}
+
+extern "C" int fif_build(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
+                         const fif_grid* grid, const double* d_centers, int64_t v_begin, int64_t v_end,
+                         const uint8_t* d_mask, double sigma, void* d_scratch, double* d_out64, float* d_out32,
+                         void* stream) {
+  FIF_CHECK_ARG(model != nullptr, "fif_build: model is NULL");
+  FIF_CHECK_ARG(factor_kind == FIF_KIND_INFO || factor_kind == FIF_KIND_TRACE, "fif_build: bad factor_kind %d",
+                factor_kind);
+  FIF_CHECK_ARG(model->kind == FIF_MODEL_QUAD || model->kind == FIF_MODEL_GP, "fif_build: bad model kind %d",
+                model->kind);
+  FIF_CHECK_ARG(v_end >= v_begin && v_begin >= 0, "fif_build: bad voxel range [%lld,%lld)", (long long)v_begin,
+                (long long)v_end);
+  FIF_CHECK_ARG(d_out64 != nullptr, "fif_build: d_out64 is NULL");
+  FIF_CHECK_ARG(sigma > 0, "fif_build: sigma must be positive");
+  FIF_CHECK_ARG(n_points >= 0, "fif_build: n_points < 0");
+  FIF_CHECK_ARG(n_points == 0 || d_points != nullptr, "fif_build: d_points is NULL");
+  FIF_CHECK_ARG(d_centers != nullptr || grid != nullptr, "fif_build: need a grid or explicit centres");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows = v_end - v_begin;
+  const bool trace = factor_kind == FIF_KIND_TRACE;
+  const int nv = model->kind == FIF_MODEL_QUAD ? 10 : model->n_v;
+  const int64_t width = trace ? nv : (int64_t)nv * 21;
+  if (rows == 0) return FIF_OK;
+  if (n_points == 0) {
+    // no landmarks: every factor is exactly zero (field.py:248-252 builds an empty map)
+    cudaMemsetAsync(d_out64, 0, sizeof(double) * rows * width, st);
+    if (d_out32) cudaMemsetAsync(d_out32, 0, sizeof(float) * rows * width, st);
+    FIF_CHECK_LAUNCH("fif_build(memset)");
+    return FIF_OK;
+  }
+  VoxSrc src{};
+  src.centers = d_centers;
+  if (grid) {
+    src.ox = grid->origin[0];
+    src.oy = grid->origin[1];
+    src.oz = grid->origin[2];
+    src.vs = grid->voxel_size;
+    src.nx = grid->dims[0];
+    src.ny = grid->dims[1];
+    src.nz = grid->dims[2];
+    if (!d_centers) {
+      FIF_CHECK_ARG(grid->voxel_size > 0 && grid->dims[0] > 0 && grid->dims[1] > 0 && grid->dims[2] > 0,
+                    "fif_build: empty grid");
+      FIF_CHECK_ARG(v_end <= grid->dims[0] * grid->dims[1] * grid->dims[2], "fif_build: v_end beyond grid");
+    }
+  }
+  const double inv_s2 = 1.0 / (sigma * sigma);
+  const bool has_mask = d_mask != nullptr;
+  int64_t n_pad = ((n_points + kLmPad - 1) / kLmPad) * kLmPad;
+  float4* lm = reinterpret_cast<float4*>(d_scratch);
+  const bool need_lm = !(model->kind == FIF_MODEL_GP && trace);
+  if (need_lm) {
+    FIF_CHECK_ARG(d_scratch != nullptr, "fif_build: d_scratch is NULL");
+    k_prep_landmarks<<<(unsigned)((n_pad + 255) / 256), 256, 0, st>>>(d_points, n_points, n_pad, lm);
+    FIF_CHECK_LAUNCH("k_prep_landmarks");
+  }
+  if (model->kind == FIF_MODEL_QUAD) {
+    if (trace) {
+      unsigned blocks = (unsigned)((rows + QT_THREADS - 1) / QT_THREADS);
+      if (has_mask)
+        k_quad_trace<true><<<blocks, QT_THREADS, 0, st>>>(lm, n_pad, n_points, src, v_begin, v_end, d_mask,
+                                                          (float)inv_s2, d_out64);
+      else
+        k_quad_trace<false><<<blocks, QT_THREADS, 0, st>>>(lm, n_pad, n_points, src, v_begin, v_end, d_mask,
+                                                           (float)inv_s2, d_out64);
+      FIF_CHECK_LAUNCH("k_quad_trace");
+    } else {
+      unsigned blocks = (unsigned)((rows + 31) / 32);
+      size_t smem = 4 * 60 * 32 * sizeof(double);
+      static bool attr_set = false;
+      if (!attr_set) {
+        cudaFuncSetAttribute(k_quad_info<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_quad_info<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+      }
+      if (has_mask)
+        k_quad_info<true><<<blocks, QI_THREADS, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, d_mask,
+                                                            (float)inv_s2, d_out64);
+      else
+        k_quad_info<false><<<blocks, QI_THREADS, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, d_mask,
+                                                             (float)inv_s2, d_out64);
+      FIF_CHECK_LAUNCH("k_quad_info");
+    }
+    return FIF_OK;
+  }
+  // GP
+  const int ns = model->n_v;
+  FIF_CHECK_ARG(ns >= 1 && ns <= 1024, "fif_build: N_s=%d out of range", ns);
+  FIF_CHECK_ARG(model->zs != nullptr, "fif_build: GP model without zs");
+  // sigmoid 1/(1 + exp(-k_s (c - cos a))) = 1/(1 + 2^(c*ax + bx))
+  const double LOG2E = 1.4426950408889634;
+  const double ax = -model->k_s * LOG2E, bx = model->k_s * model->cos_alpha * LOG2E;
+  int vb = 320 / ns;
+  if (vb < 1) vb = 1;
+  int threads = ((vb * ns + 31) / 32) * 32;
+  unsigned blocks = (unsigned)((rows + vb - 1) / vb);
+  if (trace) {
+    size_t smem = sizeof(PairT) * vb * GT_TILE + sizeof(double) * 3 * vb + sizeof(double) * 3 * GT_TILE;
+    if (has_mask)
+      k_gp_trace<true><<<blocks, threads, smem, st>>>(d_points, n_points, src, v_begin, v_end, vb, ns, model->zs,
+                                                      d_mask, inv_s2, ax, bx, d_out64, d_out32);
+    else
+      k_gp_trace<false><<<blocks, threads, smem, st>>>(d_points, n_points, src, v_begin, v_end, vb, ns, model->zs,
+                                                       d_mask, inv_s2, ax, bx, d_out64, d_out32);
+    FIF_CHECK_LAUNCH("k_gp_trace");
+  } else {
+    size_t smem = sizeof(float4) * (vb * GI_TILE * 6 + GI_TILE * 2) + sizeof(float) * 6 * vb;
+    if (smem > 48 * 1024) {
+      cudaFuncSetAttribute(k_gp_info<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_gp_info<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    if (has_mask)
+      k_gp_info<true><<<blocks, threads, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, vb, ns, model->zs,
+                                                     d_mask, (float)inv_s2, (float)ax, (float)bx, d_out64, d_out32);
+    else
+      k_gp_info<false><<<blocks, threads, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, vb, ns, model->zs,
+                                                      d_mask, (float)inv_s2, (float)ax, (float)bx, d_out64, d_out32);
+    FIF_CHECK_LAUNCH("k_gp_info");
+  }
+  return FIF_OK;
+}
+
+extern "C" int fif_export_reference(int factor_kind, const fif_model* model, const double* d_in64, int64_t rows,
+                                    double* d_out, void* stream) {
+  FIF_CHECK_ARG(model != nullptr && d_in64 != nullptr && d_out != nullptr, "fif_export_reference: NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool trace = factor_kind == FIF_KIND_TRACE;
+  const int nv = model->kind == FIF_MODEL_QUAD ? 10 : model->n_v;
+  if (rows == 0) return FIF_OK;
+  const double* src = d_in64;
+  double* tmp = nullptr;
+  if (model->kind == FIF_MODEL_GP) {
+    FIF_CHECK_ARG(model->kinv != nullptr, "fif_export_reference: GP model without kinv");
+    const int W = trace ? 1 : 21;
+    double* dst = d_out;
+    if (!trace) {
+      if (cudaMallocAsync(&tmp, sizeof(double) * rows * nv * 21, st) != cudaSuccess) {
+        set_error("fif_export_reference: cudaMallocAsync failed");
+        return FIF_ERR_CUDA;
+      }
+      dst = tmp;
+    }
+    size_t smem = sizeof(double) * nv * W;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_gp_apply_kinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_gp_apply_kinv<<<(unsigned)rows, 256, smem, st>>>(d_in64, rows, nv, W, model->kinv, dst);
+    FIF_CHECK_LAUNCH("k_gp_apply_kinv");
+    if (trace) return FIF_OK;
+    src = tmp;
+  } else if (trace) {
+    cudaMemcpyAsync(d_out, d_in64, sizeof(double) * rows * 10, cudaMemcpyDeviceToDevice, st);
+    FIF_CHECK_LAUNCH("fif_export_reference(copy)");
+    return FIF_OK;
+  }
+  int64_t blocks36 = rows * nv;
+  k_expand36<<<(unsigned)((blocks36 * 36 + 255) / 256), 256, 0, st>>>(src, blocks36, d_out);
+  FIF_CHECK_LAUNCH("k_expand36");
+  if (tmp) cudaFreeAsync(tmp, st);
+  return FIF_OK;
+}

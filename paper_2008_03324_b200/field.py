@@ -1,0 +1,713 @@
+"""GPU-resident Fisher Information Field — drop-in for fifield/field.py.
+
+Build (field.py:229-268 -> kernels.build_*_factors) runs the sm_100a N-body
+kernels of csrc/fif_build.cu; queries (field.py:313-457 -> kernels.query_* /
+field_metric_*) run the warp-per-query kernel of csrc/fif_query.cu.  The public
+surface — GridConfig, Matchability, Field.build / query_fim / query_fim_batch /
+query_metric / metric_axis_batch / query_factor / add|remove|update_landmark /
+memory_stats / serialize / deserialize and the slots / factors /
+occupied_index3 attributes — matches the reference, so callers switch by import.
+
+Device storage:
+  * ALWAYS_MATCH fields are dense: one row per voxel in INTERNAL z-major order
+    j = (iz*ny + iy)*nx + ix, so a z-slab is a contiguous row range (the
+    multi-GPU shard unit).  `slots` maps the reference's x-major linear index to
+    these rows, exactly like the reference's own slots array.
+  * Matchability-masked fields keep the reference's occupied-row order and a
+    device copy of `slots`.
+  * quad: FP64 rows (n_v, 21 packed upper triangle) or (n_v,);
+    GP: pre-kinv sums S = sum_i vs_i (x) I_i, FP64 master plus the FP32 copy the
+    query kernel streams; queries form omega = kinv v^r in FP64.
+  `factors` materialises the reference layout (kernels.py:18-20; GP: kinv @ S)
+  on demand.
+"""
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .errors import BadMagic, EmptyGrid, OutOfField, TruncatedFile, VersionMismatch, WrongFactorKind
+from .fim import DEFAULT_SIGMA
+from .geometry import Pose
+from .visibility import GpVisibility, QuadraticVisibility, SeKernelParams, gp_build, model_from_reference
+
+MAGIC = b"FIF1"
+FORMAT_VERSION = 1
+_FACTOR_CODES = {"info": 0, "trace": 1}
+_FACTOR_NAMES = {v: k for k, v in _FACTOR_CODES.items()}
+_MODEL_QUAD, _MODEL_GP = 1, 2
+_MODES = ("nearest", "trilinear")
+_PACK_R = np.array([0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5])
+_PACK_C = np.array([0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5])
+_PACK36 = _PACK_R * 6 + _PACK_C  # flat 6x6 position of each packed entry
+
+
+@dataclass(frozen=True)
+class GridConfig:
+    """Axis-aligned voxel grid: min corner, voxel edge, voxel counts (field.py:45-98)."""
+
+    origin: np.ndarray
+    voxel_size: float
+    dims: np.ndarray
+
+    def __post_init__(self) -> None:
+        origin = np.asarray(self.origin, dtype=np.float64).reshape(3).copy()
+        dims = np.asarray(self.dims, dtype=np.int64).reshape(3).copy()
+        if self.voxel_size <= 0:
+            raise ValueError("voxel_size must be positive")
+        if (dims < 1).any():
+            raise EmptyGrid(f"dims {dims.tolist()} contain an empty axis")
+        origin.flags.writeable = False
+        dims.flags.writeable = False
+        object.__setattr__(self, "origin", origin)
+        object.__setattr__(self, "dims", dims)
+        object.__setattr__(self, "voxel_size", float(self.voxel_size))
+
+    @property
+    def voxel_count(self) -> int:
+        return int(np.prod(self.dims))
+
+    @property
+    def extent(self) -> np.ndarray:
+        return self.dims * self.voxel_size
+
+    def centers(self) -> np.ndarray:
+        """(V,3) centres in the reference's x-major / z-minor order."""
+        nx, ny, nz = (int(d) for d in self.dims)
+        ix, iy, iz = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+        idx = np.stack([ix, iy, iz], axis=-1).reshape(-1, 3)
+        return self.origin + (idx + 0.5) * self.voxel_size
+
+    def linear_index(self, index3) -> np.ndarray:
+        i = np.asarray(index3, dtype=np.int64)
+        return (i[..., 0] * self.dims[1] + i[..., 1]) * self.dims[2] + i[..., 2]
+
+    def index3_of(self, linear) -> np.ndarray:
+        lin = np.asarray(linear, dtype=np.int64)
+        iz = lin % self.dims[2]
+        rest = lin // self.dims[2]
+        return np.stack([rest // self.dims[1], rest % self.dims[1], iz], axis=-1)
+
+    def internal_index(self, index3) -> np.ndarray:
+        """Row of a voxel in the dense z-major device layout."""
+        i = np.asarray(index3, dtype=np.int64)
+        return (i[..., 2] * self.dims[1] + i[..., 1]) * self.dims[0] + i[..., 0]
+
+    def index3_of_internal(self, j) -> np.ndarray:
+        j = np.asarray(j, dtype=np.int64)
+        ix = j % self.dims[0]
+        rest = j // self.dims[0]
+        return np.stack([ix, rest % self.dims[1], rest // self.dims[1]], axis=-1)
+
+    def contains(self, position) -> bool:
+        g = (np.asarray(position, dtype=np.float64) - self.origin) / self.voxel_size
+        return bool((g >= 0).all() and (g < self.dims).all())
+
+    def center_of(self, index3) -> np.ndarray:
+        return self.origin + (np.asarray(index3, dtype=np.float64) + 0.5) * self.voxel_size
+
+
+def _grid_of(cfg) -> GridConfig:
+    if isinstance(cfg, GridConfig):
+        return cfg
+    return GridConfig(np.asarray(cfg.origin), float(cfg.voxel_size), np.asarray(cfg.dims))
+
+
+@dataclass(frozen=True)
+class Matchability:
+    """Which landmarks contribute to a voxel (field.py:101-180).  The default
+    accepts every pair; the gates are evaluated on the host in FP64 with the
+    reference's arithmetic, the resulting mask is applied inside the kernels."""
+
+    d_near: float | None = None
+    d_far: float | None = None
+    view_cone_beta: float | None = None
+    occluders: object | None = None
+    predicate: object | None = None
+
+    @property
+    def is_trivial(self) -> bool:
+        return all(x is None for x in (self.d_near, self.d_far, self.view_cone_beta, self.occluders, self.predicate))
+
+    def describe(self) -> str:
+        if self.is_trivial:
+            return "always"
+        parts = []
+        if self.d_near is not None or self.d_far is not None:
+            parts.append(f"range[{self.d_near},{self.d_far}]")
+        if self.view_cone_beta is not None:
+            parts.append(f"viewcone[{self.view_cone_beta:.4f}]")
+        if self.occluders is not None:
+            parts.append("occlusion")
+        if self.predicate is not None:
+            parts.append("custom")
+        return "+".join(parts)
+
+    def mask(self, centers, points, view_dirs=None):
+        if self.is_trivial:
+            return None
+        d = points[None, :, :] - centers[:, None, :]
+        dist = np.linalg.norm(d, axis=2)
+        ok = np.ones(dist.shape, dtype=bool)
+        if self.d_near is not None:
+            ok &= dist >= self.d_near
+        if self.d_far is not None:
+            ok &= dist <= self.d_far
+        if self.view_cone_beta is not None:
+            if view_dirs is None:
+                raise ValueError("view_cone_beta requires landmark view directions")
+            cosang = np.einsum("vnk,nk->vn", d / np.maximum(dist, 1e-12)[..., None], view_dirs)
+            ok &= cosang >= np.cos(self.view_cone_beta)
+        if self.occluders is not None:
+            blocked_fn = getattr(self.occluders, "segment_blocked", None)
+            if blocked_fn is None:
+                raise TypeError("occluders must provide segment_blocked(center, points) -> bool array")
+            for v in range(centers.shape[0]):
+                ok[v] &= ~np.asarray(blocked_fn(centers[v], points), dtype=bool)
+        if self.predicate is not None:
+            for v in range(centers.shape[0]):
+                for n in range(points.shape[0]):
+                    if ok[v, n] and not self.predicate(centers[v], points[n]):
+                        ok[v, n] = False
+        return ok.astype(np.uint8)
+
+
+ALWAYS_MATCH = Matchability()
+
+
+def _as_points(landmarks):
+    """Scene, (N,3) array / tensor, or a single 3-vector -> (points, view_dirs)."""
+    view_dirs = getattr(landmarks, "view_dirs", None)
+    positions = getattr(landmarks, "positions", landmarks)
+    if isinstance(positions, torch.Tensor):
+        pts = positions.to(torch.float64).reshape(-1, 3).contiguous()
+    else:
+        pts = np.ascontiguousarray(np.asarray(positions, dtype=np.float64).reshape(-1, 3))
+    if view_dirs is not None:
+        view_dirs = np.ascontiguousarray(np.asarray(view_dirs, dtype=np.float64).reshape(-1, 3))
+    return pts, view_dirs
+
+
+class _DeviceModel:
+    """ctypes fif_model with device copies of zs / kinv (kept alive here)."""
+
+    def __init__(self, model, device: torch.device):
+        self.model = model
+        m = _lib.Model()
+        self._keep = []
+        if isinstance(model, QuadraticVisibility):
+            m.kind, m.n_v = _lib.MODEL_QUAD, 10
+            m.k2, m.k1, m.k0 = model.k2, model.k1, model.k0
+        else:
+            m.kind, m.n_v = _lib.MODEL_GP, model.n_v
+            m.k_s, m.cos_alpha = model.k_s, float(np.cos(model.alpha))
+            m.sig2, m.ell = model.params.sigma2, model.params.length_scale
+            zs = torch.from_numpy(np.ascontiguousarray(model.samples)).to(device)
+            kinv = torch.from_numpy(np.ascontiguousarray(model.kinv)).to(device)
+            self._keep += [zs, kinv]
+            m.zs, m.kinv = zs.data_ptr(), kinv.data_ptr()
+        self.c = m
+
+
+def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, device: torch.device, grid=None,
+               centers: torch.Tensor | None = None, v_begin: int = 0, v_end: int | None = None,
+               mask: torch.Tensor | None = None, dmodel: _DeviceModel | None = None, f32_copy: bool = True):
+    """One fif_build launch: rows [v_begin, v_end) of the z-major grid (or of `centers`).
+    Returns (f64 rows (R, width_packed), f32 copy or None)."""
+    dm = dmodel or _DeviceModel(model, device)
+    n_v = 10 if isinstance(model, QuadraticVisibility) else model.n_v
+    width = n_v if want_trace else n_v * 21
+    if v_end is None:
+        v_end = centers.shape[0] if centers is not None else int(np.prod(grid.dims))
+    rows = v_end - v_begin
+    out64 = torch.empty((rows, width), dtype=torch.float64, device=device)
+    gp = isinstance(model, GpVisibility)
+    out32 = torch.empty((rows, width), dtype=torch.float32, device=device) if (gp and f32_copy) else None
+    n = points.shape[0]
+    scratch = torch.empty(int(_lib.load().fif_build_scratch_bytes(n)), dtype=torch.uint8, device=device)
+    g = _lib.make_grid(grid.origin, grid.voxel_size, grid.dims) if grid is not None else None
+    kind = _lib.KIND_TRACE if want_trace else _lib.KIND_INFO
+    st = _lib.load().fif_build(kind, dm.c, _lib.ptr(points), n, g, _lib.ptr(centers), v_begin, v_end, _lib.ptr(mask),
+                               float(sigma), _lib.ptr(scratch), _lib.ptr(out64), _lib.ptr(out32),
+                               _device.stream_handle(device))
+    _lib.check(st, "fif_build")
+    return out64, out32
+
+
+class Field:
+    """Voxel map of positional factors for one visibility model (field.py:193-614)."""
+
+    def __init__(self, config: GridConfig, model, factor_kind: str, sigma: float, store64: torch.Tensor,
+                 store32: torch.Tensor | None = None, occupied_index3: np.ndarray | None = None,
+                 matchability: Matchability = ALWAYS_MATCH, dense: bool = True):
+        if factor_kind not in _FACTOR_CODES:
+            raise ValueError(f"factor_kind must be one of {tuple(_FACTOR_CODES)}")
+        self.config = _grid_of(config)
+        self.model = model_from_reference(model)
+        self.factor_kind = factor_kind
+        self.sigma = float(sigma)
+        self.matchability = matchability
+        self.device = store64.device
+        self._s64 = store64
+        self._s32 = store32
+        self._dense = dense
+        self._is_info = factor_kind == "info"
+        self._dm = _DeviceModel(self.model, self.device)
+        self._grid_c = _lib.make_grid(self.config.origin, self.config.voxel_size, self.config.dims)
+        self._ref_cache = None
+        if dense:
+            self._occ3 = None
+            self._slots_np = None
+            self._slots_dev = None
+        else:
+            self._occ3 = np.ascontiguousarray(occupied_index3, dtype=np.int32).reshape(-1, 3)
+            slots = np.full(self.config.voxel_count, -1, dtype=np.int32)
+            if self._occ3.shape[0]:
+                slots[self.config.linear_index(self._occ3)] = np.arange(self._occ3.shape[0], dtype=np.int32)
+            self._slots_np = slots
+            self._slots_dev = torch.from_numpy(slots).to(self.device)
+
+    # ── attributes of the reference Field ───────────────────────────
+    @property
+    def row_width(self) -> int:
+        return self.model.n_v * (36 if self._is_info else 1)
+
+    @property
+    def rows(self) -> int:
+        return int(self._s64.shape[0])
+
+    @property
+    def slots(self) -> np.ndarray:
+        if self._slots_np is None:
+            cfg = self.config
+            lin = np.arange(cfg.voxel_count, dtype=np.int64)
+            self._slots_np = cfg.internal_index(cfg.index3_of(lin)).astype(np.int32)
+        return self._slots_np
+
+    @property
+    def occupied_index3(self) -> np.ndarray:
+        if self._occ3 is None:
+            self._occ3 = self.config.index3_of_internal(np.arange(self.rows)).astype(np.int32)
+        return self._occ3
+
+    @property
+    def factors(self) -> np.ndarray:
+        """Reference-layout FP64 rows (rows ordered as `occupied_index3`)."""
+        if self._ref_cache is None:
+            self._ref_cache = _device.to_numpy(self.export_reference())
+        return self._ref_cache
+
+    def export_reference(self, rows: torch.Tensor | np.ndarray | None = None) -> torch.Tensor:
+        """Device tensor of reference-layout rows (all, or the given row indices)."""
+        src = self._s64 if rows is None else self._s64[torch.as_tensor(rows, device=self.device, dtype=torch.long)]
+        src = src.contiguous()
+        out = torch.empty((src.shape[0], self.row_width), dtype=torch.float64, device=self.device)
+        kind = _lib.KIND_INFO if self._is_info else _lib.KIND_TRACE
+        _lib.check(_lib.load().fif_export_reference(kind, self._dm.c, _lib.ptr(src), src.shape[0], _lib.ptr(out),
+                                                    _device.stream_handle(self.device)), "fif_export_reference")
+        return out
+
+    @property
+    def storage(self) -> dict:
+        return {"f64": self._s64, "f32": self._s32}
+
+    # ── construction ────────────────────────────────────────────────
+    @staticmethod
+    def build(landmarks, config, model, factor_kind: str = "info", matchability: Matchability = ALWAYS_MATCH,
+              sigma: float = DEFAULT_SIGMA, parallel: bool = False, device=None) -> "Field":
+        """Build every voxel's factor on the GPU.  `parallel` is accepted for API
+        compatibility (the GPU build is always parallel)."""
+        config = _grid_of(config)
+        if config.voxel_count == 0:
+            raise EmptyGrid("grid has zero voxels")
+        if factor_kind not in _FACTOR_CODES:
+            raise ValueError(f"factor_kind must be one of {tuple(_FACTOR_CODES)}")
+        model = model_from_reference(model)
+        dev = _device.require_cuda(device)
+        points, view_dirs = _as_points(landmarks)
+        want_trace = factor_kind == "trace"
+        n_v = model.n_v
+        width = n_v if want_trace else n_v * 21
+        gp = isinstance(model, GpVisibility)
+        if points.shape[0] == 0:
+            empty64 = torch.zeros((0, width), dtype=torch.float64, device=dev)
+            return Field(config, model, factor_kind, sigma, empty64, empty64.float() if gp else None,
+                         np.zeros((0, 3), np.int32), matchability, dense=False)
+        pts_dev = _device.to_device_f64(points, dev, (3,))
+        if matchability.is_trivial:
+            s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, grid=config)
+            return Field(config, model, factor_kind, sigma, s64, s32, None, matchability, dense=True)
+        pts_np = points.cpu().numpy() if isinstance(points, torch.Tensor) else points
+        centers = config.centers()
+        mask = matchability.mask(centers, pts_np, view_dirs)
+        occupied = mask.any(axis=1)
+        lin = np.nonzero(occupied)[0]
+        sub_c = torch.from_numpy(np.ascontiguousarray(centers[occupied])).to(dev)
+        sub_m = torch.from_numpy(np.ascontiguousarray(mask[occupied])).to(dev)
+        if lin.size:
+            s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, centers=sub_c, mask=sub_m)
+        else:
+            s64 = torch.zeros((0, width), dtype=torch.float64, device=dev)
+            s32 = s64.float() if gp else None
+        return Field(config, model, factor_kind, sigma, s64, s32, config.index3_of(lin).astype(np.int32),
+                     matchability, dense=False)
+
+    # ── queries ─────────────────────────────────────────────────────
+    def _check_mode(self, mode: str) -> bool:
+        if mode not in _MODES:
+            raise ValueError(f"mode must be one of {_MODES}")
+        return mode == "trilinear"
+
+    def _field_ptr(self, use_f64: bool):
+        if isinstance(self.model, QuadraticVisibility) or use_f64 or self._s32 is None:
+            return self._s64, True
+        return self._s32, False
+
+    def query_device(self, positions: torch.Tensor, axes: torch.Tensor, mode: str = "trilinear",
+                     trace: bool = True, full: bool = False, grad: bool = False, det: bool = False,
+                     lmin: bool = False, field_f64: bool = False, out: dict | None = None) -> dict:
+        """Device-resident batched query: (Q,3) positions and optical axes, float64 CUDA
+        tensors.  Returns a dict of device tensors (trace, trace_grad, fim (Q,36),
+        fim_grad (Q,6,36), det, lmin, status)."""
+        trilinear = self._check_mode(mode)
+        if (full or det or lmin) and not self._is_info:
+            raise WrongFactorKind("full FIM / det / lmin require an info-factor field")
+        q = positions.shape[0]
+        dev = self.device
+        out = {} if out is None else out
+
+        def buf(name, shape, dtype=torch.float64):
+            t = out.get(name)
+            if t is None or t.shape[0] != q:
+                t = torch.empty((q, *shape), dtype=dtype, device=dev)
+                out[name] = t
+            return t
+
+        flags = 0
+        tr_t = trg_t = fim_t = fimg_t = det_t = lmin_t = None
+        if trace:
+            flags |= _lib.Q_TRACE
+            tr_t = buf("trace", ())
+            if grad:
+                trg_t = buf("trace_grad", (6,))
+        if full:
+            flags |= _lib.Q_FULL
+            fim_t = buf("fim", (36,))
+            if grad:
+                fimg_t = buf("fim_grad", (6, 36))
+        if grad:
+            flags |= _lib.Q_GRAD
+        if det:
+            flags |= _lib.Q_DET
+            det_t = buf("det", ())
+        if lmin:
+            flags |= _lib.Q_LMIN
+            lmin_t = buf("lmin", ())
+        st_t = buf("status", (), torch.uint8)
+        field_t, is64 = self._field_ptr(field_f64)
+        if is64 and isinstance(self.model, GpVisibility):
+            flags |= _lib.Q_FIELD_F64
+        kind = _lib.KIND_INFO if self._is_info else _lib.KIND_TRACE
+        if self.rows == 0:
+            for t in (tr_t, trg_t, fim_t, fimg_t, det_t, lmin_t):
+                if t is not None:
+                    t.zero_()
+            # every voxel is empty: status still follows the grid geometry
+            dummy = torch.zeros((1, field_t.shape[1] if field_t.dim() == 2 else 1), dtype=field_t.dtype, device=dev)
+            field_t = dummy
+        slots = None if self._dense else self._slots_dev
+        if self.rows == 0:
+            slots = torch.full((self.config.voxel_count,), -1, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().fif_query(kind, self._dm.c, self._grid_c, _lib.ptr(field_t), _lib.ptr(slots),
+                                         _lib.ptr(positions), _lib.ptr(axes), q,
+                                         _lib.MODE_TRILINEAR if trilinear else _lib.MODE_NEAREST, flags,
+                                         _lib.ptr(tr_t), _lib.ptr(trg_t), _lib.ptr(fim_t), _lib.ptr(fimg_t),
+                                         _lib.ptr(det_t), _lib.ptr(lmin_t), _lib.ptr(st_t),
+                                         _device.stream_handle(dev)), "fif_query")
+        return out
+
+    def query_batch(self, positions, rotations=None, axes=None, outputs=("trace", "full"), grad: bool = False,
+                    mode: str = "trilinear", to_numpy: bool = False) -> dict:
+        """Batched query with optional analytic pose gradients (new in this build).
+
+        outputs subset of {"trace", "full", "det", "lmin"}.  Gradients are d/d[t; theta]
+        for t' = t + dt, R' = exp(dtheta^) R; shapes: trace_grad (Q,6), fim_grad (Q,6,6,6).
+        """
+        dev = self.device
+        pos = _device.to_device_f64(positions, dev, (3,))
+        if axes is None:
+            if rotations is None:
+                raise ValueError("pass rotations (Q,3,3) or axes (Q,3)")
+            r = _device.to_device_f64(rotations, dev, (3, 3))
+            ax = r[:, :, 2].contiguous()
+        else:
+            ax = _device.to_device_f64(axes, dev, (3,))
+        outs = set(outputs)
+        res = self.query_device(pos, ax, mode, trace="trace" in outs, full="full" in outs, grad=grad,
+                                det="det" in outs, lmin="lmin" in outs)
+        q = pos.shape[0]
+        ret = {"in_field": res["status"] == 0}
+        for k in ("trace", "trace_grad", "det", "lmin"):
+            if k in res:
+                ret[k] = res[k]
+        if "fim" in res:
+            ret["fim"] = res["fim"].view(q, 6, 6)
+        if "fim_grad" in res:
+            ret["fim_grad"] = res["fim_grad"].view(q, 6, 6, 6)
+        if to_numpy:
+            ret = {k: _device.to_numpy(v) for k, v in ret.items()}
+        return ret
+
+    def query_fim_batch(self, positions, rotations, mode: str = "nearest"):
+        """(fims (Q,6,6), in_field (Q,)) — zeros outside coverage (field.py:345-379)."""
+        if not self._is_info:
+            raise WrongFactorKind("FIM query requires an info-factor field")
+        self._check_mode(mode)
+        r = self.query_batch(positions, rotations=rotations, outputs=("full",), mode=mode, to_numpy=True)
+        return r["fim"], r["in_field"]
+
+    def query_fim(self, pose: Pose, mode: str = "nearest") -> np.ndarray:
+        if not self._is_info:
+            raise WrongFactorKind("FIM query requires an info-factor field")
+        self._check_mode(mode)
+        fims, ok = self.query_fim_batch(pose.translation[None], pose.rotation[None], mode)
+        if not ok[0]:
+            raise OutOfField(f"position {pose.translation.tolist()} outside field coverage")
+        return fims[0]
+
+    def metric_axis_batch(self, positions, axes, metric: str = "det", mode: str = "nearest"):
+        """(values, in_field) at (position, optical axis) pairs (field.py:418-457)."""
+        if metric not in ("det", "lmin", "trace"):
+            raise ValueError(f"unknown metric {metric!r}")
+        if not self._is_info and metric != "trace":
+            raise WrongFactorKind("det/lmin require an info-factor field")
+        self._check_mode(mode)
+        r = self.query_batch(positions, axes=axes, outputs=(metric,), mode=mode, to_numpy=True)
+        return r[metric], r["in_field"]
+
+    def query_metric(self, pose: Pose, metric: str = "det", mode: str = "nearest") -> float:
+        if metric not in ("det", "lmin", "trace"):
+            raise ValueError(f"unknown metric {metric!r}")
+        if not self._is_info and metric != "trace":
+            raise WrongFactorKind("det/lmin require an info-factor field")
+        self._check_mode(mode)
+        vals, ok = self.metric_axis_batch(pose.translation[None], pose.rotation[:, 2][None], metric, mode)
+        if not ok[0]:
+            raise OutOfField(f"position {pose.translation.tolist()} outside field coverage")
+        return float(vals[0])
+
+    def query_factor(self, position, mode: str = "nearest") -> np.ndarray:
+        """Raw (blended) reference-layout factor at a position (field.py:277-303)."""
+        trilinear = self._check_mode(mode)
+        cfg = self.config
+        pos = np.asarray(position, dtype=np.float64)
+        if trilinear:
+            g = (pos - cfg.origin) / cfg.voxel_size - 0.5
+            base = np.floor(g).astype(np.int64)
+            f = g - base
+            for a in range(3):
+                if base[a] + 1 == cfg.dims[a] and f[a] == 0.0:
+                    base[a] -= 1
+                    f[a] = 1.0
+            if (base < 0).any() or (base + 1 > cfg.dims - 1).any():
+                raise OutOfField(f"position {pos.tolist()} lacks 8 interpolation neighbors")
+            corners, wts = [], []
+            for dx in (0, 1):
+                for dy in (0, 1):
+                    for dz in (0, 1):
+                        corners.append(cfg.linear_index(base + np.array([dx, dy, dz])))
+                        wts.append((f[0] if dx else 1 - f[0]) * (f[1] if dy else 1 - f[1]) * (f[2] if dz else 1 - f[2]))
+        else:
+            i3 = np.floor((pos - cfg.origin) / cfg.voxel_size).astype(np.int64)
+            if (i3 < 0).any() or (i3 >= cfg.dims).any():
+                raise OutOfField(f"position {pos.tolist()} outside grid")
+            corners, wts = [cfg.linear_index(i3)], [1.0]
+        rows = self.slots[np.array(corners)]
+        out = np.zeros(self.row_width)
+        valid = rows >= 0
+        if valid.any():
+            ref = _device.to_numpy(self.export_reference(rows[valid]))
+            for w, row in zip(np.array(wts)[valid], ref):
+                if w != 0.0:
+                    out += w * row
+        return out.reshape(self.model.n_v, 6, 6) if self._is_info else out
+
+    # ── incremental updates (field.py:461-505) ──────────────────────
+    def _increment(self, points, view_dirs, sign: float) -> None:
+        pts, vd = _as_points(points)
+        if pts.shape[0] == 0:
+            return
+        dev = self.device
+        pts_dev = _device.to_device_f64(pts, dev, (3,))
+        want_trace = not self._is_info
+        if self.matchability.is_trivial and self._dense:
+            inc, _ = build_rows(pts_dev, self.model, want_trace, self.sigma, dev, grid=self.config,
+                                dmodel=self._dm, f32_copy=False)
+            self._s64.add_(inc, alpha=sign)
+        else:
+            pts_np = pts.cpu().numpy() if isinstance(pts, torch.Tensor) else pts
+            centers = self.config.centers()
+            mask = self.matchability.mask(centers, pts_np, vd if vd is not None else view_dirs)
+            touched = np.ones(self.config.voxel_count, bool) if mask is None else mask.any(axis=1)
+            if not touched.any():
+                return
+            lin = np.nonzero(touched)[0]
+            sub_c = torch.from_numpy(np.ascontiguousarray(centers[touched])).to(dev)
+            sub_m = None if mask is None else torch.from_numpy(np.ascontiguousarray(mask[touched])).to(dev)
+            inc, _ = build_rows(pts_dev, self.model, want_trace, self.sigma, dev, centers=sub_c, mask=sub_m,
+                                dmodel=self._dm, f32_copy=False)
+            if self._dense:
+                rows = self.slots[lin]
+            else:
+                rows = self._slots_np[lin]
+                missing = rows < 0
+                if missing.any():
+                    start = self.rows
+                    new_lin = lin[missing]
+                    self._slots_np[new_lin] = np.arange(start, start + new_lin.size, dtype=np.int32)
+                    self._slots_dev = torch.from_numpy(self._slots_np).to(dev)
+                    self._s64 = torch.cat([self._s64, torch.zeros((new_lin.size, self._s64.shape[1]),
+                                                                  dtype=torch.float64, device=dev)])
+                    self._occ3 = np.vstack([self._occ3, self.config.index3_of(new_lin).astype(np.int32)])
+                    rows = self._slots_np[lin]
+            idx = torch.as_tensor(rows.astype(np.int64), device=dev)
+            self._s64.index_add_(0, idx, inc, alpha=sign)
+        if self._s32 is not None:
+            self._s32 = self._s64.float()
+        self._ref_cache = None
+
+    def add_landmarks(self, landmarks, view_dirs=None) -> None:
+        self._increment(landmarks, view_dirs, +1.0)
+
+    def remove_landmarks(self, landmarks, view_dirs=None) -> None:
+        self._increment(landmarks, view_dirs, -1.0)
+
+    add_landmark = add_landmarks
+    remove_landmark = remove_landmarks
+
+    def update_landmark(self, old, new) -> None:
+        self.remove_landmarks(old)
+        self.add_landmarks(new)
+
+    # ── accounting and serialization (field.py:509-614) ─────────────
+    def memory_stats(self) -> dict:
+        scalars = self.row_width
+        rows = self.rows
+        bytes_factors = rows * scalars * 8
+        bytes_index = self.config.voxel_count * 4 + rows * 12
+        dev_bytes = self._s64.numel() * 8 + (self._s32.numel() * 4 if self._s32 is not None else 0)
+        return {
+            "voxel_count": rows, "grid_voxels": self.config.voxel_count, "n_v": self.model.n_v,
+            "scalars_per_voxel": scalars, "bytes_factors": bytes_factors, "bytes_factors_float32": rows * scalars * 4,
+            "bytes_index": bytes_index, "bytes_total": bytes_factors + bytes_index, "device_bytes": dev_bytes,
+        }
+
+    def serialize(self, path) -> None:
+        """FIF1 file, readable by the reference's Field.deserialize."""
+        m = self.model
+        head = bytearray(MAGIC)
+        head += struct.pack("<I", FORMAT_VERSION)
+        head += struct.pack("<B", _FACTOR_CODES[self.factor_kind])
+        if isinstance(m, QuadraticVisibility):
+            head += struct.pack("<B", _MODEL_QUAD) + struct.pack("<d", m.alpha) + struct.pack("<3d", m.k2, m.k1, m.k0)
+        else:
+            head += struct.pack("<B", _MODEL_GP) + struct.pack("<d", m.alpha) + struct.pack("<I", m.n_v)
+            head += np.ascontiguousarray(m.samples, dtype="<f8").tobytes()
+            head += struct.pack("<4d", m.params.sigma2, m.params.length_scale, m.params.jitter, m.k_s)
+        head += struct.pack("<d", self.sigma)
+        head += np.ascontiguousarray(self.config.origin, dtype="<f8").tobytes()
+        head += struct.pack("<d", self.config.voxel_size)
+        head += struct.pack("<3I", *(int(d) for d in self.config.dims))
+        head += struct.pack("<Q", self.rows)
+        occ = self.occupied_index3
+        order = np.argsort(self.config.linear_index(occ), kind="stable")
+        fac = self.factors
+        rec = np.empty(self.rows, dtype=np.dtype([("i", "<i4", (3,)), ("f", "<f8", (self.row_width,))]))
+        rec["i"] = occ[order]
+        rec["f"] = fac[order]
+        with open(path, "wb") as f:
+            f.write(bytes(head))
+            f.write(rec.tobytes())
+
+    @staticmethod
+    def deserialize(path, expect_kind: str | None = None, device=None) -> "Field":
+        with open(path, "rb") as f:
+            data = f.read()
+        off = 0
+
+        def take(n: int) -> bytes:
+            nonlocal off
+            if off + n > len(data):
+                raise TruncatedFile(f"needed {n} bytes at offset {off}, file has {len(data)}")
+            chunk = data[off:off + n]
+            off += n
+            return chunk
+
+        if take(4) != MAGIC:
+            raise BadMagic("not a field file (bad magic)")
+        (version,) = struct.unpack("<I", take(4))
+        if version != FORMAT_VERSION:
+            raise VersionMismatch(f"file version {version}, supported {FORMAT_VERSION}")
+        (kind_code,) = struct.unpack("<B", take(1))
+        if kind_code not in _FACTOR_NAMES:
+            raise TruncatedFile(f"unknown factor kind code {kind_code}")
+        factor_kind = _FACTOR_NAMES[kind_code]
+        if expect_kind is not None and factor_kind != expect_kind:
+            raise WrongFactorKind(f"file holds {factor_kind} factors, expected {expect_kind}")
+        (model_code,) = struct.unpack("<B", take(1))
+        if model_code == _MODEL_QUAD:
+            (alpha,) = struct.unpack("<d", take(8))
+            model = QuadraticVisibility(alpha, *struct.unpack("<3d", take(24)))
+        elif model_code == _MODEL_GP:
+            (alpha,) = struct.unpack("<d", take(8))
+            (n_s,) = struct.unpack("<I", take(4))
+            samples = np.frombuffer(take(24 * n_s), dtype="<f8").reshape(n_s, 3).copy()
+            sigma2, ell, jitter, k_s = struct.unpack("<4d", take(32))
+            model = gp_build(samples, SeKernelParams(sigma2, ell, jitter), alpha, k_s)  # kinv recomputed
+        else:
+            raise TruncatedFile(f"unknown model kind code {model_code}")
+        (sigma,) = struct.unpack("<d", take(8))
+        origin = np.frombuffer(take(24), dtype="<f8").copy()
+        (voxel_size,) = struct.unpack("<d", take(8))
+        dims = struct.unpack("<3I", take(12))
+        (rows,) = struct.unpack("<Q", take(8))
+        config = GridConfig(origin, voxel_size, np.asarray(dims, dtype=np.int64))
+        width = model.n_v * (36 if factor_kind == "info" else 1)
+        rec_t = np.dtype([("i", "<i4", (3,)), ("f", "<f8", (width,))])
+        rec = np.frombuffer(take(rows * rec_t.itemsize), dtype=rec_t)
+        occ3 = np.ascontiguousarray(rec["i"], dtype=np.int32)
+        factors = np.ascontiguousarray(rec["f"], dtype=np.float64)
+        if rows and ((occ3 < 0).any() or (occ3 >= np.asarray(dims)).any()):
+            raise TruncatedFile("voxel index outside grid")
+        dev = _device.require_cuda(device)
+        s64 = _device.to_device_f64(_from_reference_rows(factors, model, factor_kind), dev)
+        s64 = s64.reshape(rows, -1)
+        s32 = s64.float() if isinstance(model, GpVisibility) else None
+        fld = Field(config, model, factor_kind, sigma, s64, s32, occ3, ALWAYS_MATCH, dense=False)
+        fld._ref_cache = factors  # bitwise round trip of the stored reference rows
+        return fld
+
+
+def _from_reference_rows(factors: np.ndarray, model, factor_kind: str) -> np.ndarray:
+    """Reference-layout rows -> device storage layout (packed; GP: S = K F)."""
+    n_v = model.n_v
+    rows = factors.shape[0]
+    if factor_kind == "info":
+        packed = factors.reshape(rows, n_v, 36)[:, :, _PACK36]
+    else:
+        packed = factors.reshape(rows, n_v, 1)
+    if isinstance(model, GpVisibility):
+        from .visibility import _gram
+
+        packed = np.einsum("gk,rkw->rgw", _gram(model.samples, model.params), packed)
+    return np.ascontiguousarray(packed.reshape(rows, -1))
+
+
+def build(landmarks, config, model, factor_kind="info", matchability=ALWAYS_MATCH, sigma=DEFAULT_SIGMA,
+          parallel=False, device=None) -> Field:
+    """Module-level alias for Field.build (field.py:645-648)."""
+    return Field.build(landmarks, config, model, factor_kind, matchability, sigma, parallel, device)

@@ -1,0 +1,52 @@
+"""First GPU exercise: every kernel once against the oracle on the golden small field."""
+import sys, os, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2008_03324_b200 as F
+from paper_2008_03324_b200 import field as FD, _lib
+from oracle import oracle as O
+
+g = np.load('tests/golden/small_field.npz'); m = np.load('tests/golden/models.npz')
+pts = g['points']; grid = F.GridConfig(g['origin'], g['voxel_size'][0], g['dims'])
+quad = F.build_quad_model()
+gps = {ns: F.GpVisibility(m[f'gp{ns}_zs'], F.SeKernelParams(m[f'gp{ns}_par'][2], m[f'gp{ns}_par'][3], m[f'gp{ns}_par'][4]), m[f'gp{ns}_par'][0], m[f'gp{ns}_par'][1], m[f'gp{ns}_kinv']) for ns in (30, 70)}
+models = {'quad': quad, 'gp30': gps[30], 'gp70': gps[70]}
+pos, rots = g['positions'], g['rotations']
+for mname, model in models.items():
+    for kind in ('trace', 'info'):
+        t0 = time.time()
+        f = F.Field.build(pts, grid, model, kind)
+        torch.cuda.synchronize()
+        ref = g[f'factors_{mname}_{kind}']
+        # reorder: our rows follow occupied_index3 (z-major); reference rows are x-major
+        lin = grid.linear_index(f.occupied_index3)
+        mine = f.factors[np.argsort(lin)]
+        if kind == 'trace':
+            err = (np.linalg.norm(mine - ref, axis=1) / np.linalg.norm(ref, axis=1)).max()
+        else:
+            err = max(np.abs(mine[i] - ref[i]).max() / np.linalg.norm(ref[i]) for i in range(ref.shape[0]))
+        line = f'{mname:5s} {kind:5s} build err {err:.3e} ({time.time()-t0:.2f}s)'
+        for mode in ('nearest', 'trilinear'):
+            vals, ok = f.metric_axis_batch(pos, rots[:, :, 2], 'trace', mode)
+            rv = g[f'trace_{mname}_{kind}_{mode}']; rok = g[f'ok_{mname}_{kind}_{mode}']
+            rel = np.abs(vals - rv)[rok] / np.abs(rv[rok])
+            line += f' | {mode} status_eq {np.array_equal(ok, rok)} trace rel {rel.max():.2e}'
+            if kind == 'info':
+                fims, ok2 = f.query_fim_batch(pos, rots, mode)
+                rf = g[f'fim_{mname}_{mode}']
+                e2 = max(np.linalg.norm(fims[i] - rf[i]) / max(np.linalg.norm(rf[i]), 1e-300) for i in np.nonzero(rok)[0])
+                line += f' fim relF {e2:.2e}'
+                for met in ('det', 'lmin'):
+                    mv, _ = f.metric_axis_batch(pos, rots[:, :, 2], met, mode)
+                    rm = g[f'{met}_{mname}_{mode}']
+                    line += f' {met} {np.abs(mv - rm)[rok].max() / np.abs(rm[rok]).max():.1e}'
+        print(line, flush=True)
+pc = np.load('tests/golden/pc.npz')
+cam = F.PinholeCamera.from_fov()
+out = F.exact_pose_fim_batch(pc['rotations'], pc['translations'], pc['points'], cam)
+e = max(np.linalg.norm(out[i] - pc['fims'][i]) / np.linalg.norm(pc['fims'][i]) for i in range(out.shape[0]))
+dev = torch.device('cuda')
+mask = torch.zeros((48, pc['points'].shape[0]), dtype=torch.uint8, device=dev)
+F.exact_pose_fim_batch_device(torch.tensor(pc['rotations'], device=dev).reshape(-1, 9).contiguous(), torch.tensor(pc['translations'], device=dev), torch.tensor(pc['points'], device=dev), cam, mask=mask)
+print('pc relF', e, 'mask bit-exact', np.array_equal(mask.cpu().numpy().astype(bool), pc['visible_kernel']))
+print('launches', _lib.launch_count())
