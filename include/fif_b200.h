@@ -49,6 +49,8 @@ extern "C" {
 #define FIF_Q_DET 8u       /* det(I), blended per corner like kernels.py:1456-1468 (info only)   */
 #define FIF_Q_LMIN 16u     /* smallest eigenvalue, blended per corner (info only)                */
 #define FIF_Q_FIELD_F64 32u /* GP field operand is the FP64 S array instead of the FP32 copy     */
+/* fif_build flags */
+#define FIF_BUILD_EXACT 1u  /* quad: reproduce _nb_build_quad's FP64 operation order bit for bit     */
 
 /* Axis-aligned voxel grid (field.py:45-98 GridConfig). */
 typedef struct fif_grid {
@@ -100,11 +102,12 @@ int64_t fif_build_scratch_bytes(int64_t n_points);
  *   GP trace (rows,N_s) f64 S | GP info (rows,N_s,21) f64 S, where
  *   S = sum_i vs_i (x) I_i is the pre-kinv factor (reference factor = kinv @ S).
  * Optional d_out32: the same array in float32 (the query operand for GP).
- * d_scratch: fif_build_scratch_bytes(n_points) bytes.                        */
+ * d_scratch: fif_build_scratch_bytes(n_points) bytes.  build_flags:
+ * FIF_BUILD_EXACT (quad only) selects the bit-exact reference arithmetic.     */
 int fif_build(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
               const fif_grid* grid, const double* d_centers, int64_t v_begin, int64_t v_end,
-              const uint8_t* d_mask, double sigma, void* d_scratch, double* d_out64, float* d_out32,
-              void* stream);
+              const uint8_t* d_mask, double sigma, uint32_t build_flags, void* d_scratch, double* d_out64,
+              float* d_out32, void* stream);
 
 /* Reference-layout rows (kernels.py:18-20): quad info expands the packed
  * upper triangle to 36 per block; GP rows become kinv @ S (FP64); trace rows

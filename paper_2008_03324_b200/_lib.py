@@ -19,6 +19,7 @@ KIND_INFO, KIND_TRACE = 0, 1
 MODEL_QUAD, MODEL_GP = 1, 2
 MODE_NEAREST, MODE_TRILINEAR = 0, 1
 Q_TRACE, Q_FULL, Q_GRAD, Q_DET, Q_LMIN, Q_FIELD_F64 = 1, 2, 4, 8, 16, 32
+BUILD_EXACT = 1
 
 EXPORTED = (
     "fif_abi_version", "fif_last_error", "fif_grid_centers", "fif_build_scratch_bytes", "fif_build",
@@ -74,7 +75,7 @@ def load():
         L.fif_grid_centers.argtypes = [ctypes.POINTER(Grid), _int, _i64, _i64, _p, _p]
         L.fif_build.restype = _int
         L.fif_build.argtypes = [_int, ctypes.POINTER(Model), _p, _i64, ctypes.POINTER(Grid), _p, _i64, _i64, _p, _d,
-                                _p, _p, _p, _p]
+                                ctypes.c_uint32, _p, _p, _p, _p]
         L.fif_export_reference.restype = _int
         L.fif_export_reference.argtypes = [_int, ctypes.POINTER(Model), _p, _i64, _p, _p]
         L.fif_query.restype = _int

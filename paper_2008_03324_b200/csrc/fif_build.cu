@@ -73,59 +73,168 @@ __device__ __forceinline__ void voxel_split(const VoxSrc& src, int64_t v, float 
   split_f32(cz, ch[2], cl[2]);
 }
 
-// ─────────────────────────── quad, trace ───────────────────────────────
-// One thread per voxel; out (rows,10) f64: sum_i vp_i[k] * tr_i.
-constexpr int QT_THREADS = 128;
-constexpr int QT_TILE = 128;   // landmarks per smem tile
-constexpr int QT_FLUSH = 16;   // FP32 partial run length before the FP64 flush
+// ─────────────────────────── quad (FP64) ───────────────────────────────
+// Quad factors feed queries whose value can cancel to ~1e-3 of the factor
+// magnitude (nearest-landmark terms dominate sums weighted by 1/n^2), so the
+// per-pair arithmetic is FP64 (B200 FP64 = 1/2 FP32 rate, separate pipe).
+// EXACT=true reproduces _nb_build_quad's operation order bit for bit (IEEE sqrt
+// and division, no FMA, landmark-sequential sums); EXACT=false uses FMA and an
+// rsqrt+Newton reciprocal (~1e-16 relative, ~2x faster).
+// Landmark tile: double4 {px, py, pz, |p|^2}.
+constexpr int QD_THREADS = 128;
+constexpr int QD_TILE = 128;
 
-template <bool HAS_MASK>
-__global__ void __launch_bounds__(QT_THREADS) k_quad_trace(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real,
+__global__ void k_prep_landmarks64(const double* __restrict__ pts, int64_t n, int64_t n_pad, double4* __restrict__ tab) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  double4 a = make_double4(0.0, 0.0, 0.0, -1.0);  // pp < 0 marks padding
+  if (i < n) {
+    double px = pts[3 * i], py = pts[3 * i + 1], pz = pts[3 * i + 2];
+    a = make_double4(px, py, pz, __dadd_rn(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)), __dmul_rn(pz, pz)));
+  }
+  tab[i] = a;
+}
+
+__device__ __forceinline__ double rsqrt_nr(double n2) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(n2));
+  double h = n2 * r;
+  r = fma(0.5 * r, fma(-h, r, 1.0), r);
+  h = n2 * r;
+  r = fma(0.5 * r, fma(-h, r, 1.0), r);
+  return r;
+}
+
+struct PairD {
+  double ux, uy, uz, w;  // w = 0 when the pair is skipped
+};
+
+template <bool EXACT>
+__device__ __forceinline__ PairD pair64(double4 p, double cx, double cy, double cz, double inv_s2, bool keep) {
+  PairD q;
+  double dx = __dsub_rn(p.x, cx), dy = __dsub_rn(p.y, cy), dz = __dsub_rn(p.z, cz);
+  double n2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  keep = keep && p.w >= 0.0 && n2 >= 1e-300;  // kernels.py:444
+  if (!keep) {
+    q.ux = q.uy = q.uz = q.w = 0.0;
+    return q;
+  }
+  if (EXACT) {
+    double n = __dsqrt_rn(n2);
+    q.ux = __ddiv_rn(dx, n);
+    q.uy = __ddiv_rn(dy, n);
+    q.uz = __ddiv_rn(dz, n);
+    q.w = __ddiv_rn(inv_s2, n2);
+  } else {
+    double r = rsqrt_nr(n2);
+    q.ux = dx * r;
+    q.uy = dy * r;
+    q.uz = dz * r;
+    q.w = inv_s2 * r * r;
+  }
+  return q;
+}
+
+// Entries of the 6x6 block (kernels.py:385-423) in packed order, FP64.
+// EXACT: the reference's expressions with IEEE rounding of every operation.
+#define MUL(a, b) (EXACT ? __dmul_rn((a), (b)) : ((a) * (b)))
+#define ADD(a, b) (EXACT ? __dadd_rn((a), (b)) : ((a) + (b)))
+#define SUB(a, b) (EXACT ? __dsub_rn((a), (b)) : ((a) - (b)))
+template <bool EXACT>
+__device__ __forceinline__ void c2_of(const PairD& q, double4 p, double& c2x, double& c2y, double& c2z) {
+  c2x = SUB(MUL(p.y, q.uz), MUL(p.z, q.uy));
+  c2y = SUB(MUL(p.z, q.ux), MUL(p.x, q.uz));
+  c2z = SUB(MUL(p.x, q.uy), MUL(p.y, q.ux));
+}
+template <bool EXACT>
+__device__ __forceinline__ double entry64(int e, const PairD& q, double4 p, double c2x, double c2y, double c2z) {
+  const double w = q.w, nw = -q.w, ux = q.ux, uy = q.uy, uz = q.uz, px = p.x, py = p.y, pz = p.z, pp = p.w;
+  switch (e) {
+    case 0: return MUL(w, SUB(1.0, MUL(ux, ux)));
+    case 1: return MUL(w, MUL(-ux, uy));
+    case 2: return MUL(w, MUL(-ux, uz));
+    case 3: return MUL(nw, MUL(ux, c2x));
+    case 4: return MUL(nw, ADD(-pz, MUL(ux, c2y)));
+    case 5: return MUL(nw, ADD(py, MUL(ux, c2z)));
+    case 6: return MUL(w, SUB(1.0, MUL(uy, uy)));
+    case 7: return MUL(w, MUL(-uy, uz));
+    case 8: return MUL(nw, ADD(pz, MUL(uy, c2x)));
+    case 9: return MUL(nw, MUL(uy, c2y));
+    case 10: return MUL(nw, ADD(-px, MUL(uy, c2z)));
+    case 11: return MUL(w, SUB(1.0, MUL(uz, uz)));
+    case 12: return MUL(nw, ADD(-py, MUL(uz, c2x)));
+    case 13: return MUL(nw, ADD(px, MUL(uz, c2y)));
+    case 14: return MUL(nw, MUL(uz, c2z));
+    case 15: return MUL(w, SUB(SUB(pp, MUL(px, px)), MUL(c2x, c2x)));
+    case 16: return MUL(w, SUB(MUL(-px, py), MUL(c2x, c2y)));
+    case 17: return MUL(w, SUB(MUL(-px, pz), MUL(c2x, c2z)));
+    case 18: return MUL(w, SUB(SUB(pp, MUL(py, py)), MUL(c2y, c2y)));
+    case 19: return MUL(w, SUB(MUL(-py, pz), MUL(c2y, c2z)));
+    default: return MUL(w, SUB(ADD(MUL(-pz, pz), pp), MUL(c2z, c2z)));
+  }
+}
+
+// One thread per voxel; out (rows,10) f64 = sum_i vp_i[k] tr_i (kernels.py:459-461).
+template <bool EXACT, bool HAS_MASK>
+__global__ void __launch_bounds__(QD_THREADS) k_quad_trace(const double4* __restrict__ lm, int64_t n_pad, int64_t n_real,
                                                            VoxSrc src, int64_t v0, int64_t v1,
-                                                           const uint8_t* __restrict__ mask, float inv_s2,
+                                                           const uint8_t* __restrict__ mask, double inv_s2,
                                                            double* __restrict__ out) {
-  __shared__ float4 tile[QT_TILE * 2];
-  const int64_t v = v0 + blockIdx.x * (int64_t)QT_THREADS + threadIdx.x;
+  __shared__ double4 tile[QD_TILE];
+  const int64_t v = v0 + blockIdx.x * (int64_t)QD_THREADS + threadIdx.x;
   const bool active = v < v1;
-  float ch[3], cl[3];
-  voxel_split(src, active ? v : v0, ch, cl);
+  double cx, cy, cz;
+  voxel_center(src, active ? v : v0, cx, cy, cz);
   double acc[10];
 #pragma unroll
   for (int k = 0; k < 10; ++k) acc[k] = 0.0;
-  for (int64_t base = 0; base < n_pad; base += QT_TILE) {
+  for (int64_t base = 0; base < n_pad; base += QD_TILE) {
     __syncthreads();
-    for (int j = threadIdx.x; j < QT_TILE * 2; j += QT_THREADS) tile[j] = lm[2 * base + j];
+    for (int j = threadIdx.x; j < QD_TILE; j += QD_THREADS) tile[j] = lm[base + j];
     __syncthreads();
-#pragma unroll 1
-    for (int j0 = 0; j0 < QT_TILE; j0 += QT_FLUSH) {
-      float part[10];
-#pragma unroll
-      for (int k = 0; k < 10; ++k) part[k] = 0.f;
-#pragma unroll 4
-      for (int j = j0; j < j0 + QT_FLUSH; ++j) {
-        float4 a = tile[2 * j], b = tile[2 * j + 1];
-        if (HAS_MASK) {
-          int64_t i = base + j;
-          if (i < n_real && active && mask[(v - v0) * n_real + i] == 0) b.w = 0.f;
-        }
-        PairF q = pair_prologue(a, b, ch, cl, inv_s2);
-        // tr = w (2 + |p|^2 + (p.u)^2) = sum of the six diagonal entries (kernels.py:424)
-        float pu = fmaf(a.x, q.ux, fmaf(a.y, q.uy, a.z * q.uz));
-        float tr = q.w * fmaf(pu, pu, 2.0f + a.w);
-        float tx = tr * q.ux, ty = tr * q.uy, tz = tr * q.uz;
-        part[0] = fmaf(tx, q.ux, part[0]);
-        part[1] = fmaf(ty, q.uy, part[1]);
-        part[2] = fmaf(tz, q.uz, part[2]);
-        part[3] = fmaf(tx, q.uy, part[3]);
-        part[4] = fmaf(tx, q.uz, part[4]);
-        part[5] = fmaf(ty, q.uz, part[5]);
-        part[6] += tx;
-        part[7] += ty;
-        part[8] += tz;
-        part[9] += tr;
+#pragma unroll 2
+    for (int j = 0; j < QD_TILE; ++j) {
+      const double4 p = tile[j];
+      bool keep = active;
+      if (HAS_MASK) {
+        int64_t i = base + j;
+        keep = keep && i < n_real && mask[(v - v0) * n_real + i] != 0;
       }
+      const PairD q = pair64<EXACT>(p, cx, cy, cz, inv_s2, keep);
+      double tr;
+      if (EXACT) {
+        double c2x, c2y, c2z;
+        c2_of<true>(q, p, c2x, c2y, c2z);
+        // out[0] + out[7] + out[14] + out[21] + out[28] + out[35]  (kernels.py:424)
+        tr = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(entry64<true>(0, q, p, c2x, c2y, c2z),
+                                                                entry64<true>(6, q, p, c2x, c2y, c2z)),
+                                                      entry64<true>(11, q, p, c2x, c2y, c2z)),
+                                            entry64<true>(15, q, p, c2x, c2y, c2z)),
+                                  entry64<true>(18, q, p, c2x, c2y, c2z)),
+                        entry64<true>(20, q, p, c2x, c2y, c2z));
+        const double vp[10] = {__dmul_rn(q.ux, q.ux), __dmul_rn(q.uy, q.uy), __dmul_rn(q.uz, q.uz),
+                               __dmul_rn(q.ux, q.uy), __dmul_rn(q.ux, q.uz), __dmul_rn(q.uy, q.uz),
+                               q.ux, q.uy, q.uz, 1.0};
+        if (q.w != 0.0) {
 #pragma unroll
-      for (int k = 0; k < 10; ++k) acc[k] += (double)part[k];
+          for (int k = 0; k < 10; ++k) acc[k] = __dadd_rn(acc[k], __dmul_rn(vp[k], tr));
+        }
+      } else {
+        // trace = w (2 + |p|^2 + (p.u)^2) in closed form
+        const double pu = fma(p.x, q.ux, fma(p.y, q.uy, p.z * q.uz));
+        tr = q.w * fma(pu, pu, 2.0 + p.w);
+        const double tx = tr * q.ux, ty = tr * q.uy, tz = tr * q.uz;
+        acc[0] = fma(tx, q.ux, acc[0]);
+        acc[1] = fma(ty, q.uy, acc[1]);
+        acc[2] = fma(tz, q.uz, acc[2]);
+        acc[3] = fma(tx, q.uy, acc[3]);
+        acc[4] = fma(tx, q.uz, acc[4]);
+        acc[5] = fma(ty, q.uz, acc[5]);
+        acc[6] += tx;
+        acc[7] += ty;
+        acc[8] += tz;
+        acc[9] += tr;
+      }
     }
   }
   if (active) {
@@ -134,15 +243,11 @@ __global__ void __launch_bounds__(QT_THREADS) k_quad_trace(const float4* __restr
   }
 }
 
-// ─────────────────────────── quad, info ────────────────────────────────
-// Warp-uniform entry groups: warp (w % 4) of a CTA owns a subset of the 21
-// unique entries of the symmetric 6x6 for the CTA's 32 voxels (one per lane).
+// Info: warp-uniform entry groups; warp (w % 4) owns a subset of the 21 unique
+// entries for the CTA's 32 voxels (one per lane), FP64 accumulators in registers.
 // G0: TL {0,1,2,6,7,11}  G1: TR {3,4,5,8,9}  G2: {10,12,13,14,15}  G3: BR {16..20}
 constexpr int QI_THREADS = 128;
-constexpr int QI_TILE = 128;
-constexpr int QI_FLUSH = 32;
 template <int G> struct QGroup { static constexpr int NE = G == 0 ? 6 : 5; };
-// packed index of entry t of group G
 __host__ __device__ constexpr int qidx(int G, int t) {
   return G == 0 ? (t < 3 ? t : (t < 5 ? t + 3 : 11))
        : G == 1 ? (t < 3 ? 3 + t : 5 + t)
@@ -150,85 +255,43 @@ __host__ __device__ constexpr int qidx(int G, int t) {
        : 16 + t;
 }
 
-// Entries of w * block (kernels.py:385-423), world-frame p (global perturbation).
-template <int G>
-__device__ __forceinline__ void group_entries(const PairF& q, float4 a, float* e) {
-  const float w = q.w, ux = q.ux, uy = q.uy, uz = q.uz;
-  const float px = a.x, py = a.y, pz = a.z, pp = a.w;
-  if (G == 0) {
-    float wx = w * ux, wy = w * uy, wz = w * uz;
-    e[0] = fmaf(-wx, ux, w);
-    e[1] = -wx * uy;
-    e[2] = -wx * uz;
-    e[3] = fmaf(-wy, uy, w);
-    e[4] = -wy * uz;
-    e[5] = fmaf(-wz, uz, w);
-  } else {
-    float c2x = fmaf(py, uz, -pz * uy);
-    float c2y = fmaf(pz, ux, -px * uz);
-    float c2z = fmaf(px, uy, -py * ux);
-    if (G == 1) {
-      e[0] = -w * (ux * c2x);            // (0,3)
-      e[1] = -w * fmaf(ux, c2y, -pz);    // (0,4)
-      e[2] = -w * fmaf(ux, c2z, py);     // (0,5)
-      e[3] = -w * fmaf(uy, c2x, pz);     // (1,3)
-      e[4] = -w * (uy * c2y);            // (1,4)
-    } else if (G == 2) {
-      e[0] = -w * fmaf(uy, c2z, -px);    // (1,5)
-      e[1] = -w * fmaf(uz, c2x, -py);    // (2,3)
-      e[2] = -w * fmaf(uz, c2y, px);     // (2,4)
-      e[3] = -w * (uz * c2z);            // (2,5)
-      e[4] = w * fmaf(-c2x, c2x, fmaf(-px, px, pp));  // (3,3)
-    } else {
-      e[0] = w * fmaf(-c2x, c2y, -px * py);          // (3,4)
-      e[1] = w * fmaf(-c2x, c2z, -px * pz);          // (3,5)
-      e[2] = w * fmaf(-c2y, c2y, fmaf(-py, py, pp));  // (4,4)
-      e[3] = w * fmaf(-c2y, c2z, -py * pz);          // (4,5)
-      e[4] = w * fmaf(-c2z, c2z, fmaf(-pz, pz, pp));  // (5,5)
-    }
-  }
-}
-
-template <int G, bool HAS_MASK>
-__device__ __forceinline__ void quad_info_body(const float4* __restrict__ lm, float4* tile, double* accs, int64_t n_pad,
+template <int G, bool EXACT, bool HAS_MASK>
+__device__ __forceinline__ void quad_info_body(const double4* __restrict__ lm, double4* tile, int64_t n_pad,
                                                int64_t n_real, const VoxSrc& src, int64_t v, int64_t v0, bool active,
-                                               const uint8_t* __restrict__ mask, float inv_s2,
+                                               const uint8_t* __restrict__ mask, double inv_s2,
                                                double* __restrict__ out) {
   constexpr int NE = QGroup<G>::NE;
-  const int lane = threadIdx.x & 31;
-  float ch[3], cl[3];
-  voxel_split(src, active ? v : v0, ch, cl);
-  // FP64 accumulators live in shared memory: [k*NE + j][lane]
+  double cx, cy, cz;
+  voxel_center(src, active ? v : v0, cx, cy, cz);
+  double acc[10 * NE];
 #pragma unroll
-  for (int t = 0; t < 10 * NE; ++t) accs[t * 32 + lane] = 0.0;
-  for (int64_t base = 0; base < n_pad; base += QI_TILE) {
+  for (int t = 0; t < 10 * NE; ++t) acc[t] = 0.0;
+  for (int64_t base = 0; base < n_pad; base += QD_TILE) {
     __syncthreads();
-    for (int j = threadIdx.x; j < QI_TILE * 2; j += QI_THREADS) tile[j] = lm[2 * base + j];
+    for (int j = threadIdx.x; j < QD_TILE; j += QI_THREADS) tile[j] = lm[base + j];
     __syncthreads();
 #pragma unroll 1
-    for (int j0 = 0; j0 < QI_TILE; j0 += QI_FLUSH) {
-      float part[10 * NE];
-#pragma unroll
-      for (int t = 0; t < 10 * NE; ++t) part[t] = 0.f;
-#pragma unroll 2
-      for (int j = j0; j < j0 + QI_FLUSH; ++j) {
-        float4 a = tile[2 * j], b = tile[2 * j + 1];
-        if (HAS_MASK) {
-          int64_t i = base + j;
-          if (i < n_real && active && mask[(v - v0) * n_real + i] == 0) b.w = 0.f;
-        }
-        PairF q = pair_prologue(a, b, ch, cl, inv_s2);
-        float e[NE];
-        group_entries<G>(q, a, e);
-        const float vp[10] = {q.ux * q.ux, q.uy * q.uy, q.uz * q.uz, q.ux * q.uy, q.ux * q.uz,
-                              q.uy * q.uz, q.ux, q.uy, q.uz, 1.0f};
-#pragma unroll
-        for (int k = 0; k < 10; ++k)
-#pragma unroll
-          for (int t = 0; t < NE; ++t) part[k * NE + t] = fmaf(vp[k], e[t], part[k * NE + t]);
+    for (int j = 0; j < QD_TILE; ++j) {
+      const double4 p = tile[j];
+      bool keep = active;
+      if (HAS_MASK) {
+        int64_t i = base + j;
+        keep = keep && i < n_real && mask[(v - v0) * n_real + i] != 0;
       }
+      const PairD q = pair64<EXACT>(p, cx, cy, cz, inv_s2, keep);
+      if (EXACT && q.w == 0.0) continue;
+      double c2x = 0, c2y = 0, c2z = 0;
+      if (G != 0) c2_of<EXACT>(q, p, c2x, c2y, c2z);
+      double e[NE];
 #pragma unroll
-      for (int t = 0; t < 10 * NE; ++t) accs[t * 32 + lane] += (double)part[t];
+      for (int t = 0; t < NE; ++t) e[t] = entry64<EXACT>(qidx(G, t), q, p, c2x, c2y, c2z);
+      const double vp[10] = {MUL(q.ux, q.ux), MUL(q.uy, q.uy), MUL(q.uz, q.uz), MUL(q.ux, q.uy),
+                             MUL(q.ux, q.uz), MUL(q.uy, q.uz), q.ux, q.uy, q.uz, 1.0};
+#pragma unroll
+      for (int k = 0; k < 10; ++k)
+#pragma unroll
+        for (int t = 0; t < NE; ++t)
+          acc[k * NE + t] = EXACT ? __dadd_rn(acc[k * NE + t], __dmul_rn(vp[k], e[t])) : fma(vp[k], e[t], acc[k * NE + t]);
     }
   }
   if (active) {
@@ -236,26 +299,27 @@ __device__ __forceinline__ void quad_info_body(const float4* __restrict__ lm, fl
 #pragma unroll
     for (int k = 0; k < 10; ++k)
 #pragma unroll
-      for (int t = 0; t < NE; ++t) o[k * 21 + qidx(G, t)] = accs[(k * NE + t) * 32 + lane];
+      for (int t = 0; t < NE; ++t) o[k * 21 + qidx(G, t)] = acc[k * NE + t];
   }
 }
+#undef MUL
+#undef ADD
+#undef SUB
 
-template <bool HAS_MASK>
-__global__ void __launch_bounds__(QI_THREADS) k_quad_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real,
+template <bool EXACT, bool HAS_MASK>
+__global__ void __launch_bounds__(QI_THREADS) k_quad_info(const double4* __restrict__ lm, int64_t n_pad, int64_t n_real,
                                                           VoxSrc src, int64_t v0, int64_t v1,
-                                                          const uint8_t* __restrict__ mask, float inv_s2,
+                                                          const uint8_t* __restrict__ mask, double inv_s2,
                                                           double* __restrict__ out) {
-  __shared__ float4 tile[QI_TILE * 2];
-  extern __shared__ double accs_all[];  // 4 warps x 60 x 32 doubles
+  __shared__ double4 tile[QD_TILE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t v = v0 + blockIdx.x * (int64_t)32 + lane;
   const bool active = v < v1;
-  double* accs = accs_all + warp * 60 * 32;
   switch (warp) {
-    case 0: quad_info_body<0, HAS_MASK>(lm, tile, accs, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
-    case 1: quad_info_body<1, HAS_MASK>(lm, tile, accs, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
-    case 2: quad_info_body<2, HAS_MASK>(lm, tile, accs, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
-    default: quad_info_body<3, HAS_MASK>(lm, tile, accs, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
+    case 0: quad_info_body<0, EXACT, HAS_MASK>(lm, tile, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
+    case 1: quad_info_body<1, EXACT, HAS_MASK>(lm, tile, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
+    case 2: quad_info_body<2, EXACT, HAS_MASK>(lm, tile, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
+    default: quad_info_body<3, EXACT, HAS_MASK>(lm, tile, n_pad, n_real, src, v, v0, active, mask, inv_s2, out); break;
   }
 }
 
@@ -358,6 +422,46 @@ __global__ void k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSr
     double s = acc.value();
     out64[r * ns + g] = s;
     if (out32) out32[r * ns + g] = (float)s;
+  }
+}
+
+
+// FP32 per-pair helpers for the GP-info phase A (entries of w*block, packed order).
+template <int G>
+__device__ __forceinline__ void group_entries(const PairF& q, float4 a, float* e) {
+  const float w = q.w, ux = q.ux, uy = q.uy, uz = q.uz;
+  const float px = a.x, py = a.y, pz = a.z, pp = a.w;
+  if (G == 0) {
+    float wx = w * ux, wy = w * uy, wz = w * uz;
+    e[0] = fmaf(-wx, ux, w);
+    e[1] = -wx * uy;
+    e[2] = -wx * uz;
+    e[3] = fmaf(-wy, uy, w);
+    e[4] = -wy * uz;
+    e[5] = fmaf(-wz, uz, w);
+  } else {
+    float c2x = fmaf(py, uz, -pz * uy);
+    float c2y = fmaf(pz, ux, -px * uz);
+    float c2z = fmaf(px, uy, -py * ux);
+    if (G == 1) {
+      e[0] = -w * (ux * c2x);
+      e[1] = -w * fmaf(ux, c2y, -pz);
+      e[2] = -w * fmaf(ux, c2z, py);
+      e[3] = -w * fmaf(uy, c2x, pz);
+      e[4] = -w * (uy * c2y);
+    } else if (G == 2) {
+      e[0] = -w * fmaf(uy, c2z, -px);
+      e[1] = -w * fmaf(uz, c2x, -py);
+      e[2] = -w * fmaf(uz, c2y, px);
+      e[3] = -w * (uz * c2z);
+      e[4] = w * fmaf(-c2x, c2x, fmaf(-px, px, pp));
+    } else {
+      e[0] = w * fmaf(-c2x, c2y, -px * py);
+      e[1] = w * fmaf(-c2x, c2z, -px * pz);
+      e[2] = w * fmaf(-c2y, c2y, fmaf(-py, py, pp));
+      e[3] = w * fmaf(-c2y, c2z, -py * pz);
+      e[4] = w * fmaf(-c2z, c2z, fmaf(-pz, pz, pp));
+    }
   }
 }
 
@@ -511,8 +615,8 @@ extern "C" int64_t fif_build_scratch_bytes(int64_t n_points) {
 
 extern "C" int fif_build(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
                          const fif_grid* grid, const double* d_centers, int64_t v_begin, int64_t v_end,
-                         const uint8_t* d_mask, double sigma, void* d_scratch, double* d_out64, float* d_out32,
-                         void* stream) {
+                         const uint8_t* d_mask, double sigma, uint32_t build_flags, void* d_scratch, double* d_out64,
+                         float* d_out32, void* stream) {
   FIF_CHECK_ARG(model != nullptr, "fif_build: model is NULL");
   FIF_CHECK_ARG(factor_kind == FIF_KIND_INFO || factor_kind == FIF_KIND_TRACE, "fif_build: bad factor_kind %d",
                 factor_kind);
@@ -558,37 +662,31 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
   const bool has_mask = d_mask != nullptr;
   int64_t n_pad = ((n_points + kLmPad - 1) / kLmPad) * kLmPad;
   float4* lm = reinterpret_cast<float4*>(d_scratch);
-  const bool need_lm = !(model->kind == FIF_MODEL_GP && trace);
+  FIF_CHECK_ARG(d_scratch != nullptr || (model->kind == FIF_MODEL_GP && trace), "fif_build: d_scratch is NULL");
+  const bool need_lm = model->kind == FIF_MODEL_GP && !trace;
   if (need_lm) {
     FIF_CHECK_ARG(d_scratch != nullptr, "fif_build: d_scratch is NULL");
     k_prep_landmarks<<<(unsigned)((n_pad + 255) / 256), 256, 0, st>>>(d_points, n_points, n_pad, lm);
     FIF_CHECK_LAUNCH("k_prep_landmarks");
   }
   if (model->kind == FIF_MODEL_QUAD) {
+    const bool exact = (build_flags & FIF_BUILD_EXACT) != 0;
+    double4* lm64 = reinterpret_cast<double4*>(d_scratch);
+    k_prep_landmarks64<<<(unsigned)((n_pad + 255) / 256), 256, 0, st>>>(d_points, n_points, n_pad, lm64);
+    FIF_CHECK_LAUNCH("k_prep_landmarks64");
     if (trace) {
-      unsigned blocks = (unsigned)((rows + QT_THREADS - 1) / QT_THREADS);
-      if (has_mask)
-        k_quad_trace<true><<<blocks, QT_THREADS, 0, st>>>(lm, n_pad, n_points, src, v_begin, v_end, d_mask,
-                                                          (float)inv_s2, d_out64);
-      else
-        k_quad_trace<false><<<blocks, QT_THREADS, 0, st>>>(lm, n_pad, n_points, src, v_begin, v_end, d_mask,
-                                                           (float)inv_s2, d_out64);
+      unsigned blocks = (unsigned)((rows + QD_THREADS - 1) / QD_THREADS);
+#define QT_LAUNCH(E, M) k_quad_trace<E, M><<<blocks, QD_THREADS, 0, st>>>(lm64, n_pad, n_points, src, v_begin, v_end, d_mask, inv_s2, d_out64)
+      if (exact) { if (has_mask) QT_LAUNCH(true, true); else QT_LAUNCH(true, false); }
+      else { if (has_mask) QT_LAUNCH(false, true); else QT_LAUNCH(false, false); }
+#undef QT_LAUNCH
       FIF_CHECK_LAUNCH("k_quad_trace");
     } else {
       unsigned blocks = (unsigned)((rows + 31) / 32);
-      size_t smem = 4 * 60 * 32 * sizeof(double);
-      static bool attr_set = false;
-      if (!attr_set) {
-        cudaFuncSetAttribute(k_quad_info<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_quad_info<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-      }
-      if (has_mask)
-        k_quad_info<true><<<blocks, QI_THREADS, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, d_mask,
-                                                            (float)inv_s2, d_out64);
-      else
-        k_quad_info<false><<<blocks, QI_THREADS, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, d_mask,
-                                                             (float)inv_s2, d_out64);
+#define QI_LAUNCH(E, M) k_quad_info<E, M><<<blocks, QI_THREADS, 0, st>>>(lm64, n_pad, n_points, src, v_begin, v_end, d_mask, inv_s2, d_out64)
+      if (exact) { if (has_mask) QI_LAUNCH(true, true); else QI_LAUNCH(true, false); }
+      else { if (has_mask) QI_LAUNCH(false, true); else QI_LAUNCH(false, false); }
+#undef QI_LAUNCH
       FIF_CHECK_LAUNCH("k_quad_info");
     }
     return FIF_OK;

@@ -215,7 +215,8 @@ class _DeviceModel:
 
 def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, device: torch.device, grid=None,
                centers: torch.Tensor | None = None, v_begin: int = 0, v_end: int | None = None,
-               mask: torch.Tensor | None = None, dmodel: _DeviceModel | None = None, f32_copy: bool = True):
+               mask: torch.Tensor | None = None, dmodel: _DeviceModel | None = None, f32_copy: bool = True,
+               exact: bool = False):
     """One fif_build launch: rows [v_begin, v_end) of the z-major grid (or of `centers`).
     Returns (f64 rows (R, width_packed), f32 copy or None)."""
     dm = dmodel or _DeviceModel(model, device)
@@ -232,8 +233,8 @@ def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, devi
     g = _lib.make_grid(grid.origin, grid.voxel_size, grid.dims) if grid is not None else None
     kind = _lib.KIND_TRACE if want_trace else _lib.KIND_INFO
     st = _lib.load().fif_build(kind, dm.c, _lib.ptr(points), n, g, _lib.ptr(centers), v_begin, v_end, _lib.ptr(mask),
-                               float(sigma), _lib.ptr(scratch), _lib.ptr(out64), _lib.ptr(out32),
-                               _device.stream_handle(device))
+                               float(sigma), _lib.BUILD_EXACT if exact else 0, _lib.ptr(scratch), _lib.ptr(out64),
+                               _lib.ptr(out32), _device.stream_handle(device))
     _lib.check(st, "fif_build")
     return out64, out32
 
@@ -318,9 +319,10 @@ class Field:
     # ── construction ────────────────────────────────────────────────
     @staticmethod
     def build(landmarks, config, model, factor_kind: str = "info", matchability: Matchability = ALWAYS_MATCH,
-              sigma: float = DEFAULT_SIGMA, parallel: bool = False, device=None) -> "Field":
+              sigma: float = DEFAULT_SIGMA, parallel: bool = False, device=None, exact: bool = False) -> "Field":
         """Build every voxel's factor on the GPU.  `parallel` is accepted for API
-        compatibility (the GPU build is always parallel)."""
+        compatibility (the GPU build is always parallel).  exact=True (quad model)
+        reproduces the reference's FP64 operation order bit for bit."""
         config = _grid_of(config)
         if config.voxel_count == 0:
             raise EmptyGrid("grid has zero voxels")
@@ -339,7 +341,7 @@ class Field:
                          np.zeros((0, 3), np.int32), matchability, dense=False)
         pts_dev = _device.to_device_f64(points, dev, (3,))
         if matchability.is_trivial:
-            s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, grid=config)
+            s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, grid=config, exact=exact)
             return Field(config, model, factor_kind, sigma, s64, s32, None, matchability, dense=True)
         pts_np = points.cpu().numpy() if isinstance(points, torch.Tensor) else points
         centers = config.centers()
@@ -349,7 +351,7 @@ class Field:
         sub_c = torch.from_numpy(np.ascontiguousarray(centers[occupied])).to(dev)
         sub_m = torch.from_numpy(np.ascontiguousarray(mask[occupied])).to(dev)
         if lin.size:
-            s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, centers=sub_c, mask=sub_m)
+            s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, centers=sub_c, mask=sub_m, exact=exact)
         else:
             s64 = torch.zeros((0, width), dtype=torch.float64, device=dev)
             s32 = s64.float() if gp else None

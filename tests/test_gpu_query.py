@@ -1,0 +1,205 @@
+"""GPU query parity (fif_query through the C ABI) vs the reference and the oracle.
+
+Values: trace relative <= 1e-4, 6x6 relative Frobenius <= 1e-4; det / lmin relative to
+the batch scale <= 1e-4; status bit-exact.  Gradients (new capability):
+<= 1e-4 relative to a central finite difference (h = 1e-6) of the FP64 oracle query,
+t' = t + dt, R' = exp(dtheta^) R.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2008_03324_b200 as F
+from paper_2008_03324_b200 import field as FD
+from paper_2008_03324_b200.geometry import so3_exp
+from tests._helpers import models_from_golden, oracle_model
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def models(g_models):
+    return models_from_golden(g_models)
+
+
+@pytest.fixture(scope="module")
+def small_grid(g_small):
+    return F.GridConfig(g_small["origin"], g_small["voxel_size"][0], g_small["dims"])
+
+
+def field_from_reference(grid, model, kind, factors):
+    """A device Field holding exactly the reference's rows (x-major, all voxels)."""
+    s64 = torch.tensor(FD._from_reference_rows(factors, model, kind), device="cuda")
+    s32 = s64.float() if isinstance(model, F.GpVisibility) else None
+    occ = grid.index3_of(np.arange(grid.voxel_count)).astype(np.int32)
+    return FD.Field(grid, model, kind, 1.0, s64, s32, occ, dense=False)
+
+
+def rel(a, b):
+    return np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+
+
+@pytest.mark.parametrize("mname", ["quad", "gp30", "gp70"])
+@pytest.mark.parametrize("kind", ["trace", "info"])
+@pytest.mark.parametrize("mode", ["nearest", "trilinear"])
+@pytest.mark.parametrize("source", ["reference_field", "gpu_build"])
+def test_queries_vs_reference(g_small, models, small_grid, mname, kind, mode, source):
+    m = models[mname]
+    if source == "reference_field":
+        f = field_from_reference(small_grid, m, kind, g_small[f"factors_{mname}_{kind}"])
+    else:
+        f = F.Field.build(g_small["points"], small_grid, m, kind)
+    pos, rots = g_small["positions"], g_small["rotations"]
+    axes = np.ascontiguousarray(rots[:, :, 2])
+    ok_ref = g_small[f"ok_{mname}_{kind}_{mode}"]
+    vals, ok = f.metric_axis_batch(pos, axes, "trace", mode)
+    assert np.array_equal(ok, ok_ref)
+    ref = g_small[f"trace_{mname}_{kind}_{mode}"]
+    assert rel(vals, ref)[ok_ref].max() <= TOL
+    assert np.all(vals[~ok_ref] == 0)
+    if kind == "info":
+        fims, ok2 = f.query_fim_batch(pos, rots, mode)
+        assert np.array_equal(ok2, ok_ref)
+        rf = g_small[f"fim_{mname}_{mode}"]
+        e = np.linalg.norm((fims - rf).reshape(len(pos), -1), axis=1) / np.maximum(
+            np.linalg.norm(rf.reshape(len(pos), -1), axis=1), 1e-300)
+        assert e[ok_ref].max() <= TOL
+        assert np.allclose(fims, np.transpose(fims, (0, 2, 1)))
+        for metric in ("det", "lmin"):
+            mv, _ = f.metric_axis_batch(pos, axes, metric, mode)
+            rm = g_small[f"{metric}_{mname}_{mode}"]
+            assert (np.abs(mv - rm)[ok_ref].max() / np.abs(rm[ok_ref]).max()) <= TOL
+
+
+def test_single_pose_api_errors(g_small, models, small_grid):
+    f = F.Field.build(g_small["points"], small_grid, models["quad"], "info")
+    ft = F.Field.build(g_small["points"], small_grid, models["quad"], "trace")
+    inside = F.Pose(F.random_rotation(np.random.default_rng(1)), small_grid.center_of([2, 2, 2]) + 0.1)
+    outside = F.Pose(np.eye(3), small_grid.origin - 1.0)
+    assert f.query_fim(inside, "trilinear").shape == (6, 6)
+    with pytest.raises(F.OutOfField):
+        f.query_fim(outside)
+    with pytest.raises(F.OutOfField):
+        f.query_metric(outside, "trace")
+    with pytest.raises(F.WrongFactorKind):
+        ft.query_fim(inside)
+    with pytest.raises(F.WrongFactorKind):
+        ft.query_metric(inside, "det")
+    with pytest.raises(ValueError):
+        f.query_fim(inside, "cubic")
+    assert ft.query_metric(inside, "trace", "trilinear") == pytest.approx(
+        f.query_metric(inside, "trace", "trilinear"), rel=1e-9)  # trace consistency
+
+
+def _fd_queries(oracle, factors, grid, model, kind, pos, rots, h=1e-6):
+    """Central FD of the oracle's trilinear trace (and 6x6 for info) w.r.t. [t; theta]."""
+    slots = np.arange(grid.voxel_count, dtype=np.int32)
+    om = oracle_model(model)
+
+    def ev(p, r):
+        ax = np.ascontiguousarray(r[:, :, 2])
+        tr, st = oracle.metric_batch(slots, factors, grid.origin, grid.voxel_size, grid.dims, p, ax, om, "trace",
+                                     kind == "trace", True)
+        fim = None
+        if kind == "info":
+            fim, _ = oracle.query_fim_batch(slots, factors, grid.origin, grid.voxel_size, grid.dims, p, ax, om, True)
+        return tr, fim, st
+
+    q = pos.shape[0]
+    g_tr = np.zeros((q, 6))
+    g_fim = np.zeros((q, 6, 6, 6)) if kind == "info" else None
+    for j in range(6):
+        if j < 3:
+            d = np.zeros(3)
+            d[j] = h
+            a, b = ev(pos + d, rots), ev(pos - d, rots)
+        else:
+            w = np.zeros(3)
+            w[j - 3] = h
+            Rp, Rm = so3_exp(w), so3_exp(-w)
+            a = ev(pos, np.einsum("ij,qjk->qik", Rp, rots))
+            b = ev(pos, np.einsum("ij,qjk->qik", Rm, rots))
+        g_tr[:, j] = (a[0] - b[0]) / (2 * h)
+        if kind == "info":
+            g_fim[:, j] = (a[1] - b[1]) / (2 * h)
+    return g_tr, g_fim
+
+
+@pytest.mark.parametrize("mname", ["quad", "gp30", "gp70"])
+@pytest.mark.parametrize("kind", ["trace", "info"])
+def test_gradients_vs_finite_difference(oracle, g_small, models, small_grid, mname, kind):
+    m = models[mname]
+    factors = g_small[f"factors_{mname}_{kind}"]
+    f = field_from_reference(small_grid, m, kind, factors)
+    rng = np.random.default_rng(17)
+    c = small_grid.centers()
+    pos = rng.uniform(c[0], c[-1], size=(60, 3))
+    g = (pos - small_grid.origin) / small_grid.voxel_size - 0.5
+    frac = g - np.floor(g)
+    pos = pos[((frac > 1e-3) & (frac < 1 - 1e-3)).all(axis=1)]  # >= 2h away from cell faces
+    rots = np.stack([F.random_rotation(rng) for _ in range(pos.shape[0])])
+    outs = ("trace", "full") if kind == "info" else ("trace",)
+    for f64 in (True, False):
+        dev = torch.device("cuda")
+        res = f.query_device(torch.tensor(pos, device=dev), torch.tensor(np.ascontiguousarray(rots[:, :, 2]), device=dev),
+                             "trilinear", trace=True, full=kind == "info", grad=True, field_f64=f64)
+        g_tr_fd, g_fim_fd = _fd_queries(oracle, factors, small_grid, m, kind, pos,
+                                        rots)
+        g_tr = res["trace_grad"].cpu().numpy()
+        err = np.linalg.norm(g_tr - g_tr_fd, axis=1) / np.linalg.norm(g_tr_fd, axis=1)
+        tol = TOL if (f64 or isinstance(m, F.QuadraticVisibility)) else 5 * TOL
+        assert err.max() <= tol, (f64, err.max())
+        if kind == "info":
+            g_f = res["fim_grad"].cpu().numpy().reshape(-1, 6, 6, 6)
+            e2 = np.linalg.norm((g_f - g_fim_fd).reshape(len(pos), -1), axis=1) / np.linalg.norm(
+                g_fim_fd.reshape(len(pos), -1), axis=1)
+            assert e2.max() <= tol, (f64, e2.max())
+
+
+def test_config2_queries_end_to_end(oracle, models):
+    """GPU-built config-2 field, 64 trilinear queries with gradient, vs the oracle on a cropped field."""
+    from paper_2008_03324_b200 import scenes
+    from tests._helpers import oracle_field
+
+    w = scenes.config2(64)
+    grid = F.GridConfig(*w.grid)
+    for mname in ("quad", "gp70"):
+        m = models[mname]
+        f = F.Field.build(w.points, grid, m, "info")
+        res = f.query_batch(w.positions, rotations=w.rotations, outputs=("trace", "full"), grad=True,
+                            to_numpy=True)
+        need = sorted({int(i) for p in w.positions for i in oracle.trilinear(grid.origin, grid.voxel_size,
+                                                                            grid.dims, p)[0]})
+        need = np.array(need)
+        rows = oracle_field(oracle, m, grid.centers()[need], w.points, "info")
+        slots = np.full(grid.voxel_count, -1, np.int32)
+        slots[need] = np.arange(len(need), dtype=np.int32)
+        ax = np.ascontiguousarray(w.rotations[:, :, 2])
+        rt, st = oracle.metric_batch(slots, rows, grid.origin, grid.voxel_size, grid.dims, w.positions, ax,
+                                     oracle_model(m), "trace", False, True)
+        rf, _ = oracle.query_fim_batch(slots, rows, grid.origin, grid.voxel_size, grid.dims, w.positions, ax,
+                                       oracle_model(m), True)
+        assert np.array_equal(res["in_field"], st == 0)
+        assert rel(res["trace"], rt).max() <= TOL
+        e = np.linalg.norm((res["fim"] - rf).reshape(64, -1), axis=1) / np.linalg.norm(rf.reshape(64, -1), axis=1)
+        assert e.max() <= TOL
+        assert np.isfinite(res["fim_grad"]).all()
+
+
+def test_factorization_exact_at_voxel_centres(models):
+    """at a voxel centre the field FIM equals sum_i v_model(theta_i) I_i."""
+    rng = np.random.default_rng(4)
+    pts = rng.uniform([-3, -3, 0], [3, 3, 3], size=(150, 3))
+    grid = F.GridConfig(np.array([-1.0, -1.0, 0.5]), 0.5, np.array([4, 4, 3]))
+    for mname in ("quad", "gp30"):
+        m = models[mname]
+        f = F.Field.build(pts, grid, m, "info")
+        for idx in ([1, 1, 1], [2, 3, 0]):
+            c = grid.center_of(idx)
+            R = F.random_rotation(rng)
+            got = f.query_fim(F.Pose(R, c), "nearest")
+            vr = m.rotation_vector(R)
+            vp = m.position_vectors(c, pts)
+            direct = sum(float(vr @ vp[i]) * F.landmark_fim(c, pts[i]) for i in range(len(pts)))
+            assert np.linalg.norm(got - direct) <= 1e-6 * np.linalg.norm(direct)

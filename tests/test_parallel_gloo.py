@@ -1,0 +1,73 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): landmark broadcast, z-slab
+partition, all-gather replication.  The per-rank compute is the CPU oracle standing in
+for the CUDA build (test seam `row_builder`), so the assembled field must equal the
+single-process oracle field bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2008_03324_b200.parallel import slab_range
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        import paper_2008_03324_b200 as F
+        from paper_2008_03324_b200.parallel import build_sharded
+
+        rng = np.random.default_rng(0)
+        pts = rng.uniform([-2, -2, 0], [2, 2, 2], size=(120, 3)) if rank == 0 else None
+        grid = F.GridConfig(np.array([-1.0, -1.0, 0.0]), 0.5, np.array([5, 4, 3]))
+        model = F.build_quad_model()
+        # internal z-major centres, so slab rows line up with the device layout
+        cz = grid.center_of(grid.index3_of_internal(np.arange(grid.voxel_count)))
+
+        def row_builder(p, v0, v1):
+            rows = O.build_quad_factors(cz[v0:v1], p.numpy(), 1.0, model.k2, model.k1, model.k0, True)
+            return torch.from_numpy(rows), None
+
+        v0, v1, rows, _, full = build_sharded(pts, grid, model, "trace", device=torch.device("cpu"),
+                                              replicate=True, row_builder=row_builder)
+        if rank == 0:
+            ref = O.build_quad_factors(cz, rng_pts(), 1.0, model.k2, model.k1, model.k0, True)
+            np.save(result_path, np.stack([full.numpy(), ref]))
+    finally:
+        dist.destroy_process_group()
+
+
+def rng_pts():
+    return np.random.default_rng(0).uniform([-2, -2, 0], [2, 2, 2], size=(120, 3))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_build_matches_single_process(tmp_path, world):
+    out = str(tmp_path / "res.npy")
+    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True, start_method="spawn")
+    full, ref = np.load(out)
+    assert np.array_equal(full, ref)
+
+
+def test_slab_range_partition():
+    for total in (0, 1, 7, 137781, 25351101):
+        for world in (1, 2, 3, 4, 8):
+            r = [slab_range(total, world, k) for k in range(world)]
+            assert r[0][0] == 0 and r[-1][1] == total
+            assert all(r[k][1] == r[k + 1][0] for k in range(world - 1))
+            sizes = [e - b for b, e in r]
+            assert max(sizes) - min(sizes) <= 1

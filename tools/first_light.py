@@ -12,10 +12,10 @@ quad = F.build_quad_model()
 gps = {ns: F.GpVisibility(m[f'gp{ns}_zs'], F.SeKernelParams(m[f'gp{ns}_par'][2], m[f'gp{ns}_par'][3], m[f'gp{ns}_par'][4]), m[f'gp{ns}_par'][0], m[f'gp{ns}_par'][1], m[f'gp{ns}_kinv']) for ns in (30, 70)}
 models = {'quad': quad, 'gp30': gps[30], 'gp70': gps[70]}
 pos, rots = g['positions'], g['rotations']
-for mname, model in models.items():
+for mname, model, exact in [('quad', quad, True), ('quad', quad, False), ('gp30', gps[30], False), ('gp70', gps[70], False)]:
     for kind in ('trace', 'info'):
         t0 = time.time()
-        f = F.Field.build(pts, grid, model, kind)
+        f = F.Field.build(pts, grid, model, kind, exact=exact)
         torch.cuda.synchronize()
         ref = g[f'factors_{mname}_{kind}']
         # reorder: our rows follow occupied_index3 (z-major); reference rows are x-major
@@ -25,7 +25,7 @@ for mname, model in models.items():
             err = (np.linalg.norm(mine - ref, axis=1) / np.linalg.norm(ref, axis=1)).max()
         else:
             err = max(np.abs(mine[i] - ref[i]).max() / np.linalg.norm(ref[i]) for i in range(ref.shape[0]))
-        line = f'{mname:5s} {kind:5s} build err {err:.3e} ({time.time()-t0:.2f}s)'
+        line = f'{mname:5s}{"X" if exact else " "} {kind:5s} build err {err:.3e} bitexact {np.array_equal(mine, ref)} ({time.time()-t0:.2f}s)'
         for mode in ('nearest', 'trilinear'):
             vals, ok = f.metric_axis_batch(pos, rots[:, :, 2], 'trace', mode)
             rv = g[f'trace_{mname}_{kind}_{mode}']; rok = g[f'ok_{mname}_{kind}_{mode}']
