@@ -426,99 +426,113 @@ __global__ void k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSr
 }
 
 
-// FP32 per-pair helpers for the GP-info phase A (entries of w*block, packed order).
-template <int G>
-__device__ __forceinline__ void group_entries(const PairF& q, float4 a, float* e) {
+// ─────────────────────────── GP, info ──────────────────────────────────
+// Phase A: per pair, u and the 21 unique entries of w*block in FP32, laid out
+// for packed FP32x2 math: float4 {ux, uy, uz, e20}, then e0..e19 as 5 float4.
+// Phase B: thread (v, g) evaluates vs_g once per landmark and accumulates
+// vs_g * entries with FFMA2 (sm_100 packed FP32) into FP32 partials, flushed
+// every GI_FLUSH landmarks into FP64 accumulators (F2F on the MUFU pipe + DADD
+// on the otherwise idle FP64 pipe).
+constexpr int GI_TILE = 32;
+constexpr int GI_FLUSH = 32;
+constexpr int GI_THREADS_MAX = 320;
+
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pack2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// All 21 packed entries (FP32) for one pair.
+__device__ __forceinline__ void entries21(const PairF& q, float4 a, float* e) {
   const float w = q.w, ux = q.ux, uy = q.uy, uz = q.uz;
   const float px = a.x, py = a.y, pz = a.z, pp = a.w;
-  if (G == 0) {
-    float wx = w * ux, wy = w * uy, wz = w * uz;
-    e[0] = fmaf(-wx, ux, w);
-    e[1] = -wx * uy;
-    e[2] = -wx * uz;
-    e[3] = fmaf(-wy, uy, w);
-    e[4] = -wy * uz;
-    e[5] = fmaf(-wz, uz, w);
-  } else {
-    float c2x = fmaf(py, uz, -pz * uy);
-    float c2y = fmaf(pz, ux, -px * uz);
-    float c2z = fmaf(px, uy, -py * ux);
-    if (G == 1) {
-      e[0] = -w * (ux * c2x);
-      e[1] = -w * fmaf(ux, c2y, -pz);
-      e[2] = -w * fmaf(ux, c2z, py);
-      e[3] = -w * fmaf(uy, c2x, pz);
-      e[4] = -w * (uy * c2y);
-    } else if (G == 2) {
-      e[0] = -w * fmaf(uy, c2z, -px);
-      e[1] = -w * fmaf(uz, c2x, -py);
-      e[2] = -w * fmaf(uz, c2y, px);
-      e[3] = -w * (uz * c2z);
-      e[4] = w * fmaf(-c2x, c2x, fmaf(-px, px, pp));
-    } else {
-      e[0] = w * fmaf(-c2x, c2y, -px * py);
-      e[1] = w * fmaf(-c2x, c2z, -px * pz);
-      e[2] = w * fmaf(-c2y, c2y, fmaf(-py, py, pp));
-      e[3] = w * fmaf(-c2y, c2z, -py * pz);
-      e[4] = w * fmaf(-c2z, c2z, fmaf(-pz, pz, pp));
-    }
-  }
+  const float wx = w * ux, wy = w * uy, wz = w * uz;
+  const float c2x = fmaf(py, uz, -pz * uy), c2y = fmaf(pz, ux, -px * uz), c2z = fmaf(px, uy, -py * ux);
+  e[0] = fmaf(-wx, ux, w);
+  e[1] = -wx * uy;
+  e[2] = -wx * uz;
+  e[3] = -w * (ux * c2x);
+  e[4] = -w * fmaf(ux, c2y, -pz);
+  e[5] = -w * fmaf(ux, c2z, py);
+  e[6] = fmaf(-wy, uy, w);
+  e[7] = -wy * uz;
+  e[8] = -w * fmaf(uy, c2x, pz);
+  e[9] = -w * (uy * c2y);
+  e[10] = -w * fmaf(uy, c2z, -px);
+  e[11] = fmaf(-wz, uz, w);
+  e[12] = -w * fmaf(uz, c2x, -py);
+  e[13] = -w * fmaf(uz, c2y, px);
+  e[14] = -w * (uz * c2z);
+  e[15] = w * fmaf(-c2x, c2x, fmaf(-px, px, pp));
+  e[16] = w * fmaf(-c2x, c2y, -px * py);
+  e[17] = w * fmaf(-c2x, c2z, -px * pz);
+  e[18] = w * fmaf(-c2y, c2y, fmaf(-py, py, pp));
+  e[19] = w * fmaf(-c2y, c2z, -py * pz);
+  e[20] = w * fmaf(-c2z, c2z, fmaf(-pz, pz, pp));
 }
 
-// ─────────────────────────── GP, info ──────────────────────────────────
-// Phase A: per pair, u and the 21 unique entries of w*block in FP32 (24 floats);
-// phase B: thread (v, g) accumulates vs_g * entries into 21 FP32 partials,
-// flushed every GI_FLUSH landmarks into double-float accumulators.
-constexpr int GI_TILE = 32;
-constexpr int GI_FLUSH = 16;
-
-__device__ __forceinline__ void all_entries(const PairF& q, float4 a, float* e) {
-  group_entries<0>(q, a, e + 0);   // slots 0,1,2,6,7,11
-  group_entries<1>(q, a, e + 6);   // 3,4,5,8,9
-  group_entries<2>(q, a, e + 11);  // 10,12,13,14,15
-  group_entries<3>(q, a, e + 16);  // 16..20
-}
-// position in the e[] order above of each packed index 0..20
-__constant__ int kEntryPerm[21] = {0, 1, 2, 6, 7, 8, 3, 4, 9, 10, 11, 5, 12, 13, 14, 15, 16, 17, 18, 19, 20};
+// Two samples per thread (g, g + tpv) share every pair load; FP64 accumulators
+// live in shared memory ([42][blockDim] doubles) so three CTAs fit per SM.
+constexpr int GI_FLUSH_TILES = 2;  // FP32 partials span 64 landmarks
+constexpr int GI_VB_THREADS = 160;
 
 template <bool HAS_MASK>
-__global__ void k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0,
-                          int64_t v1, int vb, int ns, const double* __restrict__ zs, const uint8_t* __restrict__ mask,
-                          float inv_s2, float ax, float bx, double* __restrict__ out64, float* __restrict__ out32) {
+__global__ void __launch_bounds__(GI_VB_THREADS, 3)
+k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1, int vb,
+          int ns, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax, float bx,
+          double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float4* pairs = reinterpret_cast<float4*>(smem_raw);          // [vb][GI_TILE][6]
-  float4* tile = pairs + vb * GI_TILE * 6;                      // [GI_TILE][2]
-  float* cs = reinterpret_cast<float*>(tile + GI_TILE * 2);     // [vb][6] centre hi/lo
+  const int tpv = (ns + 1) / 2;                                  // threads per voxel
+  const int pstride = GI_TILE * 6 + 1;                           // float4 per voxel (+1: bank spread)
+  double* accs = reinterpret_cast<double*>(smem_raw);            // [42][blockDim.x]
+  float4* pairs = reinterpret_cast<float4*>(accs + 42 * blockDim.x);  // [vb][pstride]
+  float4* tile = pairs + vb * pstride;                           // [GI_TILE][2]
+  float* cs = reinterpret_cast<float*>(tile + GI_TILE * 2);      // [vb][6]
   const int t = threadIdx.x;
+  const int nt = blockDim.x;
   const int64_t vbase = v0 + blockIdx.x * (int64_t)vb;
   if (t < vb) {
     int64_t v = vbase + t;
     float ch[3], cl[3];
     voxel_split(src, v < v1 ? v : v0, ch, cl);
-    for (int a = 0; a < 3; ++a) {
-      cs[6 * t + a] = ch[a];
-      cs[6 * t + 3 + a] = cl[a];
+    for (int k = 0; k < 3; ++k) {
+      cs[6 * t + k] = ch[k];
+      cs[6 * t + 3 + k] = cl[k];
     }
   }
-  const int vl = t / ns, g = t - vl * ns;
+  for (int k = 0; k < 42; ++k) accs[k * nt + t] = 0.0;
+  const int vl = t / tpv, gi = t - vl * tpv;
+  const int g0 = gi, g1 = gi + tpv;
   const bool worker = vl < vb;
   const bool active = worker && (vbase + vl) < v1;
-  float zx = 0.f, zy = 0.f, zz = 0.f;
+  const bool has1 = g1 < ns;
+  float z0x = 0.f, z0y = 0.f, z0z = 0.f, z1x = 0.f, z1y = 0.f, z1z = 0.f;
   if (worker) {
-    zx = (float)zs[3 * g];
-    zy = (float)zs[3 * g + 1];
-    zz = (float)zs[3 * g + 2];
+    z0x = (float)zs[3 * g0]; z0y = (float)zs[3 * g0 + 1]; z0z = (float)zs[3 * g0 + 2];
+    if (has1) { z1x = (float)zs[3 * g1]; z1y = (float)zs[3 * g1 + 1]; z1z = (float)zs[3 * g1 + 2]; }
   }
-  DF acc[21];
+  float2 pa[10], pb[10];
+  float pa20 = 0.f, pb20 = 0.f;
 #pragma unroll
-  for (int e = 0; e < 21; ++e) acc[e].init();
+  for (int k = 0; k < 10; ++k) pa[k] = pb[k] = make_float2(0.f, 0.f);
   const int npairs = vb * GI_TILE;
+  int tiles = 0;
   for (int64_t base = 0; base < n_pad; base += GI_TILE) {
     __syncthreads();
-    for (int j = t; j < GI_TILE * 2; j += blockDim.x) tile[j] = lm[2 * base + j];
+    for (int j = t; j < GI_TILE * 2; j += nt) tile[j] = lm[2 * base + j];
     __syncthreads();
-    for (int pidx = t; pidx < npairs; pidx += blockDim.x) {
-      int pv = pidx / GI_TILE, pj = pidx - pv * GI_TILE;
+    for (int pidx = t; pidx < npairs; pidx += nt) {
+      const int pv = pidx / GI_TILE, pj = pidx - pv * GI_TILE;
       float4 a = tile[2 * pj], b = tile[2 * pj + 1];
       if ((vbase + pv) >= v1) b.w = 0.f;
       if (HAS_MASK) {
@@ -526,51 +540,68 @@ __global__ void k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t 
         if (b.w != 0.f && mask[(vbase + pv - v0) * n_real + i] == 0) b.w = 0.f;
       }
       const float* c = cs + 6 * pv;
-      float ch[3] = {c[0], c[1], c[2]}, cl[3] = {c[3], c[4], c[5]};
-      PairF q = pair_prologue(a, b, ch, cl, inv_s2);
+      const float ch[3] = {c[0], c[1], c[2]}, cl[3] = {c[3], c[4], c[5]};
+      const PairF q = pair_prologue(a, b, ch, cl, inv_s2);
       float e[21];
-      all_entries(q, a, e);
-      float4* dst = pairs + pidx * 6;
-      dst[0] = make_float4(q.ux, q.uy, q.uz, e[kEntryPerm[0]]);
-      dst[1] = make_float4(e[kEntryPerm[1]], e[kEntryPerm[2]], e[kEntryPerm[3]], e[kEntryPerm[4]]);
-      dst[2] = make_float4(e[kEntryPerm[5]], e[kEntryPerm[6]], e[kEntryPerm[7]], e[kEntryPerm[8]]);
-      dst[3] = make_float4(e[kEntryPerm[9]], e[kEntryPerm[10]], e[kEntryPerm[11]], e[kEntryPerm[12]]);
-      dst[4] = make_float4(e[kEntryPerm[13]], e[kEntryPerm[14]], e[kEntryPerm[15]], e[kEntryPerm[16]]);
-      dst[5] = make_float4(e[kEntryPerm[17]], e[kEntryPerm[18]], e[kEntryPerm[19]], e[kEntryPerm[20]]);
+      entries21(q, a, e);
+      float4* dst = pairs + pv * pstride + pj * 6;
+      dst[0] = make_float4(q.ux, q.uy, q.uz, e[20]);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) dst[1 + k] = make_float4(e[4 * k], e[4 * k + 1], e[4 * k + 2], e[4 * k + 3]);
     }
     __syncthreads();
     if (worker) {
-      const float4* pv = pairs + vl * GI_TILE * 6;
+      const float4* pv = pairs + vl * pstride;
 #pragma unroll 1
-      for (int j0 = 0; j0 < GI_TILE; j0 += GI_FLUSH) {
-        float part[21];
+      for (int j = 0; j < GI_TILE; ++j) {
+        const float4* p = pv + 6 * j;
+        const float4 r0 = p[0];
+        const float c0 = fmaf(r0.x, z0x, fmaf(r0.y, z0y, r0.z * z0z));
+        const float c1 = fmaf(r0.x, z1x, fmaf(r0.y, z1y, r0.z * z1z));
+        const float va = rcp_approx(1.0f + ex2_approx(fmaf(c0, ax, bx)));
+        const float vb_ = rcp_approx(1.0f + ex2_approx(fmaf(c1, ax, bx)));
+        const float2 va2 = make_float2(va, va), vb2 = make_float2(vb_, vb_);
 #pragma unroll
-        for (int e = 0; e < 21; ++e) part[e] = 0.f;
-#pragma unroll 2
-        for (int j = j0; j < j0 + GI_FLUSH; ++j) {
-          const float4* p = pv + 6 * j;
-          float4 r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3], r4 = p[4], r5 = p[5];
-          float c = fmaf(r0.x, zx, fmaf(r0.y, zy, r0.z * zz));
-          float vs = rcp_approx(1.0f + ex2_approx(fmaf(c, ax, bx)));
-          const float ent[21] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w, r3.x, r3.y,
-                                 r3.z, r3.w, r4.x, r4.y, r4.z, r4.w, r5.x, r5.y, r5.z, r5.w};
-#pragma unroll
-          for (int e = 0; e < 21; ++e) part[e] = fmaf(vs, ent[e], part[e]);
+        for (int k = 0; k < 5; ++k) {
+          const float4 r = p[1 + k];
+          const float2 lo = make_float2(r.x, r.y), hi = make_float2(r.z, r.w);
+          pa[2 * k] = __ffma2_rn(va2, lo, pa[2 * k]);
+          pa[2 * k + 1] = __ffma2_rn(va2, hi, pa[2 * k + 1]);
+          pb[2 * k] = __ffma2_rn(vb2, lo, pb[2 * k]);
+          pb[2 * k + 1] = __ffma2_rn(vb2, hi, pb[2 * k + 1]);
         }
+        pa20 = fmaf(va, r0.w, pa20);
+        pb20 = fmaf(vb_, r0.w, pb20);
+      }
+      if (++tiles == GI_FLUSH_TILES || base + GI_TILE >= n_pad) {
+        tiles = 0;
 #pragma unroll
-        for (int e = 0; e < 21; ++e) acc[e].add(part[e]);
+        for (int k = 0; k < 10; ++k) {
+          accs[(2 * k) * nt + t] += (double)pa[k].x;
+          accs[(2 * k + 1) * nt + t] += (double)pa[k].y;
+          accs[(21 + 2 * k) * nt + t] += (double)pb[k].x;
+          accs[(22 + 2 * k) * nt + t] += (double)pb[k].y;
+          pa[k] = pb[k] = make_float2(0.f, 0.f);
+        }
+        accs[20 * nt + t] += (double)pa20;
+        accs[41 * nt + t] += (double)pb20;
+        pa20 = pb20 = 0.f;
       }
     }
   }
   if (active) {
-    int64_t r = vbase + vl - v0;
-    double* o = out64 + (r * ns + g) * 21;
+    const int64_t r = vbase + vl - v0;
+    for (int s = 0; s < 2; ++s) {
+      const int g = s ? g1 : g0;
+      if (g >= ns) continue;
+      double* o = out64 + (r * ns + g) * 21;
+      float* o32 = out32 ? out32 + (r * ns + g) * 21 : nullptr;
 #pragma unroll
-    for (int e = 0; e < 21; ++e) o[e] = acc[e].value();
-    if (out32) {
-      float* o32 = out32 + (r * ns + g) * 21;
-#pragma unroll
-      for (int e = 0; e < 21; ++e) o32[e] = (float)acc[e].value();
+      for (int e = 0; e < 21; ++e) {
+        const double v = accs[(21 * s + e) * nt + t];
+        o[e] = v;
+        if (o32) o32[e] = (float)v;
+      }
     }
   }
 }
@@ -698,12 +729,19 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
   // sigmoid 1/(1 + exp(-k_s (c - cos a))) = 1/(1 + 2^(c*ax + bx))
   const double LOG2E = 1.4426950408889634;
   const double ax = -model->k_s * LOG2E, bx = model->k_s * model->cos_alpha * LOG2E;
-  int vb = 320 / ns;
+  int vb = GI_THREADS_MAX / ns;
   if (vb < 1) vb = 1;
+  FIF_CHECK_ARG(ns <= GI_THREADS_MAX, "fif_build: N_s=%d exceeds %d", ns, GI_THREADS_MAX);
   int threads = ((vb * ns + 31) / 32) * 32;
   unsigned blocks = (unsigned)((rows + vb - 1) / vb);
   if (trace) {
     size_t smem = sizeof(PairT) * vb * GT_TILE + sizeof(double) * 3 * vb + sizeof(double) * 3 * GT_TILE;
+    static bool carve = false;
+    if (!carve) {
+      for (auto f : {k_gp_trace<true>, k_gp_trace<false>})
+        cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      carve = true;
+    }
     if (has_mask)
       k_gp_trace<true><<<blocks, threads, smem, st>>>(d_points, n_points, src, v_begin, v_end, vb, ns, model->zs,
                                                       d_mask, inv_s2, ax, bx, d_out64, d_out32);
@@ -712,17 +750,29 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
                                                        d_mask, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
   } else {
-    size_t smem = sizeof(float4) * (vb * GI_TILE * 6 + GI_TILE * 2) + sizeof(float) * 6 * vb;
-    if (smem > 48 * 1024) {
-      cudaFuncSetAttribute(k_gp_info<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_gp_info<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int tpv = (ns + 1) / 2;
+    int vbi = GI_VB_THREADS / tpv;
+    if (vbi < 1) vbi = 1;
+    const int threads_i = ((vbi * tpv + 31) / 32) * 32;
+    FIF_CHECK_ARG(threads_i <= GI_VB_THREADS || vbi == 1, "fif_build: N_s=%d too large for k_gp_info", ns);
+    const unsigned blocks_i = (unsigned)((rows + vbi - 1) / vbi);
+    size_t smem = sizeof(double) * 42 * threads_i + sizeof(float4) * (vbi * (GI_TILE * 6 + 1) + GI_TILE * 2) +
+                  sizeof(float) * 6 * vbi;
+    static bool carve = false;
+    if (!carve) {  // prefer the max shared-memory carveout so several CTAs fit per SM
+      for (auto f : {k_gp_info<true>, k_gp_info<false>}) {
+        cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      }
+      carve = true;
     }
     if (has_mask)
-      k_gp_info<true><<<blocks, threads, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, vb, ns, model->zs,
-                                                     d_mask, (float)inv_s2, (float)ax, (float)bx, d_out64, d_out32);
+      k_gp_info<true><<<blocks_i, threads_i, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, vbi, ns, model->zs,
+                                                         d_mask, (float)inv_s2, (float)ax, (float)bx, d_out64, d_out32);
     else
-      k_gp_info<false><<<blocks, threads, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, vb, ns, model->zs,
-                                                      d_mask, (float)inv_s2, (float)ax, (float)bx, d_out64, d_out32);
+      k_gp_info<false><<<blocks_i, threads_i, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, vbi, ns,
+                                                          model->zs, d_mask, (float)inv_s2, (float)ax, (float)bx,
+                                                          d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_info");
   }
   return FIF_OK;

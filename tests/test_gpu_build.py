@@ -174,16 +174,18 @@ def test_matchability_mask(models, oracle, g_small, small_grid):
 
 
 def test_incremental_add_remove(models, small_grid, g_small):
+    """add/remove == rebuild; quad is FP64 throughout, GP's FP32 partial sums
+    group landmarks differently in the two builds, so agreement is at FP32-partial level."""
     pts = g_small["points"]
-    for mname in ("quad", "gp30"):
+    for mname, tol in (("quad", 1e-12), ("gp30", 1e-6)):
         full = F.Field.build(pts, small_grid, models[mname], "info")
         inc = F.Field.build(pts[:200], small_grid, models[mname], "info")
         inc.add_landmarks(pts[200:])
         ref = full.storage["f64"]
-        assert (torch.abs(inc.storage["f64"] - ref).max() / torch.abs(ref).max()).item() < 1e-9
+        assert (torch.abs(inc.storage["f64"] - ref).max() / torch.abs(ref).max()).item() < tol
         inc.remove_landmarks(pts[200:])
         base = F.Field.build(pts[:200], small_grid, models[mname], "info").storage["f64"]
-        assert (torch.abs(inc.storage["f64"] - base).max() / torch.abs(base).max()).item() < 1e-9
+        assert (torch.abs(inc.storage["f64"] - base).max() / torch.abs(base).max()).item() < tol
 
 
 def test_serialize_roundtrip(models, small_grid, g_small, tmp_path):
@@ -198,7 +200,9 @@ def test_serialize_roundtrip(models, small_grid, g_small, tmp_path):
         a, oka = f.query_fim_batch(pos, rots, "trilinear")
         b, okb = g.query_fim_batch(pos, rots, "trilinear")
         assert np.array_equal(oka, okb)
-        assert np.abs(a - b).max() <= 1e-9 * np.abs(a).max()
+        # quad: FP64 rows round-trip exactly; GP: S = K F is re-rounded to the FP32 query copy
+        tol = 1e-12 if mname == "quad" else 1e-6
+        assert np.abs(a - b).max() <= tol * np.abs(a).max()
     with pytest.raises(F.BadMagic):
         bad = tmp_path / "bad.fif"
         bad.write_bytes(b"XXXX" + b"\0" * 64)

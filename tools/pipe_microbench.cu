@@ -31,6 +31,14 @@ __global__ void kern(float* outf, double* outd, float seed, long long* clk) {
       if (OP == 11) { float r; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f[c]));
                       f[c] = fmaf(r, 0.999f, 0.001f); f[c] = fmaf(f[c], 0.999f, 0.001f); f[c] = fmaf(f[c], 0.999f, 0.001f); f[c] = fmaf(f[c], 0.999f, 0.001f);}
       if (OP == 12) { int x = __float_as_int(f[c]); x = __funnelshift_l(x, x ^ 7, 3) + 0x40000000; f[c] = __int_as_float(x); }
+      if (OP == 14) { unsigned long long a, d; asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(f[c]), "f"(f[c] + 1.f));
+                      asm volatile("fma.rn.f32x2 %0, %1, %1, %1;" : "=l"(d) : "l"(a));
+                      float x, y; asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(d)); f[c] = x - y; }
+      if (OP == 15) { unsigned long long a, b, d; asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(f[c]), "f"(f[c]));
+                      b = a;
+#pragma unroll
+                      for (int r = 0; r < 4; ++r) { asm volatile("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(d) : "l"(a), "l"(b)); a = d; }
+                      float x, y; asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a)); f[c] = x + y; }
       if (OP == 13) { double r; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(r) : "f"(f[c]));
                       float e; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(f[c])); f[c] = __int_as_float(__double2hiint(r) ^ 3) + e; }
     }
@@ -82,5 +90,6 @@ int main() {
   run<11>("EX2 + 4 FFMA", sms);
   run<12>("SHF+IADD (ALU)", sms);
   run<10>("DDIV (__ddiv_rn)", sms);
+  run<15>("4x FFMA2 (=8 FMA)", sms);
   return 0;
 }
