@@ -324,26 +324,35 @@ __global__ void __launch_bounds__(QI_THREADS) k_quad_info(const double4* __restr
 }
 
 // ─────────────────────────── GP, trace ─────────────────────────────────
-// CTA = VB voxels x N_s samples (thread (v, g)).  Phase A: per (voxel, landmark)
-// pair, FP64 bearing u and FP32 trace tr into smem.  Phase B: thread (v, g)
-// evaluates vs = sigmoid(k_s (u.z_g - cos a)) with the cosine in FP64 and the
-// exponent/reciprocal on MUFU, and accumulates tr * vs.
+// CTA = VB voxels x ceil(N_s/GT_G) threads; thread (v, gi) owns samples gi + s*tpv.
+// Phase A: per (voxel, landmark) pair, FP64 bearing u and FP32 trace tr into smem
+// (the reference's exact d, n2 and skip rule).  Phase B: for each landmark a
+// thread loads the 32-byte pair record once and evaluates GT_G sigmoids with the
+// cosine in FP64 (the kinv epilogue amplifies S errors ~200x),
+// converts the exponent argument to FP32 on the integer ALU, and accumulates
+// tr * vs into FP32 partials flushed into double-float accumulators.
 constexpr int GT_TILE = 64;
 constexpr int GT_FLUSH = 8;
+constexpr int GT_G = 4;
+constexpr int GT_THREADS = 256;
 struct __align__(16) PairT {
   double ux, uy, uz;
   float tr, pad;
 };
 
 template <bool HAS_MASK>
-__global__ void k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1, int vb,
-                           int ns, const double* __restrict__ zs, const uint8_t* __restrict__ mask, double inv_s2,
-                           double ax, double bx, double* __restrict__ out64, float* __restrict__ out32) {
+__global__ void __launch_bounds__(GT_THREADS) k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSrc src,
+                                                         int64_t v0, int64_t v1, int vb, int ns,
+                                                         const double* __restrict__ zs, const uint8_t* __restrict__ mask,
+                                                         double inv_s2, double ax, double bx,
+                                                         double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PairT* pairs = reinterpret_cast<PairT*>(smem_raw);                     // [vb][GT_TILE]
-  double* cen = reinterpret_cast<double*>(pairs + vb * GT_TILE);         // [vb][3]
-  double* lp = cen + 3 * vb;                                             // [GT_TILE][3] landmark tile
-  const int t = threadIdx.x;
+  const int pstride = GT_TILE + 1;                                // records per voxel (+1: bank spread)
+  PairT* pairs = reinterpret_cast<PairT*>(smem_raw);              // [vb][pstride]
+  double* cen = reinterpret_cast<double*>(pairs + vb * pstride);  // [vb][3]
+  double* lp = cen + 3 * vb;                                      // [GT_TILE][3] landmark tile
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int tpv = (ns + GT_G - 1) / GT_G;
   const int64_t vbase = v0 + blockIdx.x * (int64_t)vb;
   if (t < vb) {
     int64_t v = vbase + t;
@@ -353,41 +362,46 @@ __global__ void k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSr
     cen[3 * t + 1] = cy;
     cen[3 * t + 2] = cz;
   }
-  const int vl = t / ns, g = t - vl * ns;
+  const int vl = t / tpv, gi = t - vl * tpv;
   const bool worker = vl < vb;
   const bool active = worker && (vbase + vl) < v1;
-  double zx = 0, zy = 0, zz = 0;
-  if (worker) {
-    zx = zs[3 * g];
-    zy = zs[3 * g + 1];
-    zz = zs[3 * g + 2];
+  // x = ax (u . z) + bx = (ax zx) ux + (ax zy) uy + (ax zz) uz + bx
+  double zx[GT_G], zy[GT_G], zz[GT_G];
+#pragma unroll
+  for (int s = 0; s < GT_G; ++s) {
+    const int g = gi + s * tpv;
+    const bool ok = worker && g < ns;
+    zx[s] = ok ? ax * zs[3 * g] : 0.0;
+    zy[s] = ok ? ax * zs[3 * g + 1] : 0.0;
+    zz[s] = ok ? ax * zs[3 * g + 2] : 0.0;
   }
-  DF acc;
-  acc.init();
+  DF acc[GT_G];
+#pragma unroll
+  for (int s = 0; s < GT_G; ++s) acc[s].init();
   const int npairs = vb * GT_TILE;
   for (int64_t base = 0; base < n_real; base += GT_TILE) {
     __syncthreads();
-    for (int j = t; j < GT_TILE * 3; j += blockDim.x) {
+    for (int j = t; j < GT_TILE * 3; j += nt) {
       int64_t i = base + j / 3;
       lp[j] = i < n_real ? pts[3 * base + j] : 0.0;
     }
     __syncthreads();
-    // phase A: FP64 per-pair quantities (exactly the reference's d, n2, skip rule)
-    for (int pidx = t; pidx < npairs; pidx += blockDim.x) {
-      int pv = pidx / GT_TILE, pj = pidx - pv * GT_TILE;
-      int64_t i = base + pj;
-      double px = lp[3 * pj], py = lp[3 * pj + 1], pz = lp[3 * pj + 2];
-      double dx = px - cen[3 * pv], dy = py - cen[3 * pv + 1], dz = pz - cen[3 * pv + 2];
-      double n2 = dx * dx + dy * dy + dz * dz;
-      bool ok = i < n_real && n2 >= 1e-300 && (vbase + pv) < v1;
+    // phase A: FP64 per-pair quantities
+    for (int pidx = t; pidx < npairs; pidx += nt) {
+      const int pv = pidx / GT_TILE, pj = pidx - pv * GT_TILE;
+      const int64_t i = base + pj;
+      const double px = lp[3 * pj], py = lp[3 * pj + 1], pz = lp[3 * pj + 2];
+      const double dx = px - cen[3 * pv], dy = py - cen[3 * pv + 1], dz = pz - cen[3 * pv + 2];
+      const double n2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      bool ok = i < n_real && n2 >= 1e-300 && (vbase + pv) < v1;  // kernels.py:494
       if (HAS_MASK && ok) ok = mask[(vbase + pv - v0) * n_real + i] != 0;
       PairT pr;
       if (ok) {
-        double rn = rsqrt(n2);
-        double ux = dx * rn, uy = dy * rn, uz = dz * rn;
-        double w = inv_s2 * rn * rn;
-        double pu = px * ux + py * uy + pz * uz;
-        double pp = px * px + py * py + pz * pz;
+        const double rn = rsqrt_nr(n2);
+        const double ux = dx * rn, uy = dy * rn, uz = dz * rn;
+        const double w = inv_s2 * rn * rn;
+        const double pu = px * ux + py * uy + pz * uz;
+        const double pp = px * px + py * py + pz * pz;
         pr.ux = ux;
         pr.uy = uy;
         pr.uz = uz;
@@ -397,34 +411,46 @@ __global__ void k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSr
         pr.tr = 0.f;
       }
       pr.pad = 0.f;
-      pairs[pidx] = pr;
+      pairs[pv * pstride + pj] = pr;
     }
     __syncthreads();
     if (worker) {
-      const PairT* pv = pairs + vl * GT_TILE;
+      const PairT* pv = pairs + vl * pstride;
 #pragma unroll 1
       for (int j0 = 0; j0 < GT_TILE; j0 += GT_FLUSH) {
-        float part = 0.f;
+        float part[GT_G];
 #pragma unroll
+        for (int s = 0; s < GT_G; ++s) part[s] = 0.f;
+#pragma unroll 2
         for (int j = j0; j < j0 + GT_FLUSH; ++j) {
-          PairT pr = pv[j];
-          double c = fma(pr.ux, zx, fma(pr.uy, zy, pr.uz * zz));
-          float x = f64_to_f32_alu(fma(c, ax, bx));  // -k_s (c - cos a) log2(e)
-          float vs = rcp_approx(1.0f + ex2_approx(x));
-          part = fmaf(pr.tr, vs, part);
+          const PairT pr = pv[j];
+#pragma unroll
+          for (int s = 0; s < GT_G; ++s) {
+            // -k_s (u.z - cos a) log2(e), FP64.  + 2^-60 keeps the argument off exact
+            // zero (which the ALU conversion cannot represent); |x| is either 0 or
+            // >= ~1e-15 here, so the shift is below FP32 resolution of 2^x.
+            const float x = f64_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bx))) + 0x1p-60);
+            const float vs = rcp_approx(1.0f + ex2_approx(x));
+            part[s] = fmaf(pr.tr, vs, part[s]);
+          }
         }
-        acc.add(part);
+#pragma unroll
+        for (int s = 0; s < GT_G; ++s) acc[s].add(part[s]);
       }
     }
   }
   if (active) {
-    int64_t r = vbase + vl - v0;
-    double s = acc.value();
-    out64[r * ns + g] = s;
-    if (out32) out32[r * ns + g] = (float)s;
+    const int64_t r = vbase + vl - v0;
+#pragma unroll
+    for (int s = 0; s < GT_G; ++s) {
+      const int g = gi + s * tpv;
+      if (g >= ns) continue;
+      const double v = acc[s].value();
+      out64[r * ns + g] = v;
+      if (out32) out32[r * ns + g] = (float)v;
+    }
   }
 }
-
 
 // ─────────────────────────── GP, info ──────────────────────────────────
 // Phase A: per pair, u and the 21 unique entries of w*block in FP32, laid out
@@ -481,25 +507,29 @@ __device__ __forceinline__ void entries21(const PairF& q, float4 a, float* e) {
   e[20] = w * fmaf(-c2z, c2z, fmaf(-pz, pz, pp));
 }
 
-// Two samples per thread (g, g + tpv) share every pair load; FP64 accumulators
-// live in shared memory ([42][blockDim] doubles) so three CTAs fit per SM.
-constexpr int GI_FLUSH_TILES = 2;  // FP32 partials span 64 landmarks
-constexpr int GI_VB_THREADS = 160;
+// Shared-memory reads cost one wavefront per 128 lane-bytes even when every lane
+// reads the same address (measured: LDS.128 broadcast ~ 4 wavefronts), so each
+// thread handles GI_G samples (g, g+tpv, g+2tpv, ...) of one voxel and reuses
+// every 96-byte pair record GI_G times; FP64 accumulators live in shared memory
+// ([21*GI_G][blockDim] doubles) and are refreshed every GI_FLUSH_TILES tiles.
+constexpr int GI_G = 4;
+constexpr int GI_FLUSH_TILES = 4;  // FP32 partials span 128 landmarks
+constexpr int GI_VB_THREADS = 128;
 
 template <bool HAS_MASK>
-__global__ void __launch_bounds__(GI_VB_THREADS, 3)
+__global__ void __launch_bounds__(GI_VB_THREADS, 2)
 k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1, int vb,
           int ns, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax, float bx,
           double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tpv = (ns + 1) / 2;                                  // threads per voxel
+  const int tpv = (ns + GI_G - 1) / GI_G;                        // threads per voxel
   const int pstride = GI_TILE * 6 + 1;                           // float4 per voxel (+1: bank spread)
-  double* accs = reinterpret_cast<double*>(smem_raw);            // [42][blockDim.x]
-  float4* pairs = reinterpret_cast<float4*>(accs + 42 * blockDim.x);  // [vb][pstride]
+  const int nt = blockDim.x;
+  double* accs = reinterpret_cast<double*>(smem_raw);            // [21*GI_G][nt]
+  float4* pairs = reinterpret_cast<float4*>(accs + 21 * GI_G * nt);  // [vb][pstride]
   float4* tile = pairs + vb * pstride;                           // [GI_TILE][2]
   float* cs = reinterpret_cast<float*>(tile + GI_TILE * 2);      // [vb][6]
   const int t = threadIdx.x;
-  const int nt = blockDim.x;
   const int64_t vbase = v0 + blockIdx.x * (int64_t)vb;
   if (t < vb) {
     int64_t v = vbase + t;
@@ -510,21 +540,27 @@ k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc s
       cs[6 * t + 3 + k] = cl[k];
     }
   }
-  for (int k = 0; k < 42; ++k) accs[k * nt + t] = 0.0;
+  for (int k = 0; k < 21 * GI_G; ++k) accs[k * nt + t] = 0.0;
   const int vl = t / tpv, gi = t - vl * tpv;
-  const int g0 = gi, g1 = gi + tpv;
   const bool worker = vl < vb;
   const bool active = worker && (vbase + vl) < v1;
-  const bool has1 = g1 < ns;
-  float z0x = 0.f, z0y = 0.f, z0z = 0.f, z1x = 0.f, z1y = 0.f, z1z = 0.f;
-  if (worker) {
-    z0x = (float)zs[3 * g0]; z0y = (float)zs[3 * g0 + 1]; z0z = (float)zs[3 * g0 + 2];
-    if (has1) { z1x = (float)zs[3 * g1]; z1y = (float)zs[3 * g1 + 1]; z1z = (float)zs[3 * g1 + 2]; }
-  }
-  float2 pa[10], pb[10];
-  float pa20 = 0.f, pb20 = 0.f;
+  float zx[GI_G], zy[GI_G], zz[GI_G];
 #pragma unroll
-  for (int k = 0; k < 10; ++k) pa[k] = pb[k] = make_float2(0.f, 0.f);
+  for (int s = 0; s < GI_G; ++s) {
+    const int g = gi + s * tpv;
+    const bool ok = worker && g < ns;
+    zx[s] = ok ? (float)zs[3 * g] : 0.f;
+    zy[s] = ok ? (float)zs[3 * g + 1] : 0.f;
+    zz[s] = ok ? (float)zs[3 * g + 2] : 0.f;
+  }
+  float2 part[GI_G][10];
+  float part20[GI_G];
+#pragma unroll
+  for (int s = 0; s < GI_G; ++s) {
+    part20[s] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 10; ++k) part[s][k] = make_float2(0.f, 0.f);
+  }
   const int npairs = vb * GI_TILE;
   int tiles = 0;
   for (int64_t base = 0; base < n_pad; base += GI_TILE) {
@@ -552,47 +588,70 @@ k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc s
     __syncthreads();
     if (worker) {
       const float4* pv = pairs + vl * pstride;
-#pragma unroll 1
-      for (int j = 0; j < GI_TILE; ++j) {
-        const float4* p = pv + 6 * j;
-        const float4 r0 = p[0];
-        const float c0 = fmaf(r0.x, z0x, fmaf(r0.y, z0y, r0.z * z0z));
-        const float c1 = fmaf(r0.x, z1x, fmaf(r0.y, z1y, r0.z * z1z));
-        const float va = rcp_approx(1.0f + ex2_approx(fmaf(c0, ax, bx)));
-        const float vb_ = rcp_approx(1.0f + ex2_approx(fmaf(c1, ax, bx)));
-        const float2 va2 = make_float2(va, va), vb2 = make_float2(vb_, vb_);
+      // software pipeline: the sigmoids of landmarks j+2, j+3 (2 x GI_G independent
+      // MUFU chains) are issued before the FFMA2 block of landmarks j, j+1.
+      float vs[2][GI_G], e20[2];
+      auto sigmoids = [&](int j, float (&out)[2][GI_G], float (&oe)[2]) {
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {
-          const float4 r = p[1 + k];
-          const float2 lo = make_float2(r.x, r.y), hi = make_float2(r.z, r.w);
-          pa[2 * k] = __ffma2_rn(va2, lo, pa[2 * k]);
-          pa[2 * k + 1] = __ffma2_rn(va2, hi, pa[2 * k + 1]);
-          pb[2 * k] = __ffma2_rn(vb2, lo, pb[2 * k]);
-          pb[2 * k + 1] = __ffma2_rn(vb2, hi, pb[2 * k + 1]);
+        for (int u = 0; u < 2; ++u) {
+          const float4 r0 = pv[6 * (j + u)];
+          oe[u] = r0.w;
+#pragma unroll
+          for (int s = 0; s < GI_G; ++s) {
+            const float cg = fmaf(r0.x, zx[s], fmaf(r0.y, zy[s], r0.z * zz[s]));
+            out[u][s] = rcp_approx(1.0f + ex2_approx(fmaf(cg, ax, bx)));
+          }
         }
-        pa20 = fmaf(va, r0.w, pa20);
-        pb20 = fmaf(vb_, r0.w, pb20);
+      };
+      sigmoids(0, vs, e20);
+#pragma unroll 1
+      for (int j0 = 0; j0 < GI_TILE; j0 += 2) {
+        float vn[2][GI_G], en[2];
+        sigmoids((j0 + 2) & (GI_TILE - 1), vn, en);  // wraps harmlessly on the last step
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const float4* p = pv + 6 * (j0 + u);
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const float4 r = p[1 + k];
+            const float2 lo = make_float2(r.x, r.y), hi = make_float2(r.z, r.w);
+#pragma unroll
+            for (int s = 0; s < GI_G; ++s) {
+              const float2 v2 = make_float2(vs[u][s], vs[u][s]);
+              part[s][2 * k] = __ffma2_rn(v2, lo, part[s][2 * k]);
+              part[s][2 * k + 1] = __ffma2_rn(v2, hi, part[s][2 * k + 1]);
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < GI_G; ++s) part20[s] = fmaf(vs[u][s], e20[u], part20[s]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          e20[u] = en[u];
+#pragma unroll
+          for (int s = 0; s < GI_G; ++s) vs[u][s] = vn[u][s];
+        }
       }
       if (++tiles == GI_FLUSH_TILES || base + GI_TILE >= n_pad) {
         tiles = 0;
 #pragma unroll
-        for (int k = 0; k < 10; ++k) {
-          accs[(2 * k) * nt + t] += (double)pa[k].x;
-          accs[(2 * k + 1) * nt + t] += (double)pa[k].y;
-          accs[(21 + 2 * k) * nt + t] += (double)pb[k].x;
-          accs[(22 + 2 * k) * nt + t] += (double)pb[k].y;
-          pa[k] = pb[k] = make_float2(0.f, 0.f);
+        for (int s = 0; s < GI_G; ++s) {
+#pragma unroll
+          for (int k = 0; k < 10; ++k) {
+            accs[(21 * s + 2 * k) * nt + t] += (double)part[s][k].x;
+            accs[(21 * s + 2 * k + 1) * nt + t] += (double)part[s][k].y;
+            part[s][k] = make_float2(0.f, 0.f);
+          }
+          accs[(21 * s + 20) * nt + t] += (double)part20[s];
+          part20[s] = 0.f;
         }
-        accs[20 * nt + t] += (double)pa20;
-        accs[41 * nt + t] += (double)pb20;
-        pa20 = pb20 = 0.f;
       }
     }
   }
   if (active) {
     const int64_t r = vbase + vl - v0;
-    for (int s = 0; s < 2; ++s) {
-      const int g = s ? g1 : g0;
+    for (int s = 0; s < GI_G; ++s) {
+      const int g = gi + s * tpv;
       if (g >= ns) continue;
       double* o = out64 + (r * ns + g) * 21;
       float* o32 = out32 ? out32 + (r * ns + g) * 21 : nullptr;
@@ -728,35 +787,44 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
   FIF_CHECK_ARG(model->zs != nullptr, "fif_build: GP model without zs");
   // sigmoid 1/(1 + exp(-k_s (c - cos a))) = 1/(1 + 2^(c*ax + bx))
   const double LOG2E = 1.4426950408889634;
-  const double ax = -model->k_s * LOG2E, bx = model->k_s * model->cos_alpha * LOG2E;
+  const double ax = -model->k_s * LOG2E;
+  const double bx = model->k_s * model->cos_alpha * LOG2E;
   int vb = GI_THREADS_MAX / ns;
   if (vb < 1) vb = 1;
   FIF_CHECK_ARG(ns <= GI_THREADS_MAX, "fif_build: N_s=%d exceeds %d", ns, GI_THREADS_MAX);
   int threads = ((vb * ns + 31) / 32) * 32;
   unsigned blocks = (unsigned)((rows + vb - 1) / vb);
   if (trace) {
-    size_t smem = sizeof(PairT) * vb * GT_TILE + sizeof(double) * 3 * vb + sizeof(double) * 3 * GT_TILE;
+    const int tpv = (ns + GT_G - 1) / GT_G;
+    int vbt = GT_THREADS / tpv;
+    if (vbt < 1) vbt = 1;
+    const int threads_t = ((vbt * tpv + 31) / 32) * 32;
+    FIF_CHECK_ARG(threads_t <= GT_THREADS, "fif_build: N_s=%d too large for k_gp_trace", ns);
+    const unsigned blocks_t = (unsigned)((rows + vbt - 1) / vbt);
+    size_t smem = sizeof(PairT) * vbt * (GT_TILE + 1) + sizeof(double) * 3 * vbt + sizeof(double) * 3 * GT_TILE;
     static bool carve = false;
     if (!carve) {
-      for (auto f : {k_gp_trace<true>, k_gp_trace<false>})
+      for (auto f : {k_gp_trace<true>, k_gp_trace<false>}) {
         cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      }
       carve = true;
     }
     if (has_mask)
-      k_gp_trace<true><<<blocks, threads, smem, st>>>(d_points, n_points, src, v_begin, v_end, vb, ns, model->zs,
-                                                      d_mask, inv_s2, ax, bx, d_out64, d_out32);
+      k_gp_trace<true><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns, model->zs,
+                                                          d_mask, inv_s2, ax, bx, d_out64, d_out32);
     else
-      k_gp_trace<false><<<blocks, threads, smem, st>>>(d_points, n_points, src, v_begin, v_end, vb, ns, model->zs,
-                                                       d_mask, inv_s2, ax, bx, d_out64, d_out32);
+      k_gp_trace<false><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns,
+                                                           model->zs, d_mask, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
   } else {
-    const int tpv = (ns + 1) / 2;
+    const int tpv = (ns + GI_G - 1) / GI_G;
     int vbi = GI_VB_THREADS / tpv;
     if (vbi < 1) vbi = 1;
     const int threads_i = ((vbi * tpv + 31) / 32) * 32;
     FIF_CHECK_ARG(threads_i <= GI_VB_THREADS || vbi == 1, "fif_build: N_s=%d too large for k_gp_info", ns);
     const unsigned blocks_i = (unsigned)((rows + vbi - 1) / vbi);
-    size_t smem = sizeof(double) * 42 * threads_i + sizeof(float4) * (vbi * (GI_TILE * 6 + 1) + GI_TILE * 2) +
+    size_t smem = sizeof(double) * 21 * GI_G * threads_i + sizeof(float4) * (vbi * (GI_TILE * 6 + 1) + GI_TILE * 2) +
                   sizeof(float) * 6 * vbi;
     static bool carve = false;
     if (!carve) {  // prefer the max shared-memory carveout so several CTAs fit per SM
