@@ -16,7 +16,6 @@
 
 namespace fif {
 
-constexpr int Q_WARPS = 8;
 
 struct QueryGeom {
   double ox, oy, oz, vs;
@@ -70,64 +69,6 @@ __device__ __forceinline__ int locate(const QueryGeom& gm, const int32_t* __rest
     }
   }
   return FIF_STATUS_OK;
-}
-
-// Rotation weights into smem: wt[0][k] = weight, wt[1+a][k] = d weight / d z_a.
-// quad: v^r (kernels.py:638-649); GP: omega = kinv v^r with v^r_g = s2 exp((z.zs_g - 1)/l^2)
-// (kernels.py:652-657) — kinv symmetric, so omega . S == v^r . (kinv S).
-__device__ __forceinline__ void rotation_weights(const fif_model& m, int nv, double zx, double zy, double zz,
-                                                 double* __restrict__ wt, double* __restrict__ tmp, int lane) {
-  if (m.kind == FIF_MODEL_QUAD) {
-    if (lane < 10) {
-      const double k2 = m.k2, k1 = m.k1, k0 = m.k0, t2 = 2.0 * k2;
-      double v = 0, gx = 0, gy = 0, gz = 0;
-      switch (lane) {
-        case 0: v = __dmul_rn(__dmul_rn(k2, zx), zx); gx = t2 * zx; break;
-        case 1: v = __dmul_rn(__dmul_rn(k2, zy), zy); gy = t2 * zy; break;
-        case 2: v = __dmul_rn(__dmul_rn(k2, zz), zz); gz = t2 * zz; break;
-        case 3: v = __dmul_rn(__dmul_rn(t2, zx), zy); gx = t2 * zy; gy = t2 * zx; break;
-        case 4: v = __dmul_rn(__dmul_rn(t2, zx), zz); gx = t2 * zz; gz = t2 * zx; break;
-        case 5: v = __dmul_rn(__dmul_rn(t2, zy), zz); gy = t2 * zz; gz = t2 * zy; break;
-        case 6: v = __dmul_rn(k1, zx); gx = k1; break;
-        case 7: v = __dmul_rn(k1, zy); gy = k1; break;
-        case 8: v = __dmul_rn(k1, zz); gz = k1; break;
-        default: v = k0; break;
-      }
-      wt[lane] = v;
-      wt[nv + lane] = gx;
-      wt[2 * nv + lane] = gy;
-      wt[3 * nv + lane] = gz;
-    }
-    __syncwarp();
-    return;
-  }
-  const double inv_l2 = 1.0 / (m.ell * m.ell);
-  for (int g = lane; g < nv; g += 32) {
-    double zsx = m.zs[3 * g], zsy = m.zs[3 * g + 1], zsz = m.zs[3 * g + 2];
-    double c = __dadd_rn(__dadd_rn(__dmul_rn(zx, zsx), __dmul_rn(zy, zsy)), __dmul_rn(zz, zsz));
-    double vr = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
-    tmp[g] = vr;
-    double s = vr * inv_l2;
-    tmp[nv + g] = s * zsx;
-    tmp[2 * nv + g] = s * zsy;
-    tmp[3 * nv + g] = s * zsz;
-  }
-  __syncwarp();
-  for (int k = lane; k < nv; k += 32) {
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    for (int g = 0; g < nv; ++g) {
-      double kg = __ldg(m.kinv + (int64_t)g * nv + k);
-      a0 = fma(kg, tmp[g], a0);
-      a1 = fma(kg, tmp[nv + g], a1);
-      a2 = fma(kg, tmp[2 * nv + g], a2);
-      a3 = fma(kg, tmp[3 * nv + g], a3);
-    }
-    wt[k] = a0;
-    wt[nv + k] = a1;
-    wt[2 * nv + k] = a2;
-    wt[3 * nv + k] = a3;
-  }
-  __syncwarp();
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -200,10 +141,6 @@ __constant__ int kPackR[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3
 __constant__ int kPackC[21] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5};
 __constant__ int kIsDiag[21] = {1, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 1, 0, 1};
 
-template <typename T>
-__device__ __forceinline__ double ld_field(const T* __restrict__ p) {
-  return (double)__ldg(p);
-}
 
 struct QueryOut {
   double* trace;
@@ -215,210 +152,450 @@ struct QueryOut {
   uint8_t* status;
 };
 
-// KIND: FIF_KIND_INFO rows (nv,21) | FIF_KIND_TRACE rows (nv)
-template <typename T, int KIND, bool GRAD, bool METRIC>
-__global__ void __launch_bounds__(Q_WARPS * 32) k_query(fif_model m, QueryGeom gm, const T* __restrict__ field,
-                                                        const int32_t* __restrict__ slots,
-                                                        const double* __restrict__ pos,
-                                                        const double* __restrict__ axes, int64_t nq, int trilinear,
-                                                        QueryOut out) {
-  extern __shared__ double qsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// ───────────────────────── prep: corners + rotation weights ─────────────
+// Per query q: status, 8 corner rows (int32, -1 = empty/absent), corner weights
+// cw[q][c] = {w, dw/dx, dw/dy, dw/dz}, and rotation weights wt[q][4][nv] =
+// {omega, d omega/dz_x, d omega/dz_y, d omega/dz_z} in FP64, where omega = v^r (quad,
+// kernels.py:638-649) or kinv v^r (GP, kernels.py:652-657; kinv symmetric so
+// omega . S == v^r . (kinv S)).  A CTA handles QP_Q queries; the GP matrix-vector
+// products run one thread per (query, output k) with v^r staged in smem.
+constexpr int QP_Q = 8;
+constexpr int QP_THREADS = 256;
+
+__global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeom gm, const int32_t* __restrict__ slots,
+                                                          const double* __restrict__ pos, const double* __restrict__ axes,
+                                                          int64_t nq, int trilinear, uint8_t* __restrict__ status,
+                                                          int32_t* __restrict__ rows, double4* __restrict__ cw,
+                                                          double* __restrict__ wt) {
+  extern __shared__ double sv[];  // [QP_Q][4][nv]
   const int nv = m.kind == FIF_MODEL_QUAD ? 10 : m.n_v;
-  double* wt = qsm + warp * (8 * nv + 8 * 21);  // [4][nv] weights
-  double* tmp = wt + 4 * nv;                     // [4][nv] GP scratch
-  double* cornerfim = tmp + 4 * nv;              // [8][21] (METRIC)
-  const int64_t rw = KIND == FIF_KIND_INFO ? (int64_t)nv * 21 : nv;
-  for (int64_t q = blockIdx.x * (int64_t)Q_WARPS + warp; q < nq; q += (int64_t)gridDim.x * Q_WARPS) {
-    const double px = pos[3 * q], py = pos[3 * q + 1], pz = pos[3 * q + 2];
-    const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+  const int64_t q0 = blockIdx.x * (int64_t)QP_Q;
+  const int t = threadIdx.x;
+  // corners and trilinear weights: one thread per query (FP64, reference order)
+  if (t < QP_Q && q0 + t < nq) {
+    const int64_t q = q0 + t;
     int nc = 0;
-    int64_t rows[8];
+    int64_t r[8];
     double w[8], dw[8][3];
-    const int st = locate(gm, slots, px, py, pz, trilinear != 0, nc, rows, w, dw);
-    if (out.status && lane == 0) out.status[q] = (uint8_t)st;
-    if (st != FIF_STATUS_OK) {
-      if (KIND == FIF_KIND_INFO) {
-        for (int j = lane; j < 36; j += 32) if (out.fim) out.fim[q * 36 + j] = 0.0;
-        if (out.fim_grad) for (int j = lane; j < 216; j += 32) out.fim_grad[q * 216 + j] = 0.0;
+    const int st = locate(gm, slots, pos[3 * q], pos[3 * q + 1], pos[3 * q + 2], trilinear != 0, nc, r, w, dw);
+    status[q] = (uint8_t)st;
+    for (int c = 0; c < 8; ++c) {
+      const bool ok = st == FIF_STATUS_OK && c < nc;
+      rows[q * 8 + c] = ok ? (int32_t)r[c] : -1;
+      cw[q * 8 + c] = ok ? make_double4(w[c], dw[c][0], dw[c][1], dw[c][2]) : make_double4(0, 0, 0, 0);
+    }
+  }
+  if (m.kind == FIF_MODEL_QUAD) {
+    for (int idx = t; idx < QP_Q * 10; idx += blockDim.x) {
+      const int qi = idx / 10, k = idx - qi * 10;
+      const int64_t q = q0 + qi;
+      if (q >= nq) continue;
+      const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+      const double k2 = m.k2, k1 = m.k1, k0 = m.k0, t2 = 2.0 * k2;
+      double v = 0, gx = 0, gy = 0, gz = 0;
+      switch (k) {
+        case 0: v = __dmul_rn(__dmul_rn(k2, zx), zx); gx = t2 * zx; break;
+        case 1: v = __dmul_rn(__dmul_rn(k2, zy), zy); gy = t2 * zy; break;
+        case 2: v = __dmul_rn(__dmul_rn(k2, zz), zz); gz = t2 * zz; break;
+        case 3: v = __dmul_rn(__dmul_rn(t2, zx), zy); gx = t2 * zy; gy = t2 * zx; break;
+        case 4: v = __dmul_rn(__dmul_rn(t2, zx), zz); gx = t2 * zz; gz = t2 * zx; break;
+        case 5: v = __dmul_rn(__dmul_rn(t2, zy), zz); gy = t2 * zz; gz = t2 * zy; break;
+        case 6: v = __dmul_rn(k1, zx); gx = k1; break;
+        case 7: v = __dmul_rn(k1, zy); gy = k1; break;
+        case 8: v = __dmul_rn(k1, zz); gz = k1; break;
+        default: v = k0; break;
       }
+      double* o = wt + q * 4 * 10;
+      o[k] = v;
+      o[10 + k] = gx;
+      o[20 + k] = gy;
+      o[30 + k] = gz;
+    }
+    return;
+  }
+  // GP: v^r and its z-derivatives into smem, then omega = kinv v^r (FP64)
+  const double inv_l2 = 1.0 / (m.ell * m.ell);
+  for (int idx = t; idx < QP_Q * nv; idx += blockDim.x) {
+    const int qi = idx / nv, g = idx - qi * nv;
+    const int64_t q = q0 + qi;
+    double* o = sv + qi * 4 * nv;
+    if (q >= nq) {
+      o[g] = o[nv + g] = o[2 * nv + g] = o[3 * nv + g] = 0.0;
+      continue;
+    }
+    const double zsx = m.zs[3 * g], zsy = m.zs[3 * g + 1], zsz = m.zs[3 * g + 2];
+    const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * q], zsx), __dmul_rn(axes[3 * q + 1], zsy)),
+                               __dmul_rn(axes[3 * q + 2], zsz));
+    const double vr = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
+    const double sc = vr * inv_l2;
+    o[g] = vr;
+    o[nv + g] = sc * zsx;
+    o[2 * nv + g] = sc * zsy;
+    o[3 * nv + g] = sc * zsz;
+  }
+  __syncthreads();
+  for (int idx = t; idx < QP_Q * nv; idx += blockDim.x) {
+    const int qi = idx / nv, k = idx - qi * nv;
+    const int64_t q = q0 + qi;
+    if (q >= nq) continue;
+    const double* v = sv + qi * 4 * nv;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int g = 0; g < nv; ++g) {
+      const double kg = __ldg(m.kinv + (int64_t)g * nv + k);
+      a0 = fma(kg, v[g], a0);
+      a1 = fma(kg, v[nv + g], a1);
+      a2 = fma(kg, v[2 * nv + g], a2);
+      a3 = fma(kg, v[3 * nv + g], a3);
+    }
+    double* o = wt + q * 4 * nv;
+    o[k] = a0;
+    o[nv + k] = a1;
+    o[2 * nv + k] = a2;
+    o[3 * nv + k] = a3;
+  }
+}
+
+// ───────────────────────── contraction: info fields ─────────────────────
+// One warp per query, lane e < 21 owns packed entry e.  The (query, corner) rows
+// are streamed into shared memory with TMA bulk copies (cp.async.bulk, one 16-B
+// aligned superset of the 5880-B / 1680-B row), QI_NBUF deep per warp across query
+// boundaries, completion tracked by mbarrier transaction counts; the warp computes
+// G_c = omega . S_c and H_c,a = d omega_a . S_c from smem while the next rows land.
+constexpr int QC_WARPS = 8;
+constexpr int QI_NBUF = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, int NC, bool GRAD, bool METRIC>
+__global__ void __launch_bounds__(QC_WARPS * 32) k_query_info(int nv, const T* __restrict__ field,
+                                                             const double* __restrict__ axes, int64_t nq,
+                                                             const uint8_t* __restrict__ status,
+                                                             const int32_t* __restrict__ rows,
+                                                             const double4* __restrict__ cw,
+                                                             const double* __restrict__ wt, QueryOut out) {
+  extern __shared__ __align__(128) unsigned char qraw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rw = (int64_t)nv * 21;                               // elements per row
+  const uint32_t rowcap = (uint32_t)(((rw * sizeof(T) + 16) + 15) & ~15ull);  // bytes, incl. alignment slack
+  const uint32_t per_warp = 128 + QI_NBUF * rowcap + (uint32_t)sizeof(double) * (4 * nv + 8 * 21);
+  unsigned char* wbase = qraw + (size_t)warp * ((per_warp + 127) & ~127u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase);                // [QI_NBUF]
+  unsigned char* bufs = wbase + 128;                                   // [QI_NBUF][rowcap]
+  double* wq = reinterpret_cast<double*>(bufs + QI_NBUF * rowcap);     // [4][nv]
+  double* cfim = wq + 4 * nv;                                          // [8][21]
+  if (lane == 0) {
+    for (int b = 0; b < QI_NBUF; ++b) mbar_init(&bars[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const bool on = lane < 21;
+  const int e = on ? lane : 0;
+  const int64_t qstride = (int64_t)gridDim.x * QC_WARPS;
+  const int64_t qfirst = blockIdx.x * (int64_t)QC_WARPS + warp;
+  const int64_t nmine = qfirst < nq ? (nq - qfirst + qstride - 1) / qstride : 0;
+  const int64_t items = nmine * NC;
+  // producer (lane 0): issue item `it` into buffer it % QI_NBUF; byte offset of the
+  // row inside the buffer is returned through `off` of the consumer recomputation.
+  auto issue = [&](int64_t it) {
+    if (lane != 0 || it >= items) return;
+    const int b = (int)(it % QI_NBUF);
+    const int64_t q = qfirst + (it / NC) * qstride;
+    const int c = (int)(it % NC);
+    const int32_t r = status[q] == FIF_STATUS_OK ? rows[q * 8 + c] : -1;
+    if (r < 0) {
+      mbar_arrive(&bars[b]);  // nothing to fetch: complete the phase
+      return;
+    }
+    const char* src = reinterpret_cast<const char*>(field + (int64_t)r * rw);
+    const char* a0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15);
+    const char* a1 = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(src + rw * sizeof(T)) + 15) &
+                                                   ~(uintptr_t)15);
+    const uint32_t bytes = (uint32_t)(a1 - a0);
+    mbar_expect_tx(&bars[b], bytes);
+    tma_bulk_g2s(bufs + (size_t)b * rowcap, a0, bytes, &bars[b]);
+  };
+  for (int64_t it = 0; it < QI_NBUF && it < items; ++it) issue(it);
+  double val = 0, pgx = 0, pgy = 0, pgz = 0, rgx = 0, rgy = 0, rgz = 0;
+  int st = FIF_STATUS_OK;
+  for (int64_t it = 0; it < items; ++it) {
+    const int64_t q = qfirst + (it / NC) * qstride;
+    const int c = (int)(it % NC);
+    const int b = (int)(it % QI_NBUF);
+    const uint32_t parity = (uint32_t)((it / QI_NBUF) & 1);
+    if (c == 0) {
+      st = status[q];
+      val = pgx = pgy = pgz = rgx = rgy = rgz = 0.0;
+      if (st == FIF_STATUS_OK) {
+        const double* wsrc = wt + q * 4 * nv;
+        for (int j = lane; j < (GRAD ? 4 : 1) * nv; j += 32) wq[j] = wsrc[j];
+      }
+      __syncwarp();
+    }
+    const int32_t r = st == FIF_STATUS_OK ? rows[q * 8 + c] : -1;
+    mbar_wait(&bars[b], parity);
+    if (r >= 0) {
+      const T* src = field + (int64_t)r * rw;
+      const uint32_t off = (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15);
+      const T* row = reinterpret_cast<const T*>(bufs + (size_t)b * rowcap + off) + e;
+      double g0a = 0, g0b = 0, g1 = 0, g2 = 0, g3 = 0;
+      if (on) {
+        int k = 0;
+        for (; k + 2 <= nv; k += 2) {
+          const double s0 = (double)row[k * 21], s1 = (double)row[(k + 1) * 21];
+          g0a = fma(wq[k], s0, g0a);
+          g0b = fma(wq[k + 1], s1, g0b);
+          if (GRAD) {
+            g1 = fma(wq[nv + k + 1], s1, fma(wq[nv + k], s0, g1));
+            g2 = fma(wq[2 * nv + k + 1], s1, fma(wq[2 * nv + k], s0, g2));
+            g3 = fma(wq[3 * nv + k + 1], s1, fma(wq[3 * nv + k], s0, g3));
+          }
+        }
+        if (k < nv) {
+          const double s0 = (double)row[k * 21];
+          g0a = fma(wq[k], s0, g0a);
+          if (GRAD) {
+            g1 = fma(wq[nv + k], s0, g1);
+            g2 = fma(wq[2 * nv + k], s0, g2);
+            g3 = fma(wq[3 * nv + k], s0, g3);
+          }
+        }
+      }
+      const double G = g0a + g0b;
+      const double4 d = cw[q * 8 + c];
+      val = fma(d.x, G, val);
+      if (GRAD) {
+        pgx = fma(d.y, G, pgx);
+        pgy = fma(d.z, G, pgy);
+        pgz = fma(d.w, G, pgz);
+        rgx = fma(d.x, g1, rgx);
+        rgy = fma(d.x, g2, rgy);
+        rgz = fma(d.x, g3, rgz);
+      }
+      if (METRIC && on) cfim[c * 21 + lane] = G;
+    } else if (METRIC && on) {
+      cfim[c * 21 + lane] = 0.0;
+    }
+    // all lanes are done with buffer b: refill it with item it + QI_NBUF
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue(it + QI_NBUF);
+    if (c != NC - 1) continue;
+    // ── query complete: outputs ──
+    if (st != FIF_STATUS_OK) {
+      if (out.fim) for (int j = lane; j < 36; j += 32) out.fim[q * 36 + j] = 0.0;
+      if (out.fim_grad) for (int j = lane; j < 216; j += 32) out.fim_grad[q * 216 + j] = 0.0;
       if (lane == 0) {
         if (out.trace) out.trace[q] = 0.0;
         if (out.det) out.det[q] = 0.0;
         if (out.lmin) out.lmin[q] = 0.0;
       }
       if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
+      if (out.status && lane == 0) out.status[q] = (uint8_t)st;
       continue;
     }
-    rotation_weights(m, nv, zx, zy, zz, wt, tmp, lane);
-    // val, d/dt (3), d/dz (3)
-    double val = 0, pgx = 0, pgy = 0, pgz = 0, rgx = 0, rgy = 0, rgz = 0;
-    double mdet = 0, mlmin = 0;
-    if (KIND == FIF_KIND_INFO) {
-      const bool on = lane < 21;
-      const int e = on ? lane : 0;
-      for (int c = 0; c < nc; ++c) {
-        if (rows[c] < 0) {
-          if (METRIC && on) cornerfim[c * 21 + e] = 0.0;
-          continue;  // empty voxel: exact zero factor (field.py:12)
-        }
-        const T* f = field + rows[c] * rw + e;
-        double g0 = 0, g1 = 0, g2 = 0, g3 = 0;
-        if (on) {
-          int k = 0;
-          for (; k + 4 <= nv; k += 4) {
-            double f0 = ld_field(f + (k + 0) * 21), f1 = ld_field(f + (k + 1) * 21);
-            double f2 = ld_field(f + (k + 2) * 21), f3 = ld_field(f + (k + 3) * 21);
-            g0 = fma(wt[k], f0, g0); g0 = fma(wt[k + 1], f1, g0); g0 = fma(wt[k + 2], f2, g0); g0 = fma(wt[k + 3], f3, g0);
-            if (GRAD) {
-              g1 = fma(wt[nv + k], f0, g1); g1 = fma(wt[nv + k + 1], f1, g1);
-              g1 = fma(wt[nv + k + 2], f2, g1); g1 = fma(wt[nv + k + 3], f3, g1);
-              g2 = fma(wt[2 * nv + k], f0, g2); g2 = fma(wt[2 * nv + k + 1], f1, g2);
-              g2 = fma(wt[2 * nv + k + 2], f2, g2); g2 = fma(wt[2 * nv + k + 3], f3, g2);
-              g3 = fma(wt[3 * nv + k], f0, g3); g3 = fma(wt[3 * nv + k + 1], f1, g3);
-              g3 = fma(wt[3 * nv + k + 2], f2, g3); g3 = fma(wt[3 * nv + k + 3], f3, g3);
-            }
-          }
-          for (; k < nv; ++k) {
-            double f0 = ld_field(f + k * 21);
-            g0 = fma(wt[k], f0, g0);
-            if (GRAD) {
-              g1 = fma(wt[nv + k], f0, g1);
-              g2 = fma(wt[2 * nv + k], f0, g2);
-              g3 = fma(wt[3 * nv + k], f0, g3);
-            }
-          }
-        }
-        val = fma(w[c], g0, val);
-        if (GRAD) {
-          pgx = fma(dw[c][0], g0, pgx);
-          pgy = fma(dw[c][1], g0, pgy);
-          pgz = fma(dw[c][2], g0, pgz);
-          rgx = fma(w[c], g1, rgx);
-          rgy = fma(w[c], g2, rgy);
-          rgz = fma(w[c], g3, rgz);
-        }
-        if (METRIC && on) cornerfim[c * 21 + e] = g0;
-      }
-      if (out.fim && lane < 21) {
-        int r = kPackR[lane], cc = kPackC[lane];
-        out.fim[q * 36 + r * 6 + cc] = val;
-        out.fim[q * 36 + cc * 6 + r] = val;
-      }
-      // d/dtheta = z x d/dz
-      const double tgx = zy * rgz - zz * rgy, tgy = zz * rgx - zx * rgz, tgz = zx * rgy - zy * rgx;
-      if (GRAD && out.fim_grad && lane < 21) {
-        int r = kPackR[lane], cc = kPackC[lane];
-        double g[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
-        for (int j = 0; j < 6; ++j) {
-          out.fim_grad[q * 216 + j * 36 + r * 6 + cc] = g[j];
-          out.fim_grad[q * 216 + j * 36 + cc * 6 + r] = g[j];
-        }
-      }
-      if (out.trace || (GRAD && out.trace_grad)) {
-        const bool dg = lane < 21 && kIsDiag[lane];
-        double tv = warp_sum(dg ? val : 0.0);
-        if (out.trace && lane == 0) out.trace[q] = tv;
-        if (GRAD && out.trace_grad) {
-          double g[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
-          for (int j = 0; j < 6; ++j) {
-            double s = warp_sum(dg ? g[j] : 0.0);
-            if (lane == j) out.trace_grad[q * 6 + j] = s;
-          }
-        }
-      }
-      if (METRIC) {
-        __syncwarp();
-        // corner metric by lanes 0..nc-1, blended in the reference's corner order
-        double mv_det = 0, mv_lmin = 0;
-        if (lane < nc) {
-          double a[36];
-          for (int j = 0; j < 21; ++j) {
-            double v = cornerfim[lane * 21 + j];
-            a[kPackR[j] * 6 + kPackC[j]] = v;
-            a[kPackC[j] * 6 + kPackR[j]] = v;
-          }
-          if (rows[lane] >= 0) {
-            if (out.det) mv_det = det6(a);
-            if (out.lmin) mv_lmin = lmin6(a);
-          }
-        }
-        for (int c = 0; c < nc; ++c) {
-          double dd = __shfl_sync(0xffffffffu, mv_det, c), ll = __shfl_sync(0xffffffffu, mv_lmin, c);
-          if (w[c] != 0.0) {
-            mdet = fma(w[c], dd, mdet);
-            mlmin = fma(w[c], ll, mlmin);
-          }
-        }
-        if (lane == 0) {
-          if (out.det) out.det[q] = mdet;
-          if (out.lmin) out.lmin[q] = mlmin;
-        }
-        __syncwarp();
-      }
-    } else {
-      // trace field: lanes over k, 7 per-lane partial sums, warp reduction
-      for (int c = 0; c < nc; ++c) {
-        if (rows[c] < 0) continue;
-        const T* f = field + rows[c] * rw;
-        for (int k = lane; k < nv; k += 32) {
-          double s = ld_field(f + k);
-          double ws = wt[k] * s;
-          val = fma(w[c], ws, val);
-          if (GRAD) {
-            pgx = fma(dw[c][0], ws, pgx);
-            pgy = fma(dw[c][1], ws, pgy);
-            pgz = fma(dw[c][2], ws, pgz);
-            rgx = fma(w[c], wt[nv + k] * s, rgx);
-            rgy = fma(w[c], wt[2 * nv + k] * s, rgy);
-            rgz = fma(w[c], wt[3 * nv + k] * s, rgz);
-          }
-        }
-      }
-      val = warp_sum(val);
-      if (out.trace && lane == 0) out.trace[q] = val;
-      if (GRAD && out.trace_grad) {
-        pgx = warp_sum(pgx); pgy = warp_sum(pgy); pgz = warp_sum(pgz);
-        rgx = warp_sum(rgx); rgy = warp_sum(rgy); rgz = warp_sum(rgz);
-        double g[6] = {pgx, pgy, pgz, zy * rgz - zz * rgy, zz * rgx - zx * rgz, zx * rgy - zy * rgx};
-        if (lane < 6) out.trace_grad[q * 6 + lane] = g[lane];
+    const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+    const double tgx = zy * rgz - zz * rgy, tgy = zz * rgx - zx * rgz, tgz = zx * rgy - zy * rgx;  // z x d/dz
+    if (out.fim && on) {
+      const int pr = kPackR[lane], pc = kPackC[lane];
+      out.fim[q * 36 + pr * 6 + pc] = val;
+      out.fim[q * 36 + pc * 6 + pr] = val;
+    }
+    if (GRAD && out.fim_grad && on) {
+      const int pr = kPackR[lane], pc = kPackC[lane];
+      const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        out.fim_grad[q * 216 + j * 36 + pr * 6 + pc] = g6[j];
+        out.fim_grad[q * 216 + j * 36 + pc * 6 + pr] = g6[j];
       }
     }
-    __syncwarp();
+    if (out.trace || (GRAD && out.trace_grad)) {
+      const bool dg = on && kIsDiag[lane];
+      const double tv = warp_sum(dg ? val : 0.0);
+      if (out.trace && lane == 0) out.trace[q] = tv;
+      if (GRAD && out.trace_grad) {
+        const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const double sgl = warp_sum(dg ? g6[j] : 0.0);
+          if (lane == j) out.trace_grad[q * 6 + j] = sgl;
+        }
+      }
+    }
+    if (METRIC) {
+      __syncwarp();
+      double mv_det = 0, mv_lmin = 0;
+      if (lane < NC) {
+        double a[36];
+        for (int j = 0; j < 21; ++j) {
+          const double v = cfim[lane * 21 + j];
+          a[kPackR[j] * 6 + kPackC[j]] = v;
+          a[kPackC[j] * 6 + kPackR[j]] = v;
+        }
+        if (rows[q * 8 + lane] >= 0) {
+          if (out.det) mv_det = det6(a);
+          if (out.lmin) mv_lmin = lmin6(a);
+        }
+      }
+      double mdet = 0, mlmin = 0;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        const double dd = __shfl_sync(0xffffffffu, mv_det, cc), ll = __shfl_sync(0xffffffffu, mv_lmin, cc);
+        const double wc = cw[q * 8 + cc].x;
+        if (wc != 0.0) {
+          mdet = fma(wc, dd, mdet);
+          mlmin = fma(wc, ll, mlmin);
+        }
+      }
+      if (lane == 0) {
+        if (out.det) out.det[q] = mdet;
+        if (out.lmin) out.lmin[q] = mlmin;
+      }
+      __syncwarp();
+    }
+    if (out.status && lane == 0) out.status[q] = (uint8_t)st;
   }
 }
 
-template <typename T, int KIND, bool GRAD, bool METRIC>
-static int launch_query(const fif_model& m, const QueryGeom& gm, const void* field, const int32_t* slots,
-                        const double* pos, const double* axes, int64_t q, int mode, const QueryOut& out,
-                        cudaStream_t st) {
-  const int nv = m.kind == FIF_MODEL_QUAD ? 10 : m.n_v;
-  size_t smem = sizeof(double) * Q_WARPS * (8 * nv + 8 * 21);
-  auto kern = k_query<T, KIND, GRAD, METRIC>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int64_t need = (q + Q_WARPS - 1) / Q_WARPS;
-  int64_t cap = (int64_t)kSMs * 16;
-  unsigned blocks = (unsigned)(need < cap ? need : cap);
-  if (blocks == 0) blocks = 1;
-  kern<<<blocks, Q_WARPS * 32, smem, st>>>(m, gm, reinterpret_cast<const T*>(field), slots, pos, axes, q,
-                                           mode == FIF_MODE_TRILINEAR, out);
-  FIF_CHECK_LAUNCH("k_query");
+// ───────────────────────── contraction: trace fields ────────────────────
+// Rows of n_v scalars: lanes stride over k, per-lane partial sums, warp reduction.
+template <typename T, int NC, bool GRAD>
+__global__ void __launch_bounds__(QC_WARPS * 32) k_query_trace(int nv, const T* __restrict__ field,
+                                                              const double* __restrict__ axes, int64_t nq,
+                                                              const uint8_t* __restrict__ status,
+                                                              const int32_t* __restrict__ rows,
+                                                              const double4* __restrict__ cw,
+                                                              const double* __restrict__ wt, QueryOut out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t q = blockIdx.x * (int64_t)QC_WARPS + warp; q < nq; q += (int64_t)gridDim.x * QC_WARPS) {
+    const int st = status[q];
+    if (st != FIF_STATUS_OK) {
+      if (lane == 0 && out.trace) out.trace[q] = 0.0;
+      if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
+      if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+      continue;
+    }
+    const double* wq = wt + q * 4 * nv;
+    int32_t r[NC];
+    double w[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      r[c] = rows[q * 8 + c];
+      w[c] = cw[q * 8 + c].x;
+    }
+    double G[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) G[c] = 0.0;
+    double R0 = 0, R1 = 0, R2 = 0;
+    for (int k = lane; k < nv; k += 32) {
+      double s[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) s[c] = r[c] >= 0 ? (double)__ldg(field + (int64_t)r[c] * nv + k) : 0.0;
+      const double om = wq[k];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) G[c] = fma(om, s[c], G[c]);
+      if (GRAD) {
+        double b = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) b = fma(w[c], s[c], b);
+        R0 = fma(wq[nv + k], b, R0);
+        R1 = fma(wq[2 * nv + k], b, R1);
+        R2 = fma(wq[3 * nv + k], b, R2);
+      }
+    }
+    double val = 0, pgx = 0, pgy = 0, pgz = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double g = warp_sum(G[c]);
+      val = fma(w[c], g, val);
+      if (GRAD) {
+        const double4 d = cw[q * 8 + c];
+        pgx = fma(d.y, g, pgx);
+        pgy = fma(d.z, g, pgy);
+        pgz = fma(d.w, g, pgz);
+      }
+    }
+    if (lane == 0 && out.trace) out.trace[q] = val;
+    if (GRAD && out.trace_grad) {
+      R0 = warp_sum(R0);
+      R1 = warp_sum(R1);
+      R2 = warp_sum(R2);
+      const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+      const double g6[6] = {pgx, pgy, pgz, zy * R2 - zz * R1, zz * R0 - zx * R2, zx * R1 - zy * R0};
+      if (lane < 6) out.trace_grad[q * 6 + lane] = g6[lane];
+    }
+    if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+  }
+}
+
+static unsigned query_blocks(int64_t q) {
+  int64_t need = (q + QC_WARPS - 1) / QC_WARPS;
+  int64_t cap = (int64_t)kSMs * 32;
+  return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
+}
+
+template <typename T>
+static int launch_contract(int kind, bool trilinear, bool grad, bool metric, int nv, const void* field,
+                           const double* axes, int64_t q, const uint8_t* status, const int32_t* rows,
+                           const double4* cw, const double* wt, const QueryOut& out, cudaStream_t st) {
+  const T* f = reinterpret_cast<const T*>(field);
+  const unsigned blocks = query_blocks(q);
+  const int threads = QC_WARPS * 32;
+  if (kind == FIF_KIND_TRACE) {
+#define QT(NC, G) k_query_trace<T, NC, G><<<blocks, threads, 0, st>>>(nv, f, axes, q, status, rows, cw, wt, out)
+    if (trilinear) { if (grad) QT(8, true); else QT(8, false); }
+    else { if (grad) QT(1, true); else QT(1, false); }
+#undef QT
+    FIF_CHECK_LAUNCH("k_query_trace");
+    return FIF_OK;
+  }
+  const size_t rw_bytes = (size_t)nv * 21 * sizeof(T);
+  const size_t rowcap = ((rw_bytes + 16) + 15) & ~(size_t)15;
+  const size_t per_warp = 128 + QI_NBUF * rowcap + sizeof(double) * (4 * nv + 8 * 21);
+  const size_t smem = QC_WARPS * ((per_warp + 127) & ~(size_t)127);
+#define QI(NC, G, M)                                                                                      \
+  do {                                                                                                    \
+    auto kern = k_query_info<T, NC, G, M>;                                                                \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                 \
+    kern<<<blocks, threads, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out);                       \
+  } while (0)
+  if (trilinear) {
+    if (metric) { if (grad) QI(8, true, true); else QI(8, false, true); }
+    else { if (grad) QI(8, true, false); else QI(8, false, false); }
+  } else {
+    if (metric) { if (grad) QI(1, true, true); else QI(1, false, true); }
+    else { if (grad) QI(1, true, false); else QI(1, false, false); }
+  }
+#undef QI
+  FIF_CHECK_LAUNCH("k_query_info");
   return FIF_OK;
-}
-
-template <typename T, int KIND>
-static int dispatch_query(bool grad, bool metric, const fif_model& m, const QueryGeom& gm, const void* field,
-                          const int32_t* slots, const double* pos, const double* axes, int64_t q, int mode,
-                          const QueryOut& out, cudaStream_t st) {
-  if (KIND == FIF_KIND_TRACE) {
-    return grad ? launch_query<T, KIND, true, false>(m, gm, field, slots, pos, axes, q, mode, out, st)
-                : launch_query<T, KIND, false, false>(m, gm, field, slots, pos, axes, q, mode, out, st);
-  }
-  if (metric)
-    return grad ? launch_query<T, KIND, true, true>(m, gm, field, slots, pos, axes, q, mode, out, st)
-                : launch_query<T, KIND, false, true>(m, gm, field, slots, pos, axes, q, mode, out, st);
-  return grad ? launch_query<T, KIND, true, false>(m, gm, field, slots, pos, axes, q, mode, out, st)
-              : launch_query<T, KIND, false, false>(m, gm, field, slots, pos, axes, q, mode, out, st);
 }
 
 }  // namespace fif
@@ -441,6 +618,8 @@ extern "C" int fif_query(int factor_kind, const fif_model* model, const fif_grid
   FIF_CHECK_ARG(info || !(d_fim || d_fim_grad || d_det || d_lmin),
                 "fif_query: full FIM / det / lmin need an info field (WrongFactorKind)");
   FIF_CHECK_ARG(grid->voxel_size > 0, "fif_query: voxel_size <= 0");
+  const int nv = model->kind == FIF_MODEL_QUAD ? 10 : model->n_v;
+  FIF_CHECK_ARG(nv >= 1 && nv <= 1024, "fif_query: n_v out of range");
   QueryGeom gm{grid->origin[0], grid->origin[1], grid->origin[2], grid->voxel_size,
                grid->dims[0],   grid->dims[1],   grid->dims[2]};
   QueryOut out{(flags & FIF_Q_TRACE) ? d_trace : nullptr,
@@ -452,16 +631,43 @@ extern "C" int fif_query(int factor_kind, const fif_model* model, const fif_grid
                d_status};
   const bool grad = (flags & FIF_Q_GRAD) && (out.trace_grad || out.fim_grad);
   const bool metric = info && (out.det || out.lmin);
+  const bool trilinear = mode == FIF_MODE_TRILINEAR;
   cudaStream_t st = (cudaStream_t)stream;
-  const bool f64 = model->kind == FIF_MODEL_QUAD || (flags & FIF_Q_FIELD_F64);
-  if (f64) {
-    return info ? dispatch_query<double, FIF_KIND_INFO>(grad, metric, *model, gm, d_field, d_slots, d_positions,
-                                                        d_axes, q, mode, out, st)
-                : dispatch_query<double, FIF_KIND_TRACE>(grad, metric, *model, gm, d_field, d_slots, d_positions,
-                                                         d_axes, q, mode, out, st);
+  // stream-ordered scratch: status, rows, corner weights, rotation weights
+  const size_t b_status = ((size_t)q + 255) & ~(size_t)255;
+  const size_t b_rows = (size_t)q * 8 * sizeof(int32_t);
+  const size_t b_cw = (size_t)q * 8 * sizeof(double4);
+  const size_t b_wt = (size_t)q * 4 * nv * sizeof(double);
+  static bool pool_set = false;
+  if (!pool_set) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set = true;
   }
-  return info ? dispatch_query<float, FIF_KIND_INFO>(grad, metric, *model, gm, d_field, d_slots, d_positions, d_axes,
-                                                     q, mode, out, st)
-              : dispatch_query<float, FIF_KIND_TRACE>(grad, metric, *model, gm, d_field, d_slots, d_positions,
-                                                      d_axes, q, mode, out, st);
+  unsigned char* scratch = nullptr;
+  if (cudaMallocAsync(&scratch, b_status + b_rows + b_cw + b_wt + 256, st) != cudaSuccess) {
+    set_error("fif_query: cudaMallocAsync of %zu bytes failed", b_status + b_rows + b_cw + b_wt);
+    return FIF_ERR_CUDA;
+  }
+  uint8_t* s_status = scratch;
+  double4* s_cw = reinterpret_cast<double4*>(scratch + b_status);
+  int32_t* s_rows = reinterpret_cast<int32_t*>(scratch + b_status + b_cw);
+  double* s_wt = reinterpret_cast<double*>(scratch + b_status + b_cw + ((b_rows + 255) & ~(size_t)255));
+  const size_t prep_smem = sizeof(double) * QP_Q * 4 * nv;
+  if (prep_smem > 48 * 1024) cudaFuncSetAttribute(k_query_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem);
+  k_query_prep<<<(unsigned)((q + QP_Q - 1) / QP_Q), QP_THREADS, prep_smem, st>>>(
+      *model, gm, d_slots, d_positions, d_axes, q, trilinear ? 1 : 0, s_status, s_rows, s_cw, s_wt);
+  FIF_CHECK_LAUNCH("k_query_prep");
+  const bool f64 = model->kind == FIF_MODEL_QUAD || (flags & FIF_Q_FIELD_F64);
+  int rc = f64 ? launch_contract<double>(factor_kind, trilinear, grad, metric, nv, d_field, d_axes, q, s_status,
+                                         s_rows, s_cw, s_wt, out, st)
+               : launch_contract<float>(factor_kind, trilinear, grad, metric, nv, d_field, d_axes, q, s_status,
+                                        s_rows, s_cw, s_wt, out, st);
+  cudaFreeAsync(scratch, st);
+  return rc;
 }
