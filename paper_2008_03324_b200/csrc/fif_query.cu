@@ -262,7 +262,8 @@ __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeo
 // boundaries, completion tracked by mbarrier transaction counts; the warp computes
 // G_c = omega . S_c and H_c,a = d omega_a . S_c from smem while the next rows land.
 constexpr int QC_WARPS = 8;
-constexpr int QI_NBUF = 4;
+constexpr int QI_NBUF = 2;
+constexpr int QI_CG = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -292,194 +293,227 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       : "memory");
 }
 
+// Block-cooperative contraction: the NC corner rows and the rotation weights of
+// one query land in shared memory with TMA bulk copies (one mbarrier transaction);
+// the block's 8 warps split the k (sample) range, lane e < 21 owns packed entry e,
+// so every weight is read once per block per query and reused for all NC corners.
+// Per-warp partials (G_c, R_a) are reduced through shared memory by warp 0, which
+// also writes the outputs; the next query's rows are in flight meanwhile.
+constexpr int QB_WARPS = 8;
+
 template <typename T, int NC, bool GRAD, bool METRIC>
-__global__ void __launch_bounds__(QC_WARPS * 32) k_query_info(int nv, const T* __restrict__ field,
+__global__ void __launch_bounds__(QB_WARPS * 32, 3) k_query_info(int nv, const T* __restrict__ field,
                                                              const double* __restrict__ axes, int64_t nq,
                                                              const uint8_t* __restrict__ status,
                                                              const int32_t* __restrict__ rows,
                                                              const double4* __restrict__ cw,
                                                              const double* __restrict__ wt, QueryOut out) {
+  constexpr int NP = NC + 3;  // partials per lane: G_0..G_{NC-1}, R0, R1, R2
   extern __shared__ __align__(128) unsigned char qraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t rw = (int64_t)nv * 21;                               // elements per row
-  const uint32_t rowcap = (uint32_t)(((rw * sizeof(T) + 16) + 15) & ~15ull);  // bytes, incl. alignment slack
-  const uint32_t per_warp = 128 + QI_NBUF * rowcap + (uint32_t)sizeof(double) * (4 * nv + 8 * 21);
-  unsigned char* wbase = qraw + (size_t)warp * ((per_warp + 127) & ~127u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase);                // [QI_NBUF]
-  unsigned char* bufs = wbase + 128;                                   // [QI_NBUF][rowcap]
-  double* wq = reinterpret_cast<double*>(bufs + QI_NBUF * rowcap);     // [4][nv]
-  double* cfim = wq + 4 * nv;                                          // [8][21]
-  if (lane == 0) {
-    for (int b = 0; b < QI_NBUF; ++b) mbar_init(&bars[b], 1);
+  const int64_t rw = (int64_t)nv * 21;
+  const uint32_t rowcap = (uint32_t)(((rw * sizeof(T) + 16) + 15) & ~15ull);
+  const uint32_t wbytes = (uint32_t)(4 * nv * sizeof(double));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(qraw);
+  unsigned char* rbuf = qraw + 128;                                        // [NC][rowcap]
+  double* wq = reinterpret_cast<double*>(rbuf + (size_t)NC * rowcap);      // [4][nv]
+  double* part = wq + 4 * nv;                                              // [QB_WARPS][NP][32]
+  double* cfim = part + QB_WARPS * NP * 32;                                // [8][21]
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncwarp();
-  const bool on = lane < 21;
-  const int e = on ? lane : 0;
-  const int64_t qstride = (int64_t)gridDim.x * QC_WARPS;
-  const int64_t qfirst = blockIdx.x * (int64_t)QC_WARPS + warp;
-  const int64_t nmine = qfirst < nq ? (nq - qfirst + qstride - 1) / qstride : 0;
-  const int64_t items = nmine * NC;
-  // producer (lane 0): issue item `it` into buffer it % QI_NBUF; byte offset of the
-  // row inside the buffer is returned through `off` of the consumer recomputation.
-  auto issue = [&](int64_t it) {
-    if (lane != 0 || it >= items) return;
-    const int b = (int)(it % QI_NBUF);
-    const int64_t q = qfirst + (it / NC) * qstride;
-    const int c = (int)(it % NC);
-    const int32_t r = status[q] == FIF_STATUS_OK ? rows[q * 8 + c] : -1;
-    if (r < 0) {
-      mbar_arrive(&bars[b]);  // nothing to fetch: complete the phase
-      return;
-    }
+  __syncthreads();
+  auto row_src = [&](int32_t r, uint32_t& bytes, uint32_t& off) -> const char* {
     const char* src = reinterpret_cast<const char*>(field + (int64_t)r * rw);
     const char* a0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15);
-    const char* a1 = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(src + rw * sizeof(T)) + 15) &
-                                                   ~(uintptr_t)15);
-    const uint32_t bytes = (uint32_t)(a1 - a0);
-    mbar_expect_tx(&bars[b], bytes);
-    tma_bulk_g2s(bufs + (size_t)b * rowcap, a0, bytes, &bars[b]);
+    const uintptr_t end = (reinterpret_cast<uintptr_t>(src + rw * sizeof(T)) + 15) & ~(uintptr_t)15;
+    bytes = (uint32_t)(end - reinterpret_cast<uintptr_t>(a0));
+    off = (uint32_t)(src - a0);
+    return a0;
   };
-  for (int64_t it = 0; it < QI_NBUF && it < items; ++it) issue(it);
-  double val = 0, pgx = 0, pgy = 0, pgz = 0, rgx = 0, rgy = 0, rgz = 0;
-  int st = FIF_STATUS_OK;
-  for (int64_t it = 0; it < items; ++it) {
-    const int64_t q = qfirst + (it / NC) * qstride;
-    const int c = (int)(it % NC);
-    const int b = (int)(it % QI_NBUF);
-    const uint32_t parity = (uint32_t)((it / QI_NBUF) & 1);
-    if (c == 0) {
-      st = status[q];
-      val = pgx = pgy = pgz = rgx = rgy = rgz = 0.0;
-      if (st == FIF_STATUS_OK) {
-        const double* wsrc = wt + q * 4 * nv;
-        for (int j = lane; j < (GRAD ? 4 : 1) * nv; j += 32) wq[j] = wsrc[j];
-      }
-      __syncwarp();
+  auto issue = [&](int64_t q) {  // thread 0 only
+    if (q >= nq) return;
+    const bool ok = status[q] == FIF_STATUS_OK;
+    uint32_t total = 0;
+    for (int c = 0; c < NC; ++c) {
+      const int32_t r = ok ? rows[q * 8 + c] : -1;
+      if (r < 0) continue;
+      uint32_t bytes, off;
+      row_src(r, bytes, off);
+      total += bytes;
     }
-    const int32_t r = st == FIF_STATUS_OK ? rows[q * 8 + c] : -1;
-    mbar_wait(&bars[b], parity);
-    if (r >= 0) {
-      const T* src = field + (int64_t)r * rw;
-      const uint32_t off = (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15);
-      const T* row = reinterpret_cast<const T*>(bufs + (size_t)b * rowcap + off) + e;
-      double g0a = 0, g0b = 0, g1 = 0, g2 = 0, g3 = 0;
-      if (on) {
-        int k = 0;
-        for (; k + 2 <= nv; k += 2) {
-          const double s0 = (double)row[k * 21], s1 = (double)row[(k + 1) * 21];
-          g0a = fma(wq[k], s0, g0a);
-          g0b = fma(wq[k + 1], s1, g0b);
-          if (GRAD) {
-            g1 = fma(wq[nv + k + 1], s1, fma(wq[nv + k], s0, g1));
-            g2 = fma(wq[2 * nv + k + 1], s1, fma(wq[2 * nv + k], s0, g2));
-            g3 = fma(wq[3 * nv + k + 1], s1, fma(wq[3 * nv + k], s0, g3));
+    if (ok) total += (GRAD ? 4 : 1) * (uint32_t)(nv * sizeof(double));
+    if (total == 0) {
+      mbar_arrive(bar);
+      return;
+    }
+    mbar_expect_tx(bar, total);
+    if (ok) tma_bulk_g2s(wq, wt + q * 4 * nv, (GRAD ? 4 : 1) * (uint32_t)(nv * sizeof(double)), bar);
+    for (int c = 0; c < NC; ++c) {
+      const int32_t r = ok ? rows[q * 8 + c] : -1;
+      if (r < 0) continue;
+      uint32_t bytes, off;
+      const char* a0 = row_src(r, bytes, off);
+      tma_bulk_g2s(rbuf + (size_t)c * rowcap, a0, bytes, bar);
+    }
+  };
+  (void)wbytes;
+  const bool on = lane < 21;
+  const int e = on ? lane : 0;
+  const int kper = (nv + QB_WARPS - 1) / QB_WARPS;
+  const int k0 = warp * kper, k1 = min(nv, k0 + kper);
+  uint32_t phase = 0;
+  if (threadIdx.x == 0) issue(blockIdx.x);
+  for (int64_t q = blockIdx.x; q < nq; q += gridDim.x, phase ^= 1u) {
+    const int st = status[q];
+    int32_t r[NC];
+    const T* rp[NC];
+    double w[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      r[c] = st == FIF_STATUS_OK ? rows[q * 8 + c] : -1;
+      w[c] = r[c] >= 0 ? cw[q * 8 + c].x : 0.0;
+      uint32_t bytes = 0, off = 0;
+      if (r[c] >= 0) row_src(r[c], bytes, off);
+      rp[c] = reinterpret_cast<const T*>(rbuf + (size_t)c * rowcap + off) + e;
+    }
+    mbar_wait(bar, phase);
+    double G[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) G[c] = 0.0;
+    double R0 = 0, R1 = 0, R2 = 0;
+    if (on && st == FIF_STATUS_OK) {
+#pragma unroll 2
+      for (int k = k0; k < k1; ++k) {
+        double sv[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sv[c] = r[c] >= 0 ? (double)rp[c][k * 21] : 0.0;
+        const double om = wq[k];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) G[c] = fma(om, sv[c], G[c]);
+        if (GRAD) {
+          double bl = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) bl = fma(w[c], sv[c], bl);
+          R0 = fma(wq[nv + k], bl, R0);
+          R1 = fma(wq[2 * nv + k], bl, R1);
+          R2 = fma(wq[3 * nv + k], bl, R2);
+        }
+      }
+    }
+    double* pw = part + (size_t)warp * NP * 32;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) pw[c * 32 + lane] = G[c];
+    if (GRAD) {
+      pw[NC * 32 + lane] = R0;
+      pw[(NC + 1) * 32 + lane] = R1;
+      pw[(NC + 2) * 32 + lane] = R2;
+    }
+    __syncthreads();  // rows / weights consumed, partials visible
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(q + gridDim.x);
+    }
+    if (warp == 0) {
+      double Gs[NC];
+      double S0 = 0, S1 = 0, S2 = 0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) Gs[c] = 0.0;
+      for (int ww = 0; ww < QB_WARPS; ++ww) {
+        const double* p = part + (size_t)ww * NP * 32;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) Gs[c] += p[c * 32 + lane];
+        if (GRAD) {
+          S0 += p[NC * 32 + lane];
+          S1 += p[(NC + 1) * 32 + lane];
+          S2 += p[(NC + 2) * 32 + lane];
+        }
+      }
+      double val = 0, pgx = 0, pgy = 0, pgz = 0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        val = fma(w[c], Gs[c], val);
+        if (GRAD && r[c] >= 0) {
+          const double4 d = cw[q * 8 + c];
+          pgx = fma(d.y, Gs[c], pgx);
+          pgy = fma(d.z, Gs[c], pgy);
+          pgz = fma(d.w, Gs[c], pgz);
+        }
+        if (METRIC && on) cfim[c * 21 + lane] = Gs[c];
+      }
+      if (st != FIF_STATUS_OK) {
+        if (out.fim) for (int j = lane; j < 36; j += 32) out.fim[q * 36 + j] = 0.0;
+        if (out.fim_grad) for (int j = lane; j < 216; j += 32) out.fim_grad[q * 216 + j] = 0.0;
+        if (lane == 0) {
+          if (out.trace) out.trace[q] = 0.0;
+          if (out.det) out.det[q] = 0.0;
+          if (out.lmin) out.lmin[q] = 0.0;
+        }
+        if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
+      } else {
+        const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+        const double tgx = zy * S2 - zz * S1, tgy = zz * S0 - zx * S2, tgz = zx * S1 - zy * S0;  // z x d/dz
+        if (out.fim && on) {
+          const int pr = kPackR[lane], pc = kPackC[lane];
+          out.fim[q * 36 + pr * 6 + pc] = val;
+          out.fim[q * 36 + pc * 6 + pr] = val;
+        }
+        if (GRAD && out.fim_grad && on) {
+          const int pr = kPackR[lane], pc = kPackC[lane];
+          const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
+#pragma unroll
+          for (int j = 0; j < 6; ++j) {
+            out.fim_grad[q * 216 + j * 36 + pr * 6 + pc] = g6[j];
+            out.fim_grad[q * 216 + j * 36 + pc * 6 + pr] = g6[j];
           }
         }
-        if (k < nv) {
-          const double s0 = (double)row[k * 21];
-          g0a = fma(wq[k], s0, g0a);
-          if (GRAD) {
-            g1 = fma(wq[nv + k], s0, g1);
-            g2 = fma(wq[2 * nv + k], s0, g2);
-            g3 = fma(wq[3 * nv + k], s0, g3);
+        if (out.trace || (GRAD && out.trace_grad)) {
+          const bool dg = on && kIsDiag[lane];
+          const double tv = warp_sum(dg ? val : 0.0);
+          if (out.trace && lane == 0) out.trace[q] = tv;
+          if (GRAD && out.trace_grad) {
+            const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
+#pragma unroll
+            for (int j = 0; j < 6; ++j) {
+              const double sgl = warp_sum(dg ? g6[j] : 0.0);
+              if (lane == j) out.trace_grad[q * 6 + j] = sgl;
+            }
+          }
+        }
+        if (METRIC) {
+          __syncwarp();
+          double mv_det = 0, mv_lmin = 0;
+          if (lane < NC) {
+            double a[36];
+            for (int j = 0; j < 21; ++j) {
+              const double v = cfim[lane * 21 + j];
+              a[kPackR[j] * 6 + kPackC[j]] = v;
+              a[kPackC[j] * 6 + kPackR[j]] = v;
+            }
+            if (rows[q * 8 + lane] >= 0) {
+              if (out.det) mv_det = det6(a);
+              if (out.lmin) mv_lmin = lmin6(a);
+            }
+          }
+          double mdet = 0, mlmin = 0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double dd = __shfl_sync(0xffffffffu, mv_det, c), ll = __shfl_sync(0xffffffffu, mv_lmin, c);
+            if (w[c] != 0.0) {
+              mdet = fma(w[c], dd, mdet);
+              mlmin = fma(w[c], ll, mlmin);
+            }
+          }
+          if (lane == 0) {
+            if (out.det) out.det[q] = mdet;
+            if (out.lmin) out.lmin[q] = mlmin;
           }
         }
       }
-      const double G = g0a + g0b;
-      const double4 d = cw[q * 8 + c];
-      val = fma(d.x, G, val);
-      if (GRAD) {
-        pgx = fma(d.y, G, pgx);
-        pgy = fma(d.z, G, pgy);
-        pgz = fma(d.w, G, pgz);
-        rgx = fma(d.x, g1, rgx);
-        rgy = fma(d.x, g2, rgy);
-        rgz = fma(d.x, g3, rgz);
-      }
-      if (METRIC && on) cfim[c * 21 + lane] = G;
-    } else if (METRIC && on) {
-      cfim[c * 21 + lane] = 0.0;
-    }
-    // all lanes are done with buffer b: refill it with item it + QI_NBUF
-    __syncwarp();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    issue(it + QI_NBUF);
-    if (c != NC - 1) continue;
-    // ── query complete: outputs ──
-    if (st != FIF_STATUS_OK) {
-      if (out.fim) for (int j = lane; j < 36; j += 32) out.fim[q * 36 + j] = 0.0;
-      if (out.fim_grad) for (int j = lane; j < 216; j += 32) out.fim_grad[q * 216 + j] = 0.0;
-      if (lane == 0) {
-        if (out.trace) out.trace[q] = 0.0;
-        if (out.det) out.det[q] = 0.0;
-        if (out.lmin) out.lmin[q] = 0.0;
-      }
-      if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
       if (out.status && lane == 0) out.status[q] = (uint8_t)st;
-      continue;
     }
-    const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
-    const double tgx = zy * rgz - zz * rgy, tgy = zz * rgx - zx * rgz, tgz = zx * rgy - zy * rgx;  // z x d/dz
-    if (out.fim && on) {
-      const int pr = kPackR[lane], pc = kPackC[lane];
-      out.fim[q * 36 + pr * 6 + pc] = val;
-      out.fim[q * 36 + pc * 6 + pr] = val;
-    }
-    if (GRAD && out.fim_grad && on) {
-      const int pr = kPackR[lane], pc = kPackC[lane];
-      const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        out.fim_grad[q * 216 + j * 36 + pr * 6 + pc] = g6[j];
-        out.fim_grad[q * 216 + j * 36 + pc * 6 + pr] = g6[j];
-      }
-    }
-    if (out.trace || (GRAD && out.trace_grad)) {
-      const bool dg = on && kIsDiag[lane];
-      const double tv = warp_sum(dg ? val : 0.0);
-      if (out.trace && lane == 0) out.trace[q] = tv;
-      if (GRAD && out.trace_grad) {
-        const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          const double sgl = warp_sum(dg ? g6[j] : 0.0);
-          if (lane == j) out.trace_grad[q * 6 + j] = sgl;
-        }
-      }
-    }
-    if (METRIC) {
-      __syncwarp();
-      double mv_det = 0, mv_lmin = 0;
-      if (lane < NC) {
-        double a[36];
-        for (int j = 0; j < 21; ++j) {
-          const double v = cfim[lane * 21 + j];
-          a[kPackR[j] * 6 + kPackC[j]] = v;
-          a[kPackC[j] * 6 + kPackR[j]] = v;
-        }
-        if (rows[q * 8 + lane] >= 0) {
-          if (out.det) mv_det = det6(a);
-          if (out.lmin) mv_lmin = lmin6(a);
-        }
-      }
-      double mdet = 0, mlmin = 0;
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        const double dd = __shfl_sync(0xffffffffu, mv_det, cc), ll = __shfl_sync(0xffffffffu, mv_lmin, cc);
-        const double wc = cw[q * 8 + cc].x;
-        if (wc != 0.0) {
-          mdet = fma(wc, dd, mdet);
-          mlmin = fma(wc, ll, mlmin);
-        }
-      }
-      if (lane == 0) {
-        if (out.det) out.det[q] = mdet;
-        if (out.lmin) out.lmin[q] = mlmin;
-      }
-      __syncwarp();
-    }
-    if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+    __syncthreads();  // partials consumed before the next query overwrites them
   }
 }
 
@@ -577,14 +611,19 @@ static int launch_contract(int kind, bool trilinear, bool grad, bool metric, int
   }
   const size_t rw_bytes = (size_t)nv * 21 * sizeof(T);
   const size_t rowcap = ((rw_bytes + 16) + 15) & ~(size_t)15;
-  const size_t per_warp = 128 + QI_NBUF * rowcap + sizeof(double) * (4 * nv + 8 * 21);
-  const size_t smem = QC_WARPS * ((per_warp + 127) & ~(size_t)127);
+  const int nc = trilinear ? 8 : 1;
+  const size_t smem = 128 + nc * rowcap + sizeof(double) * (4 * nv + QB_WARPS * (nc + 3) * 32 + 8 * 21);
+  FIF_CHECK_ARG(smem <= 220 * 1024, "fif_query: a %zu-byte field row does not fit the shared-memory pipeline",
+                rw_bytes);
+  const int per_sm = (int)((228 * 1024) / (smem + 1024));
+  int64_t cap = (int64_t)kSMs * (per_sm > 0 ? per_sm : 1);
+  const unsigned blocks_i = (unsigned)(q < cap ? q : cap);
 #define QI(NC, G, M)                                                                                      \
   do {                                                                                                    \
     auto kern = k_query_info<T, NC, G, M>;                                                                \
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                 \
-    kern<<<blocks, threads, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out);                       \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                   \
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                      \
+    kern<<<blocks_i, QB_WARPS * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out);              \
   } while (0)
   if (trilinear) {
     if (metric) { if (grad) QI(8, true, true); else QI(8, false, true); }
