@@ -51,6 +51,7 @@ extern "C" {
 #define FIF_Q_FIELD_F64 32u /* GP field operand is the FP64 S array instead of the FP32 copy     */
 /* fif_build flags */
 #define FIF_BUILD_EXACT 1u  /* quad: reproduce _nb_build_quad's FP64 operation order bit for bit     */
+#define FIF_BUILD_SIMT 2u   /* GP info: FP32 SIMT (FFMA2) kernel instead of the tensor-pipe kernel   */
 
 /* Axis-aligned voxel grid (field.py:45-98 GridConfig). */
 typedef struct fif_grid {

@@ -665,6 +665,205 @@ k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc s
   }
 }
 
+// ─────────────────────────── GP, info on the tensor pipe ────────────────
+// S_v[g][e] = sum_j vs_v(j, g) E_v(j, e) is, per voxel, a (samples x landmarks) x
+// (landmarks x entries) matrix product whose A operand (the sigmoids) is generated
+// on the fly.  Each warp owns one voxel and up to 5 m16 sample tiles; per k-step of
+// 8 landmarks a lane evaluates 4 sigmoids per m-tile (exactly the A-fragment entries
+// it holds: no redundant MUFU work) and the warp issues mma.sync m16n8k8 TF32 with a
+// 3-term split (hi*hi + hi*lo + lo*hi ~ FP32 products) into FP32 accumulators that are
+// flushed to FP64 (shared memory) every GC_FLUSH landmarks.  B fragments (entries,
+// pre-split into TF32 hi/lo by phase A) are read from a bank-conflict-free layout.
+constexpr int GC_TILE = 64;       // landmarks per smem tile
+constexpr int GC_FLUSH_TILES = 2; // FP32 accumulators span 128 landmarks
+constexpr int GC_MT = 5;          // m16 tiles per warp (80 samples)
+constexpr int GC_WARPS = 4;
+constexpr int GC_NT = 3;          // n8 tiles (24 >= 21 entries)
+
+// TF32 split by truncation (1 LOP3; cvt.rna.tf32 costs ~5 instructions on sm_100):
+// hi keeps 10 explicit mantissa bits, lo = x - hi is exact in FP32 and is truncated
+// again, so hi + lo == x to 2^-22 relative.
+__device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+  hi = tf32_hi(x);
+  lo = tf32_hi(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <bool HAS_MASK>
+__global__ void __launch_bounds__(GC_WARPS * 32, 2)
+k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1,
+             int ns, int wpv, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax,
+             float bx, double* __restrict__ out64, float* __restrict__ out32) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int vpc = GC_WARPS / wpv;                                   // voxels per CTA
+  float* eh = reinterpret_cast<float*>(smem_raw);                   // [vpc][GC_TILE][24] entries (FP32)
+  float4* uu = reinterpret_cast<float4*>(eh + vpc * GC_TILE * 24);  // [vpc][GC_TILE] bearings
+  float4* tile = uu + vpc * GC_TILE;                                // [GC_TILE][2] landmarks
+  float* cs = reinterpret_cast<float*>(tile + GC_TILE * 2);         // [vpc][6] centre hi/lo
+  double* acc = reinterpret_cast<double*>(cs + ((6 * vpc + 1) & ~1));  // [GC_WARPS][GC_MT*GC_NT*4][32]
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int vl = warp / wpv, mg = warp - vl * wpv;
+  const int64_t vbase = v0 + blockIdx.x * (int64_t)vpc;
+  const int64_t myv = vbase + vl;
+  if (t < vpc) {
+    const int64_t v = vbase + t;
+    float ch[3], cl[3];
+    voxel_split(src, v < v1 ? v : v0, ch, cl);
+    for (int k = 0; k < 3; ++k) {
+      cs[6 * t + k] = ch[k];
+      cs[6 * t + 3 + k] = cl[k];
+    }
+  }
+  double* myacc = acc + (size_t)warp * GC_MT * GC_NT * 4 * 32;
+  for (int i = 0; i < GC_MT * GC_NT * 4; ++i) myacc[i * 32 + lane] = 0.0;
+  // sample directions of this lane's A rows: rows gid and gid+8 of each m-tile; folded
+  // into the exponent argument x = (ax z) . u + bx
+  float zr[GC_MT][2][3];
+#pragma unroll
+  for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = (mg * GC_MT + m) * 16 + gid + 8 * h;
+      const bool ok = g < ns;
+      zr[m][h][0] = ok ? (float)(ax * zs[3 * g]) : 0.f;
+      zr[m][h][1] = ok ? (float)(ax * zs[3 * g + 1]) : 0.f;
+      zr[m][h][2] = ok ? (float)(ax * zs[3 * g + 2]) : 0.f;
+    }
+  float c[GC_MT][GC_NT][4];
+#pragma unroll
+  for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+    for (int n = 0; n < GC_NT; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[m][n][i] = 0.f;
+  const int npairs = vpc * GC_TILE;
+  int tiles = 0;
+  for (int64_t base = 0; base < n_pad; base += GC_TILE) {
+    __syncthreads();
+    for (int j = t; j < GC_TILE * 2; j += blockDim.x) tile[j] = lm[2 * base + j];
+    __syncthreads();
+    // phase A: per (voxel, landmark) bearing + 21 entries, entries split to TF32 hi/lo
+    for (int pidx = t; pidx < npairs; pidx += blockDim.x) {
+      const int pv = pidx / GC_TILE, pj = pidx - pv * GC_TILE;
+      float4 a = tile[2 * pj], b = tile[2 * pj + 1];
+      if ((vbase + pv) >= v1) b.w = 0.f;
+      if (HAS_MASK) {
+        const int64_t i = base + pj;
+        if (b.w != 0.f && mask[(vbase + pv - v0) * n_real + i] == 0) b.w = 0.f;
+      }
+      const float* cc = cs + 6 * pv;
+      const float ch[3] = {cc[0], cc[1], cc[2]}, cl[3] = {cc[3], cc[4], cc[5]};
+      const PairF q = pair_prologue(a, b, ch, cl, inv_s2);
+      float e[21];
+      entries21(q, a, e);
+      float4* dh = reinterpret_cast<float4*>(eh + (pv * GC_TILE + pj) * 24);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) dh[k] = make_float4(e[4 * k], e[4 * k + 1], e[4 * k + 2], e[4 * k + 3]);
+      dh[5] = make_float4(e[20], 0.f, 0.f, 0.f);
+      uu[pv * GC_TILE + pj] = make_float4(q.ux, q.uy, q.uz, 0.f);
+    }
+    __syncthreads();
+    if (vl < vpc) {
+      const float* ehv = eh + vl * GC_TILE * 24;
+      const float4* uv = uu + vl * GC_TILE;
+      // A fragments (TF32 hi/lo) for one k-step: all 20 sigmoid chains of the 5 m-tiles
+      // are independent, so their MUFU latencies overlap; the next k-step's fragments are
+      // computed while the tensor pipe works through this step's 45 MMAs.
+      // a0 (row gid, col tig), a1 (row gid+8, col tig), a2 (row gid, col tig+4), a3 (row gid+8, col tig+4)
+      // sigmoids of m-tile m for landmarks k0 + {tig, tig+4}, split to TF32 hi/lo
+      auto afrag_m = [&](int k0, int m, uint32_t (&ah)[4], uint32_t (&al)[4]) {
+        const float4 u0 = uv[k0 + tig], u1 = uv[k0 + tig + 4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int h = i & 1;
+          const float4 u = (i < 2) ? u0 : u1;
+          const float x = fmaf(u.x, zr[m][h][0], fmaf(u.y, zr[m][h][1], fmaf(u.z, zr[m][h][2], bx)));
+          tf32_split(rcp_approx(1.0f + ex2_approx(x)), ah[i], al[i]);
+        }
+      };
+      uint32_t ah[GC_MT][4], al[GC_MT][4];
+#pragma unroll
+      for (int m = 0; m < GC_MT; ++m) afrag_m(0, m, ah[m], al[m]);
+#pragma unroll 1
+      for (int k0 = 0; k0 < GC_TILE; k0 += 8) {
+        // B fragments: rows (landmarks) k0+tig, k0+tig+4; column (entry) 8n + gid
+        // (each (landmark, entry) element is held by exactly one lane: split here, once)
+        uint32_t bh[GC_NT][2], bl[GC_NT][2];
+#pragma unroll
+        for (int n = 0; n < GC_NT; ++n) {
+          tf32_split(ehv[(k0 + tig) * 24 + 8 * n + gid], bh[n][0], bl[n][0]);
+          tf32_split(ehv[(k0 + tig + 4) * 24 + 8 * n + gid], bh[n][1], bl[n][1]);
+        }
+        const int kn = (k0 + 8) & (GC_TILE - 1);  // next step (wraps harmlessly on the last)
+        uint32_t nh[GC_MT][4], nl[GC_MT][4];
+        // The MMA passes (15 accumulators each, so dependent MMAs are 15 apart) are
+        // interleaved with the next step's sigmoid chains so the MUFU pipe and the
+        // tensor pipe work at the same time inside one warp.
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int n = 0; n < GC_NT; ++n) mma_tf32(c[m][n], ah[m], bh[n][0], bh[n][1]);
+        afrag_m(kn, 0, nh[0], nl[0]);
+        afrag_m(kn, 1, nh[1], nl[1]);
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int n = 0; n < GC_NT; ++n) mma_tf32(c[m][n], ah[m], bl[n][0], bl[n][1]);
+        afrag_m(kn, 2, nh[2], nl[2]);
+        afrag_m(kn, 3, nh[3], nl[3]);
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int n = 0; n < GC_NT; ++n) mma_tf32(c[m][n], al[m], bh[n][0], bh[n][1]);
+        afrag_m(kn, 4, nh[4], nl[4]);
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            ah[m][i] = nh[m][i];
+            al[m][i] = nl[m][i];
+          }
+      }
+      if (++tiles == GC_FLUSH_TILES || base + GC_TILE >= n_pad) {
+        tiles = 0;
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int n = 0; n < GC_NT; ++n)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              myacc[((m * GC_NT + n) * 4 + i) * 32 + lane] += (double)c[m][n][i];
+              c[m][n][i] = 0.f;
+            }
+      }
+    }
+  }
+  if (vl < vpc && myv < v1) {
+    const int64_t r = myv - v0;
+    // C fragment: c0 (row gid, col 2tig), c1 (row gid, col 2tig+1), c2 (row gid+8, 2tig), c3 (row gid+8, 2tig+1)
+#pragma unroll
+    for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+      for (int n = 0; n < GC_NT; ++n)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int g = (mg * GC_MT + m) * 16 + gid + ((i >> 1) << 3);
+          const int en = 8 * n + 2 * tig + (i & 1);
+          if (g >= ns || en >= 21) continue;
+          const double v = myacc[((m * GC_NT + n) * 4 + i) * 32 + lane];
+          out64[(r * ns + g) * 21 + en] = v;
+          if (out32) out32[(r * ns + g) * 21 + en] = (float)v;
+        }
+  }
+}
+
 // ─────────────────────────── exports ───────────────────────────────────
 // Expand packed (rows, nv, 21) to the reference's (rows, nv*36).
 __global__ void k_expand36(const double* __restrict__ in, int64_t blocks, double* __restrict__ out) {
@@ -817,6 +1016,31 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
       k_gp_trace<false><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns,
                                                            model->zs, d_mask, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
+  } else if (!(build_flags & FIF_BUILD_SIMT)) {
+    // tensor-pipe path (mma.sync TF32x3): a warp covers 80 samples of one voxel
+    const int wpv = (ns + 16 * GC_MT - 1) / (16 * GC_MT);
+    FIF_CHECK_ARG(wpv >= 1 && wpv <= GC_WARPS, "fif_build: N_s=%d too large for k_gp_info_tc", ns);
+    const int vpc = GC_WARPS / wpv;
+    const unsigned blocks_c = (unsigned)((rows + vpc - 1) / vpc);
+    size_t smem = sizeof(float) * (vpc * GC_TILE * 24) + sizeof(float4) * (vpc * GC_TILE + GC_TILE * 2) +
+                  sizeof(float) * ((6 * vpc + 1) & ~1) + sizeof(double) * GC_WARPS * GC_MT * GC_NT * 4 * 32;
+    static bool carve_tc = false;
+    if (!carve_tc) {
+      for (auto f : {k_gp_info_tc<true>, k_gp_info_tc<false>}) {
+        cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      }
+      carve_tc = true;
+    }
+    if (has_mask)
+      k_gp_info_tc<true><<<blocks_c, GC_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv,
+                                                                 model->zs, d_mask, (float)inv_s2, (float)ax,
+                                                                 (float)bx, d_out64, d_out32);
+    else
+      k_gp_info_tc<false><<<blocks_c, GC_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv,
+                                                                  model->zs, d_mask, (float)inv_s2, (float)ax,
+                                                                  (float)bx, d_out64, d_out32);
+    FIF_CHECK_LAUNCH("k_gp_info_tc");
   } else {
     const int tpv = (ns + GI_G - 1) / GI_G;
     int vbi = GI_VB_THREADS / tpv;

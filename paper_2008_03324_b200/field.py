@@ -213,6 +213,11 @@ class _DeviceModel:
         self.c = m
 
 
+# GP info builds run on the tensor pipe (mma.sync TF32x3) unless this is set; the FP32
+# SIMT kernel is kept as a cross-check and for models the tensor kernel does not cover.
+GP_INFO_SIMT = False
+
+
 def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, device: torch.device, grid=None,
                centers: torch.Tensor | None = None, v_begin: int = 0, v_end: int | None = None,
                mask: torch.Tensor | None = None, dmodel: _DeviceModel | None = None, f32_copy: bool = True,
@@ -233,7 +238,8 @@ def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, devi
     g = _lib.make_grid(grid.origin, grid.voxel_size, grid.dims) if grid is not None else None
     kind = _lib.KIND_TRACE if want_trace else _lib.KIND_INFO
     st = _lib.load().fif_build(kind, dm.c, _lib.ptr(points), n, g, _lib.ptr(centers), v_begin, v_end, _lib.ptr(mask),
-                               float(sigma), _lib.BUILD_EXACT if exact else 0, _lib.ptr(scratch), _lib.ptr(out64),
+                               float(sigma), (_lib.BUILD_EXACT if exact else 0) | (_lib.BUILD_SIMT if GP_INFO_SIMT else 0),
+                               _lib.ptr(scratch), _lib.ptr(out64),
                                _lib.ptr(out32), _device.stream_handle(device))
     _lib.check(st, "fif_build")
     return out64, out32

@@ -40,9 +40,16 @@ def test_centers_bit_exact(oracle, small_grid, order):
     assert np.array_equal(out.cpu().numpy(), ref)
 
 
+@pytest.fixture(params=["tensor", "simt"])
+def gp_info_kernel(request, monkeypatch):
+    """Both GP-info kernels (mma.sync TF32x3 default, FP32 FFMA2 SIMT) must meet parity."""
+    monkeypatch.setattr(FD, "GP_INFO_SIMT", request.param == "simt")
+    return request.param
+
+
 @pytest.mark.parametrize("mname", ["quad", "gp30", "gp70"])
 @pytest.mark.parametrize("kind", ["trace", "info"])
-def test_build_vs_reference_golden(g_small, models, small_grid, mname, kind):
+def test_build_vs_reference_golden(g_small, models, small_grid, mname, kind, gp_info_kernel):
     f = F.Field.build(g_small["points"], small_grid, models[mname], kind)
     mine, ref = reference_order(f), g_small[f"factors_{mname}_{kind}"]
     err = trace_rel_l2(mine, ref) if kind == "trace" else info_rel_fro(mine, ref)
@@ -80,7 +87,7 @@ def test_config1_sampled_rows(g_cfg1, models):
 
 @pytest.mark.parametrize("mname", ["quad", "gp70"])
 @pytest.mark.parametrize("kind", ["trace", "info"])
-def test_config1_full_grid_vs_oracle(oracle, models, mname, kind):
+def test_config1_full_grid_vs_oracle(oracle, models, mname, kind, gp_info_kernel):
     """Every voxel of BASELINE config 1 (21x21x7 grid, 2 000 uniform landmarks)."""
     from paper_2008_03324_b200 import scenes
 
@@ -94,7 +101,7 @@ def test_config1_full_grid_vs_oracle(oracle, models, mname, kind):
 
 
 @pytest.mark.parametrize("mname", ["quad", "gp70"])
-def test_config2_sampled_voxels(oracle, models, mname):
+def test_config2_sampled_voxels(oracle, models, mname, gp_info_kernel):
     """BASELINE config 2 (20 000 float32 room landmarks) on random + boundary voxels."""
     from paper_2008_03324_b200 import scenes
 
