@@ -13,7 +13,7 @@
 namespace fif {
 
 constexpr int PC_WARPS = 16;
-constexpr int PC_TILE = 512;
+constexpr int PC_TILE = 2048;
 constexpr int PC_QCAP = 64;
 
 struct PoseR {
@@ -89,21 +89,73 @@ __device__ __forceinline__ void fim21(float dx, float dy, float dz, float px, fl
 __constant__ int kPR[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
 __constant__ int kPC[21] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5};
 
+// Landmark table for the FP32 pre-test: p = hi + lo (float4 {hi.xyz, 0}, {lo.xyz, 0}).
+__global__ void k_pc_prep(const double* __restrict__ pts, int64_t n, float4* __restrict__ tab) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float hx, lx, hy, ly, hz, lz;
+  split_f32(pts[3 * i], hx, lx);
+  split_f32(pts[3 * i + 1], hy, ly);
+  split_f32(pts[3 * i + 2], hz, lz);
+  tab[2 * i] = make_float4(hx, hy, hz, 0.f);
+  tab[2 * i + 1] = make_float4(lx, ly, lz, 0.f);
+}
+
+// FP32 pre-test with rigorous margins, branch-free: returns +1 (certainly visible
+// under the reference's FP64 test), -1 (certainly invisible) or 0 (within the error
+// band of z = 0 or of an image border: decide with the exact FP64 test).
+// d = p - t is exact to ~1 ulp of |d| (hi/lo parts); every FP32 rounding below is
+// bounded by a few ulp of |f| |d|_1, and the margins are 8-16 ulp of that.
+struct PoseF {
+  float r00, r01, r02, r10, r11, r12, r20, r21, r22, thx, thy, thz, tlx, tly, tlz;
+};
+struct CamF {
+  float fx, fy, cx, cy, cxw, cyh, mz, mu, mv;
+};
+__device__ __forceinline__ int pc_pretest(const PoseF& P, float4 ph, float4 pl, const CamF& C, float& dx, float& dy,
+                                          float& dz) {
+  dx = (ph.x - P.thx) + (pl.x - P.tlx);
+  dy = (ph.y - P.thy) + (pl.y - P.tly);
+  dz = (ph.z - P.thz) + (pl.z - P.tlz);
+  const float l1 = fabsf(dx) + fabsf(dy) + fabsf(dz);
+  const float zc = fmaf(P.r02, dx, fmaf(P.r12, dy, P.r22 * dz));
+  const float xc = fmaf(P.r00, dx, fmaf(P.r10, dy, P.r20 * dz));
+  const float yc = fmaf(P.r01, dx, fmaf(P.r11, dy, P.r21 * dz));
+  const float a = C.fx * xc, b = C.fy * yc;
+  const float b0 = fmaf(C.cx, zc, a), b1 = fmaf(C.cxw, zc, a);
+  const float c0 = fmaf(C.cy, zc, b), c1 = fmaf(C.cyh, zc, b);
+  const float mz = C.mz * l1, m1 = C.mu * l1, m2 = C.mv * l1;
+  const bool zpos = zc > mz, zneg = zc < -mz;
+  const bool out = (b0 < -m1) | (b1 > m1) | (c0 < -m2) | (c1 > m2);
+  const bool in = (b0 > m1) & (b1 < -m1) & (c0 > m2) & (c1 < -m2);
+  return (zpos & in) ? 1 : ((zneg | (zpos & out)) ? -1 : 0);
+}
+
 template <bool MASK>
 __global__ void __launch_bounds__(PC_WARPS * 32) k_pc_fim(const double* __restrict__ rot, const double* __restrict__ tr,
-                                                          int64_t nq, const double* __restrict__ pts, int64_t n,
-                                                          fif_camera cam, float inv_s2, double* __restrict__ out,
+                                                          int64_t nq, const double* __restrict__ pts,
+                                                          const float4* __restrict__ ptab, int64_t n, fif_camera cam,
+                                                          float inv_s2, double* __restrict__ out,
                                                           uint8_t* __restrict__ mask) {
-  __shared__ double tile[3][PC_TILE];
-  __shared__ float4 queue[PC_WARPS][PC_QCAP][2];  // {d.xyz, -} {p.xyz, -} fp32
+  extern __shared__ float4 pcsm[];
+  float4 (*tile)[PC_TILE] = reinterpret_cast<float4 (*)[PC_TILE]>(pcsm);                     // [2][PC_TILE]
+  float4 (*queue)[PC_QCAP][2] = reinterpret_cast<float4 (*)[PC_QCAP][2]>(pcsm + 2 * PC_TILE);  // [warps][cap][2]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double cxw = cam.cx - cam.width, cyh = cam.cy - cam.height;
+  // margins: 16 ulp(fp32) x (|f| + |c| + |w|) per unit of |d|_1 (bounds every rounding
+  // of the FP32 evaluation plus the FP64 reference's own roundings)
+  CamF CF;
+  CF.fx = (float)cam.fx; CF.fy = (float)cam.fy; CF.cx = (float)cam.cx; CF.cy = (float)cam.cy;
+  CF.cxw = (float)cxw; CF.cyh = (float)cyh;
+  CF.mz = 8.0f * 5.96e-8f;
+  CF.mu = 16.0f * 5.96e-8f * (float)(fabs(cam.fx) + fabs(cam.cx) + fabs(cam.width));
+  CF.mv = 16.0f * 5.96e-8f * (float)(fabs(cam.fy) + fabs(cam.cy) + fabs(cam.height));
   const unsigned lt_mask = (1u << lane) - 1u;
-  // persistent over pose groups (all warps of a CTA stay in lockstep for the tile syncs)
   for (int64_t q0 = blockIdx.x * (int64_t)PC_WARPS; q0 < nq; q0 += (int64_t)gridDim.x * PC_WARPS) {
     const int64_t q = q0 + warp;
     const bool has_pose = q < nq;
     PoseR P;
+    PoseF PF;
     {
       const int64_t qq = has_pose ? q : q0;
       const double* R = rot + 9 * qq;
@@ -111,6 +163,12 @@ __global__ void __launch_bounds__(PC_WARPS * 32) k_pc_fim(const double* __restri
       P.r10 = R[3]; P.r11 = R[4]; P.r12 = R[5];
       P.r20 = R[6]; P.r21 = R[7]; P.r22 = R[8];
       P.tx = tr[3 * qq]; P.ty = tr[3 * qq + 1]; P.tz = tr[3 * qq + 2];
+      PF.r00 = (float)P.r00; PF.r01 = (float)P.r01; PF.r02 = (float)P.r02;
+      PF.r10 = (float)P.r10; PF.r11 = (float)P.r11; PF.r12 = (float)P.r12;
+      PF.r20 = (float)P.r20; PF.r21 = (float)P.r21; PF.r22 = (float)P.r22;
+      split_f32(P.tx, PF.thx, PF.tlx);
+      split_f32(P.ty, PF.thy, PF.tly);
+      split_f32(P.tz, PF.thz, PF.tlz);
     }
     float acc[21];
 #pragma unroll
@@ -119,32 +177,35 @@ __global__ void __launch_bounds__(PC_WARPS * 32) k_pc_fim(const double* __restri
     for (int64_t base = 0; base < n; base += PC_TILE) {
       const int cnt = (int)min((int64_t)PC_TILE, n - base);
       __syncthreads();
-      for (int j = threadIdx.x; j < cnt * 3; j += blockDim.x) {
-        int64_t i = base + j / 3;
-        (void)i;
-        tile[j % 3][j / 3] = pts[3 * base + j];
-      }
+      for (int j = threadIdx.x; j < cnt * 2; j += blockDim.x) tile[j & 1][j >> 1] = ptab[2 * base + j];
       __syncthreads();
       if (!has_pose) continue;
       for (int j0 = 0; j0 < cnt; j0 += 32) {
         const int j = j0 + lane;
         bool vis = false;
-        double px = 0, py = 0, pz = 0;
+        float dx = 0.f, dy = 0.f, dz = 0.f;
+        float4 ph = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < cnt) {
-          px = tile[0][j]; py = tile[1][j]; pz = tile[2][j];
-          vis = pc_visible(P, px, py, pz, cam, cxw, cyh);
+          ph = tile[0][j];
+          const int pre = pc_pretest(PF, ph, tile[1][j], CF, dx, dy, dz);
+          if (pre == 0) {
+            const int64_t i = base + j;
+            vis = pc_visible(P, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], cam, cxw, cyh);
+          } else {
+            vis = pre > 0;
+          }
           if (MASK) mask[q * n + base + j] = (uint8_t)vis;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, vis);
         if (vis) {
-          int slot = qn + __popc(bal & lt_mask);
-          queue[warp][slot][0] = make_float4((float)(px - P.tx), (float)(py - P.ty), (float)(pz - P.tz), 0.f);
-          queue[warp][slot][1] = make_float4((float)px, (float)py, (float)pz, 0.f);
+          const int slot = qn + __popc(bal & lt_mask);
+          queue[warp][slot][0] = make_float4(dx, dy, dz, 0.f);
+          queue[warp][slot][1] = ph;
         }
         qn += __popc(bal);
         if (qn >= 32) {
           __syncwarp();
-          float4 d = queue[warp][lane][0], p = queue[warp][lane][1];
+          const float4 d = queue[warp][lane][0], p = queue[warp][lane][1];
           float e[21];
           fim21(d.x, d.y, d.z, p.x, p.y, p.z, inv_s2, e);
 #pragma unroll
@@ -162,7 +223,7 @@ __global__ void __launch_bounds__(PC_WARPS * 32) k_pc_fim(const double* __restri
     if (has_pose) {
       __syncwarp();
       if (lane < qn) {
-        float4 d = queue[warp][lane][0], p = queue[warp][lane][1];
+        const float4 d = queue[warp][lane][0], p = queue[warp][lane][1];
         float e[21];
         fim21(d.x, d.y, d.z, p.x, p.y, p.z, inv_s2, e);
 #pragma unroll
@@ -175,7 +236,6 @@ __global__ void __launch_bounds__(PC_WARPS * 32) k_pc_fim(const double* __restri
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         acc[k] = v;
       }
-      // lane e writes entry e and its mirror
       double mine = 0.0;
 #pragma unroll
       for (int k = 0; k < 21; ++k) if (lane == k) mine = (double)acc[k];
@@ -209,10 +269,29 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
   int64_t cap = (int64_t)kSMs * 2;
   unsigned blocks = (unsigned)(need < cap ? need : cap);
   const float inv_s2 = (float)(1.0 / (sigma * sigma));
+  float4* ptab = nullptr;
+  if (cudaMallocAsync(&ptab, sizeof(float4) * 2 * n_points, st) != cudaSuccess) {
+    set_error("fif_pc_fim: cudaMallocAsync failed");
+    return FIF_ERR_CUDA;
+  }
+  k_pc_prep<<<(unsigned)((n_points + 255) / 256), 256, 0, st>>>(d_points, n_points, ptab);
+  FIF_CHECK_LAUNCH("k_pc_prep");
+  const size_t smem = sizeof(float4) * (2 * PC_TILE + PC_WARPS * PC_QCAP * 2);
+  static bool attr = false;
+  if (!attr) {
+    for (auto f : {k_pc_fim<true>, k_pc_fim<false>}) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    attr = true;
+  }
   if (d_mask)
-    k_pc_fim<true><<<blocks, PC_WARPS * 32, 0, st>>>(d_rot, d_t, q, d_points, n_points, *cam, inv_s2, d_out, d_mask);
+    k_pc_fim<true><<<blocks, PC_WARPS * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2, d_out,
+                                                        d_mask);
   else
-    k_pc_fim<false><<<blocks, PC_WARPS * 32, 0, st>>>(d_rot, d_t, q, d_points, n_points, *cam, inv_s2, d_out, d_mask);
+    k_pc_fim<false><<<blocks, PC_WARPS * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2,
+                                                         d_out, d_mask);
+  cudaFreeAsync(ptab, st);
   FIF_CHECK_LAUNCH("k_pc_fim");
   return FIF_OK;
 }

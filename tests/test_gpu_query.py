@@ -188,7 +188,9 @@ def test_config2_queries_end_to_end(oracle, models):
 
 
 def test_factorization_exact_at_voxel_centres(models):
-    """at a voxel centre the field FIM equals sum_i v_model(theta_i) I_i."""
+    """at a voxel centre the field FIM equals sum_i v_model(theta_i) I_i
+    (1e-9 for the FP64 quad build; GP builds use FP32/TF32 per-pair arithmetic, so the
+    bar is the query tolerance's 10x-tighter 1e-5)."""
     rng = np.random.default_rng(4)
     pts = rng.uniform([-3, -3, 0], [3, 3, 3], size=(150, 3))
     grid = F.GridConfig(np.array([-1.0, -1.0, 0.5]), 0.5, np.array([4, 4, 3]))
@@ -202,4 +204,5 @@ def test_factorization_exact_at_voxel_centres(models):
             vr = m.rotation_vector(R)
             vp = m.position_vectors(c, pts)
             direct = sum(float(vr @ vp[i]) * F.landmark_fim(c, pts[i]) for i in range(len(pts)))
-            assert np.linalg.norm(got - direct) <= 1e-6 * np.linalg.norm(direct)
+            tol = 1e-9 if mname == "quad" else 1e-5
+            assert np.linalg.norm(got - direct) <= tol * np.linalg.norm(direct)
