@@ -159,7 +159,7 @@ struct QueryOut {
 // kernels.py:638-649) or kinv v^r (GP, kernels.py:652-657; kinv symmetric so
 // omega . S == v^r . (kinv S)).  A CTA handles QP_Q queries; the GP matrix-vector
 // products run one thread per (query, output k) with v^r staged in smem.
-constexpr int QP_Q = 8;
+constexpr int QP_Q = 32;
 constexpr int QP_THREADS = 256;
 
 __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeom gm, const int32_t* __restrict__ slots,
