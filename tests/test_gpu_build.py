@@ -129,14 +129,14 @@ def test_linearity_and_slab_determinism(models, small_grid, g_small):
 
     dev = torch.device("cuda")
     pts = g_small["points"]
-    for mname in ("quad", "gp30"):
+    for mname, tol in (("quad", 1e-12), ("gp30", 1e-5)):  # GP: FP32/TF32 per-pair math, FP32 partial sums
         m = models[mname]
         full = F.Field.build(pts, small_grid, m, "info")
         a = F.Field.build(pts[:150], small_grid, m, "info")
         b = F.Field.build(pts[150:], small_grid, m, "info")
         s = a.storage["f64"] + b.storage["f64"]
         ref = full.storage["f64"]
-        assert (torch.abs(s - ref).max() / torch.abs(ref).max()).item() < 1e-6
+        assert (torch.abs(s - ref).max() / torch.abs(ref).max()).item() < tol
         P = torch.tensor(pts, device=dev)
         V = small_grid.voxel_count
         for world in (2, 3, 8):
@@ -184,7 +184,7 @@ def test_incremental_add_remove(models, small_grid, g_small):
     """add/remove == rebuild; quad is FP64 throughout, GP's FP32 partial sums
     group landmarks differently in the two builds, so agreement is at FP32-partial level."""
     pts = g_small["points"]
-    for mname, tol in (("quad", 1e-12), ("gp30", 1e-6)):
+    for mname, tol in (("quad", 1e-12), ("gp30", 1e-5)):
         full = F.Field.build(pts, small_grid, models[mname], "info")
         inc = F.Field.build(pts[:200], small_grid, models[mname], "info")
         inc.add_landmarks(pts[200:])
