@@ -695,7 +695,9 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <bool HAS_MASK>
+// DEAD_TOP: the upper 8 rows of the warp's last m-tile are padding (e.g. N_s = 70 with
+// 5 m-tiles): their sigmoids are skipped at compile time (A rows = 0, no MUFU work).
+template <bool HAS_MASK, bool DEAD_TOP>
 __global__ void __launch_bounds__(GC_WARPS * 32, 2)
 k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1,
              int ns, int wpv, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax,
@@ -783,6 +785,10 @@ k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSr
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int h = i & 1;
+          if (DEAD_TOP && h == 1 && m == GC_MT - 1) {
+            ah[i] = al[i] = 0u;
+            continue;
+          }
           const float4 u = (i < 2) ? u0 : u1;
           const float x = fmaf(u.x, zr[m][h][0], fmaf(u.y, zr[m][h][1], fmaf(u.z, zr[m][h][2], bx)));
           tf32_split(rcp_approx(1.0f + ex2_approx(x)), ah[i], al[i]);
@@ -1026,20 +1032,23 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
                   sizeof(float) * ((6 * vpc + 1) & ~1) + sizeof(double) * GC_WARPS * GC_MT * GC_NT * 4 * 32;
     static bool carve_tc = false;
     if (!carve_tc) {
-      for (auto f : {k_gp_info_tc<true>, k_gp_info_tc<false>}) {
+      for (auto f : {k_gp_info_tc<true, true>, k_gp_info_tc<false, true>, k_gp_info_tc<true, false>,
+                     k_gp_info_tc<false, false>}) {
         cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
       carve_tc = true;
     }
-    if (has_mask)
-      k_gp_info_tc<true><<<blocks_c, GC_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv,
-                                                                 model->zs, d_mask, (float)inv_s2, (float)ax,
-                                                                 (float)bx, d_out64, d_out32);
-    else
-      k_gp_info_tc<false><<<blocks_c, GC_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv,
-                                                                  model->zs, d_mask, (float)inv_s2, (float)ax,
-                                                                  (float)bx, d_out64, d_out32);
+    // the top 8 rows of the last warp's last m-tile are padding for every warp of the
+    // voxel only when wpv == 1; with wpv > 1 earlier warps' tiles are real
+    const bool dead_top = wpv == 1 && (GC_MT - 1) * 16 + 8 >= ns;
+#define GC_LAUNCH(M, D)                                                                                       \
+  k_gp_info_tc<M, D><<<blocks_c, GC_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv, \
+                                                           model->zs, d_mask, (float)inv_s2, (float)ax, (float)bx, \
+                                                           d_out64, d_out32)
+    if (has_mask) { if (dead_top) GC_LAUNCH(true, true); else GC_LAUNCH(true, false); }
+    else { if (dead_top) GC_LAUNCH(false, true); else GC_LAUNCH(false, false); }
+#undef GC_LAUNCH
     FIF_CHECK_LAUNCH("k_gp_info_tc");
   } else {
     const int tpv = (ns + GI_G - 1) / GI_G;
