@@ -214,3 +214,18 @@ def test_serialize_roundtrip(models, small_grid, g_small, tmp_path):
         bad = tmp_path / "bad.fif"
         bad.write_bytes(b"XXXX" + b"\0" * 64)
         F.Field.deserialize(bad)
+
+
+@pytest.mark.parametrize("kind", ["trace", "info"])
+def test_gp150_build(oracle, kind, gp_info_kernel):
+    """N_s = 150 (the largest GP size of the paper's Table I; two warps per voxel on the
+    tensor path) on a small scene vs the oracle."""
+    m = F.build_gp_model(150)
+    rng = np.random.default_rng(12)
+    pts = rng.uniform([-3, -3, 0], [3, 3, 2], size=(300, 3))
+    grid = F.GridConfig(np.array([-1.0, -1.0, 0.25]), 0.5, np.array([4, 3, 3]))
+    f = F.Field.build(pts, grid, m, kind)
+    ref = oracle_field(oracle, m, grid.centers(), pts, kind)
+    mine = reference_order(f)
+    err = trace_rel_l2(mine, ref) if kind == "trace" else info_rel_fro(mine, ref)
+    assert err.max() <= (TRACE_TOL if kind == "trace" else INFO_TOL)
