@@ -14,6 +14,8 @@
 // rows are streamed once per corner (HBM-bound) and blended in FP64.
 #include "fif_common.cuh"
 
+#include <cstdlib>
+
 namespace fif {
 
 
@@ -154,25 +156,29 @@ struct QueryOut {
 
 // ───────────────────────── prep: corners + rotation weights ─────────────
 // Per query q: status, 8 corner rows (int32, -1 = empty/absent), corner weights
-// cw[q][c] = {w, dw/dx, dw/dy, dw/dz}, and rotation weights wt[q][4][nv] =
-// {omega, d omega/dz_x, d omega/dz_y, d omega/dz_z} in FP64, where omega = v^r (quad,
-// kernels.py:638-649) or kinv v^r (GP, kernels.py:652-657; kinv symmetric so
-// omega . S == v^r . (kinv S)).  A CTA handles QP_Q queries; the GP matrix-vector
-// products run one thread per (query, output k) with v^r staged in smem.
-constexpr int QP_Q = 32;
+// cw[q][c] = {w, dw/dx, dw/dy, dw/dz}, and rotation weights wt[q][k] = {omega_k,
+// d omega_k/dz_x, d omega_k/dz_y, d omega_k/dz_z} (one double4 per sample k, FP64),
+// where omega = v^r (quad, kernels.py:638-649) or kinv v^r (GP, kernels.py:652-657;
+// kinv symmetric so omega . S == v^r . (kinv S)).  A CTA handles QP_Q queries.
+// GP: v^r into smem, then one thread per (k, group of QP_G queries) runs the FP64
+// matrix-vector products with kinv read through L1 (coalesced over k) and v^r
+// broadcast from smem; the three derivative rows reuse t = kinv_gk v^r_g:
+// d omega_a = inv_l2 kinv (v^r . zs_a).
+constexpr int QP_Q = 64;
+constexpr int QP_G = 4;
 constexpr int QP_THREADS = 256;
 
 __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeom gm, const int32_t* __restrict__ slots,
                                                           const double* __restrict__ pos, const double* __restrict__ axes,
                                                           int64_t nq, int trilinear, uint8_t* __restrict__ status,
                                                           int32_t* __restrict__ rows, double4* __restrict__ cw,
-                                                          double* __restrict__ wt) {
-  extern __shared__ double sv[];  // [QP_Q][4][nv]
+                                                          double4* __restrict__ wt) {
+  extern __shared__ double sv[];  // [QP_Q][nv] v^r, then zs [nv][3]
   const int nv = m.kind == FIF_MODEL_QUAD ? 10 : m.n_v;
   const int64_t q0 = blockIdx.x * (int64_t)QP_Q;
   const int t = threadIdx.x;
   // corners and trilinear weights: one thread per query (FP64, reference order)
-  if (t < QP_Q && q0 + t < nq) {
+  if (t < QP_Q && q0 + t < nq) {  // (QP_Q <= QP_THREADS)
     const int64_t q = q0 + t;
     int nc = 0;
     int64_t r[8];
@@ -205,65 +211,69 @@ __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeo
         case 8: v = __dmul_rn(k1, zz); gz = k1; break;
         default: v = k0; break;
       }
-      double* o = wt + q * 4 * 10;
-      o[k] = v;
-      o[10 + k] = gx;
-      o[20 + k] = gy;
-      o[30 + k] = gz;
+      wt[q * 10 + k] = make_double4(v, gx, gy, gz);
     }
     return;
   }
-  // GP: v^r and its z-derivatives into smem, then omega = kinv v^r (FP64)
+  // GP: v^r into smem (kernels.py:652-657 sample kernel), zs / l^2 staged after it
   const double inv_l2 = 1.0 / (m.ell * m.ell);
+  double* zs = sv + QP_Q * nv;
+  for (int idx = t; idx < 3 * nv; idx += blockDim.x) zs[idx] = m.zs[idx] * inv_l2;
   for (int idx = t; idx < QP_Q * nv; idx += blockDim.x) {
     const int qi = idx / nv, g = idx - qi * nv;
     const int64_t q = q0 + qi;
-    double* o = sv + qi * 4 * nv;
     if (q >= nq) {
-      o[g] = o[nv + g] = o[2 * nv + g] = o[3 * nv + g] = 0.0;
+      sv[idx] = 0.0;
       continue;
     }
-    const double zsx = m.zs[3 * g], zsy = m.zs[3 * g + 1], zsz = m.zs[3 * g + 2];
-    const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * q], zsx), __dmul_rn(axes[3 * q + 1], zsy)),
-                               __dmul_rn(axes[3 * q + 2], zsz));
-    const double vr = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
-    const double sc = vr * inv_l2;
-    o[g] = vr;
-    o[nv + g] = sc * zsx;
-    o[2 * nv + g] = sc * zsy;
-    o[3 * nv + g] = sc * zsz;
+    const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * q], m.zs[3 * g]), __dmul_rn(axes[3 * q + 1], m.zs[3 * g + 1])),
+                               __dmul_rn(axes[3 * q + 2], m.zs[3 * g + 2]));
+    sv[idx] = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
   }
   __syncthreads();
-  for (int idx = t; idx < QP_Q * nv; idx += blockDim.x) {
-    const int qi = idx / nv, k = idx - qi * nv;
-    const int64_t q = q0 + qi;
-    if (q >= nq) continue;
-    const double* v = sv + qi * 4 * nv;
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  // one thread per (k, group of QP_G queries): each kinv element read once feeds
+  // QP_G queries; zs is warp-uniform, v^r uniform within the query group.
+  for (int idx = t; idx < (QP_Q / QP_G) * nv; idx += blockDim.x) {
+    const int qg = idx / nv, k = idx - qg * nv;
+    const double* v = sv + qg * QP_G * nv;
+    const double* kc = m.kinv + k;
+    double a[QP_G][4];
+#pragma unroll
+    for (int i = 0; i < QP_G; ++i) a[i][0] = a[i][1] = a[i][2] = a[i][3] = 0.0;
+#pragma unroll 2
     for (int g = 0; g < nv; ++g) {
-      const double kg = __ldg(m.kinv + (int64_t)g * nv + k);
-      a0 = fma(kg, v[g], a0);
-      a1 = fma(kg, v[nv + g], a1);
-      a2 = fma(kg, v[2 * nv + g], a2);
-      a3 = fma(kg, v[3 * nv + g], a3);
+      const double kg = __ldg(kc + (int64_t)g * nv);
+      const double z0 = zs[3 * g], z1 = zs[3 * g + 1], z2 = zs[3 * g + 2];
+#pragma unroll
+      for (int i = 0; i < QP_G; ++i) {
+        const double tg = kg * v[i * nv + g];
+        a[i][0] += tg;
+        a[i][1] = fma(tg, z0, a[i][1]);
+        a[i][2] = fma(tg, z1, a[i][2]);
+        a[i][3] = fma(tg, z2, a[i][3]);
+      }
     }
-    double* o = wt + q * 4 * nv;
-    o[k] = a0;
-    o[nv + k] = a1;
-    o[2 * nv + k] = a2;
-    o[3 * nv + k] = a3;
+#pragma unroll
+    for (int i = 0; i < QP_G; ++i) {
+      const int64_t q = q0 + qg * QP_G + i;
+      if (q < nq) wt[q * nv + k] = make_double4(a[i][0], a[i][1], a[i][2], a[i][3]);
+    }
   }
 }
 
 // ───────────────────────── contraction: info fields ─────────────────────
-// One warp per query, lane e < 21 owns packed entry e.  The (query, corner) rows
-// are streamed into shared memory with TMA bulk copies (cp.async.bulk, one 16-B
-// aligned superset of the 5880-B / 1680-B row), QI_NBUF deep per warp across query
-// boundaries, completion tracked by mbarrier transaction counts; the warp computes
-// G_c = omega . S_c and H_c,a = d omega_a . S_c from smem while the next rows land.
-constexpr int QC_WARPS = 8;
-constexpr int QI_NBUF = 2;
-constexpr int QI_CG = 2;
+// One warp per query, lane e < 21 owns packed entry e.  Each warp streams its
+// queries through a private QW_STAGES-deep ring of k-chunks: one chunk = KC
+// samples of all NC corner rows (KC*21 contiguous entries of each row, one TMA
+// bulk copy per corner, 16-B aligned superset) plus the KC rotation weights, all
+// completing on the stage's mbarrier.  Lane 0 refills a stage as soon as the warp
+// has consumed it, so the next chunks (of this or the next query) are in flight
+// while the warp computes
+//     G_c += omega_k S_c,k          (every corner: the 6x6 blend and d/dt)
+//     R_a += d omega_k/dz_a . (sum_c w_c S_c,k)   (rotation gradient, blend first)
+// in FP64 from the smem copy.  No block-level synchronisation: warps are
+// independent streams, the block only shares a zero row used for absent corners.
+constexpr int QW_WARPS = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -293,231 +303,254 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       : "memory");
 }
 
-// Block-cooperative contraction: the NC corner rows and the rotation weights of
-// one query land in shared memory with TMA bulk copies (one mbarrier transaction);
-// the block's 8 warps split the k (sample) range, lane e < 21 owns packed entry e,
-// so every weight is read once per block per query and reused for all NC corners.
-// Per-warp partials (G_c, R_a) are reduced through shared memory by warp 0, which
-// also writes the outputs; the next query's rows are in flight meanwhile.
-constexpr int QB_WARPS = 8;
+// k-chunk length: 840 bytes of each corner row per stage for FP32 and FP64 rows.
+template <typename T>
+struct QWShape {
+  static constexpr int KC = sizeof(T) == 4 ? 10 : 5;
+  static constexpr uint32_t CHUNK = KC * 21 * sizeof(T);
+  static constexpr uint32_t CAP = (CHUNK + 32 + 15) & ~15u;  // + alignment slack both ends
+};
+template <typename T, int NC, int STAGES, bool METRIC>
+__host__ __device__ constexpr uint32_t qw_warp_bytes() {
+  return 64 + STAGES * (NC * QWShape<T>::CAP + QWShape<T>::KC * 32) + (METRIC ? 8 * 21 * 8 : 0);
+}
 
-template <typename T, int NC, bool GRAD, bool METRIC>
-__global__ void __launch_bounds__(QB_WARPS * 32, 3) k_query_info(int nv, const T* __restrict__ field,
+template <typename T, int NC, int STAGES, bool GRAD, bool METRIC>
+__global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_info(int nv, const T* __restrict__ field,
                                                              const double* __restrict__ axes, int64_t nq,
                                                              const uint8_t* __restrict__ status,
                                                              const int32_t* __restrict__ rows,
                                                              const double4* __restrict__ cw,
-                                                             const double* __restrict__ wt, QueryOut out) {
-  constexpr int NP = NC + 3;  // partials per lane: G_0..G_{NC-1}, R0, R1, R2
+                                                             const double4* __restrict__ wt, QueryOut out) {
+  using SH = QWShape<T>;
+  constexpr int KC = SH::KC;
+  constexpr uint32_t CAP = SH::CAP;
+  constexpr uint32_t STAGE = NC * CAP + KC * 32;
+  constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(128) unsigned char qraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t rw = (int64_t)nv * 21;
-  const uint32_t rowcap = (uint32_t)(((rw * sizeof(T) + 16) + 15) & ~15ull);
-  const uint32_t wbytes = (uint32_t)(4 * nv * sizeof(double));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(qraw);
-  unsigned char* rbuf = qraw + 128;                                        // [NC][rowcap]
-  double* wq = reinterpret_cast<double*>(rbuf + (size_t)NC * rowcap);      // [4][nv]
-  double* part = wq + 4 * nv;                                              // [QB_WARPS][NP][32]
-  double* cfim = part + QB_WARPS * NP * 32;                                // [8][21]
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
+  const T* zero_row = reinterpret_cast<const T*>(qraw);  // [CHUNK] zeros, shared
+  unsigned char* wbase = qraw + ((SH::CHUNK + 127) & ~127u) + (size_t)warp * ((qw_warp_bytes<T, NC, STAGES, METRIC>() + 127) & ~127u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase);
+  unsigned char* stages = wbase + 64;
+  double* cfim = reinterpret_cast<double*>(stages + STAGES * STAGE);  // METRIC: [8][21]
+  for (int i = threadIdx.x; i < (int)(SH::CHUNK / 4); i += blockDim.x) reinterpret_cast<float*>(qraw)[i] = 0.f;
+  if (lane == 0) {
+    for (int b = 0; b < STAGES; ++b) mbar_init(&bars[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto row_src = [&](int32_t r, uint32_t& bytes, uint32_t& off) -> const char* {
-    const char* src = reinterpret_cast<const char*>(field + (int64_t)r * rw);
-    const char* a0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15);
-    const uintptr_t end = (reinterpret_cast<uintptr_t>(src + rw * sizeof(T)) + 15) & ~(uintptr_t)15;
-    bytes = (uint32_t)(end - reinterpret_cast<uintptr_t>(a0));
-    off = (uint32_t)(src - a0);
-    return a0;
+  const int64_t rw = (int64_t)nv * 21;
+  const int nch = (nv + KC - 1) / KC;
+  const int64_t tw = (int64_t)gridDim.x * QW_WARPS;
+  const int64_t qfirst = blockIdx.x * (int64_t)QW_WARPS + warp;
+  const int64_t nmine = qfirst < nq ? (nq - qfirst + tw - 1) / tw : 0;
+  auto qof = [&](int64_t i) { return qfirst + i * tw; };
+  auto row_of = [&](int64_t i) -> int32_t {  // lane c < NC: corner c's row of my i-th query
+    return (i < nmine && lane < NC) ? __ldg(rows + qof(i) * 8 + lane) : -1;
   };
-  auto issue = [&](int64_t q) {  // thread 0 only
-    if (q >= nq) return;
-    const bool ok = status[q] == FIF_STATUS_OK;
-    uint32_t total = 0;
-    for (int c = 0; c < NC; ++c) {
-      const int32_t r = ok ? rows[q * 8 + c] : -1;
-      if (r < 0) continue;
-      uint32_t bytes, off;
-      row_src(r, bytes, off);
-      total += bytes;
+
+  // ── producer (whole warp; lane c < NC copies corner c, lane NC the weights) ──
+  int64_t pi = 0;
+  int pj = 0, pb = 0;
+  int32_t p_r = row_of(0), pn_r = row_of(1);
+  auto produce = [&]() {
+    if (pi >= nmine) return;
+    const int64_t q = qof(pi);
+    const int k0 = pj * KC, kn = min(KC, nv - k0);
+    uintptr_t a0 = 0;
+    uint32_t bytes = 0;
+    if (lane < NC) {
+      if (p_r >= 0) {
+        const uintptr_t src = reinterpret_cast<uintptr_t>(field + (int64_t)p_r * rw + (int64_t)k0 * 21);
+        a0 = src & ~(uintptr_t)15;
+        bytes = (uint32_t)(((src + kn * 21 * sizeof(T) + 15) & ~(uintptr_t)15) - a0);
+      }
+    } else if (lane == NC) {
+      a0 = reinterpret_cast<uintptr_t>(wt + q * nv + k0);
+      bytes = (uint32_t)kn * 32u;
     }
-    if (ok) total += (GRAD ? 4 : 1) * (uint32_t)(nv * sizeof(double));
-    if (total == 0) {
-      mbar_arrive(bar);
-      return;
-    }
-    mbar_expect_tx(bar, total);
-    if (ok) tma_bulk_g2s(wq, wt + q * 4 * nv, (GRAD ? 4 : 1) * (uint32_t)(nv * sizeof(double)), bar);
-    for (int c = 0; c < NC; ++c) {
-      const int32_t r = ok ? rows[q * 8 + c] : -1;
-      if (r < 0) continue;
-      uint32_t bytes, off;
-      const char* a0 = row_src(r, bytes, off);
-      tma_bulk_g2s(rbuf + (size_t)c * rowcap, a0, bytes, bar);
+    const uint32_t total = __reduce_add_sync(FULL, bytes);
+    if (lane == 0) mbar_expect_tx(&bars[pb], total);
+    __syncwarp();
+    if (bytes) tma_bulk_g2s(stages + (size_t)pb * STAGE + (lane < NC ? lane : NC) * CAP,
+                            reinterpret_cast<const void*>(a0), bytes, &bars[pb]);
+    if (++pb == STAGES) pb = 0;
+    if (++pj == nch) {
+      pj = 0;
+      ++pi;
+      p_r = pn_r;
+      pn_r = row_of(pi + 1);
     }
   };
-  (void)wbytes;
+  for (int s = 0; s < STAGES - 1; ++s) produce();
+
+  // ── consumer ──
   const bool on = lane < 21;
   const int e = on ? lane : 0;
-  const int kper = (nv + QB_WARPS - 1) / QB_WARPS;
-  const int k0 = warp * kper, k1 = min(nv, k0 + kper);
-  uint32_t phase = 0;
-  if (threadIdx.x == 0) issue(blockIdx.x);
-  for (int64_t q = blockIdx.x; q < nq; q += gridDim.x, phase ^= 1u) {
-    const int st = status[q];
+  int32_t c_r = row_of(0);
+  double4 c_cw = lane < NC && nmine > 0 ? cw[qof(0) * 8 + lane] : make_double4(0, 0, 0, 0);
+  int c_st = nmine > 0 ? status[qof(0)] : 0;
+  int cb = 0;
+  uint32_t cphase = 0;
+  for (int64_t i = 0; i < nmine; ++i) {
+    const int64_t q = qof(i);
+    const int st = c_st;
     int32_t r[NC];
-    const T* rp[NC];
-    double w[NC];
+    double w[NC], G[NC];
+    uint32_t off[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      r[c] = st == FIF_STATUS_OK ? rows[q * 8 + c] : -1;
-      w[c] = r[c] >= 0 ? cw[q * 8 + c].x : 0.0;
-      uint32_t bytes = 0, off = 0;
-      if (r[c] >= 0) row_src(r[c], bytes, off);
-      rp[c] = reinterpret_cast<const T*>(rbuf + (size_t)c * rowcap + off) + e;
+      r[c] = __shfl_sync(FULL, c_r, c);
+      w[c] = __shfl_sync(FULL, c_cw.x, c);
+      off[c] = (uint32_t)(reinterpret_cast<uintptr_t>(field + (int64_t)(r[c] < 0 ? 0 : r[c]) * rw) & 15);
+      G[c] = 0.0;
     }
-    mbar_wait(bar, phase);
-    double G[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) G[c] = 0.0;
+    const double4 my_cw = c_cw;
+    // prefetch the next query's metadata
+    c_r = row_of(i + 1);
+    if (i + 1 < nmine) {
+      c_cw = lane < NC ? cw[qof(i + 1) * 8 + lane] : make_double4(0, 0, 0, 0);
+      c_st = status[qof(i + 1)];
+    }
     double R0 = 0, R1 = 0, R2 = 0;
-    if (on && st == FIF_STATUS_OK) {
-#pragma unroll 2
-      for (int k = k0; k < k1; ++k) {
-        double sv[NC];
+    for (int j = 0; j < nch; ++j) {
+      __syncwarp();  // every lane is done with the stage produce() refills next
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      produce();
+      mbar_wait(&bars[cb], cphase);
+      if (st == FIF_STATUS_OK && on) {
+        const int k0 = j * KC, kn = min(KC, nv - k0);
+        const unsigned char* sb = stages + (size_t)cb * STAGE;
+        const T* src[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) sv[c] = r[c] >= 0 ? (double)rp[c][k * 21] : 0.0;
-        const double om = wq[k];
+        for (int c = 0; c < NC; ++c)
+          src[c] = r[c] >= 0
+                       ? reinterpret_cast<const T*>(sb + c * CAP + ((off[c] + (uint32_t)(k0 * 21 * sizeof(T))) & 15u)) + e
+                       : zero_row + e;
+        const double4* wk = reinterpret_cast<const double4*>(sb + NC * CAP);
+        auto step = [&](int kk) {
+          const double4 om = wk[kk];
+          double sv[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) G[c] = fma(om, sv[c], G[c]);
-        if (GRAD) {
-          double bl = 0.0;
+          for (int c = 0; c < NC; ++c) sv[c] = (double)src[c][kk * 21];
 #pragma unroll
-          for (int c = 0; c < NC; ++c) bl = fma(w[c], sv[c], bl);
-          R0 = fma(wq[nv + k], bl, R0);
-          R1 = fma(wq[2 * nv + k], bl, R1);
-          R2 = fma(wq[3 * nv + k], bl, R2);
+          for (int c = 0; c < NC; ++c) G[c] = fma(om.x, sv[c], G[c]);
+          if (GRAD) {
+            // blend over corners as two independent chains (halves the DFMA dependency depth)
+            double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; c += 2) {
+              b0 = fma(w[c], sv[c], b0);
+              if (c + 1 < NC) b1 = fma(w[c + 1], sv[c + 1], b1);
+            }
+            const double bl = b0 + b1;
+            R0 = fma(om.y, bl, R0);
+            R1 = fma(om.z, bl, R1);
+            R2 = fma(om.w, bl, R2);
+          }
+        };
+        if (kn == KC) {
+#pragma unroll
+          for (int kk = 0; kk < KC; ++kk) step(kk);
+        } else {
+#pragma unroll 1
+          for (int kk = 0; kk < kn; ++kk) step(kk);
+        }
+      }
+      if (++cb == STAGES) {
+        cb = 0;
+        cphase ^= 1u;
+      }
+    }
+    // ── query complete: outputs ──
+    if (st != FIF_STATUS_OK) {
+      if (out.fim) for (int i2 = lane; i2 < 36; i2 += 32) out.fim[q * 36 + i2] = 0.0;
+      if (out.fim_grad) for (int i2 = lane; i2 < 216; i2 += 32) out.fim_grad[q * 216 + i2] = 0.0;
+      if (lane == 0) {
+        if (out.trace) out.trace[q] = 0.0;
+        if (out.det) out.det[q] = 0.0;
+        if (out.lmin) out.lmin[q] = 0.0;
+      }
+      if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
+      if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+      continue;
+    }
+    double val = 0, pgx = 0, pgy = 0, pgz = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      val = fma(w[c], G[c], val);
+      if (GRAD) {
+        pgx = fma(__shfl_sync(FULL, my_cw.y, c), G[c], pgx);
+        pgy = fma(__shfl_sync(FULL, my_cw.z, c), G[c], pgy);
+        pgz = fma(__shfl_sync(FULL, my_cw.w, c), G[c], pgz);
+      }
+      if (METRIC && on) cfim[c * 21 + lane] = G[c];
+    }
+    const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+    const double tgx = zy * R2 - zz * R1, tgy = zz * R0 - zx * R2, tgz = zx * R1 - zy * R0;  // z x d/dz
+    if (out.fim && on) {
+      const int pr = kPackR[lane], pc = kPackC[lane];
+      out.fim[q * 36 + pr * 6 + pc] = val;
+      out.fim[q * 36 + pc * 6 + pr] = val;
+    }
+    if (GRAD && out.fim_grad && on) {
+      const int pr = kPackR[lane], pc = kPackC[lane];
+      const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
+#pragma unroll
+      for (int d = 0; d < 6; ++d) {
+        out.fim_grad[q * 216 + d * 36 + pr * 6 + pc] = g6[d];
+        out.fim_grad[q * 216 + d * 36 + pc * 6 + pr] = g6[d];
+      }
+    }
+    if (out.trace || (GRAD && out.trace_grad)) {
+      const bool dg = on && kIsDiag[lane];
+      const double tv = warp_sum(dg ? val : 0.0);
+      if (out.trace && lane == 0) out.trace[q] = tv;
+      if (GRAD && out.trace_grad) {
+        const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+          const double sgl = warp_sum(dg ? g6[d] : 0.0);
+          if (lane == d) out.trace_grad[q * 6 + d] = sgl;
         }
       }
     }
-    double* pw = part + (size_t)warp * NP * 32;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) pw[c * 32 + lane] = G[c];
-    if (GRAD) {
-      pw[NC * 32 + lane] = R0;
-      pw[(NC + 1) * 32 + lane] = R1;
-      pw[(NC + 2) * 32 + lane] = R2;
-    }
-    __syncthreads();  // rows / weights consumed, partials visible
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(q + gridDim.x);
-    }
-    if (warp == 0) {
-      double Gs[NC];
-      double S0 = 0, S1 = 0, S2 = 0;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) Gs[c] = 0.0;
-      for (int ww = 0; ww < QB_WARPS; ++ww) {
-        const double* p = part + (size_t)ww * NP * 32;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) Gs[c] += p[c * 32 + lane];
-        if (GRAD) {
-          S0 += p[NC * 32 + lane];
-          S1 += p[(NC + 1) * 32 + lane];
-          S2 += p[(NC + 2) * 32 + lane];
+    if (METRIC) {
+      __syncwarp();
+      double mv_det = 0, mv_lmin = 0;
+      if (lane < NC) {
+        double a[36];
+        for (int x = 0; x < 21; ++x) {
+          const double v = cfim[lane * 21 + x];
+          a[kPackR[x] * 6 + kPackC[x]] = v;
+          a[kPackC[x] * 6 + kPackR[x]] = v;
+        }
+        if (rows[q * 8 + lane] >= 0) {
+          if (out.det) mv_det = det6(a);
+          if (out.lmin) mv_lmin = lmin6(a);
         }
       }
-      double val = 0, pgx = 0, pgy = 0, pgz = 0;
+      double mdet = 0, mlmin = 0;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        val = fma(w[c], Gs[c], val);
-        if (GRAD && r[c] >= 0) {
-          const double4 d = cw[q * 8 + c];
-          pgx = fma(d.y, Gs[c], pgx);
-          pgy = fma(d.z, Gs[c], pgy);
-          pgz = fma(d.w, Gs[c], pgz);
-        }
-        if (METRIC && on) cfim[c * 21 + lane] = Gs[c];
-      }
-      if (st != FIF_STATUS_OK) {
-        if (out.fim) for (int j = lane; j < 36; j += 32) out.fim[q * 36 + j] = 0.0;
-        if (out.fim_grad) for (int j = lane; j < 216; j += 32) out.fim_grad[q * 216 + j] = 0.0;
-        if (lane == 0) {
-          if (out.trace) out.trace[q] = 0.0;
-          if (out.det) out.det[q] = 0.0;
-          if (out.lmin) out.lmin[q] = 0.0;
-        }
-        if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
-      } else {
-        const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
-        const double tgx = zy * S2 - zz * S1, tgy = zz * S0 - zx * S2, tgz = zx * S1 - zy * S0;  // z x d/dz
-        if (out.fim && on) {
-          const int pr = kPackR[lane], pc = kPackC[lane];
-          out.fim[q * 36 + pr * 6 + pc] = val;
-          out.fim[q * 36 + pc * 6 + pr] = val;
-        }
-        if (GRAD && out.fim_grad && on) {
-          const int pr = kPackR[lane], pc = kPackC[lane];
-          const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
-#pragma unroll
-          for (int j = 0; j < 6; ++j) {
-            out.fim_grad[q * 216 + j * 36 + pr * 6 + pc] = g6[j];
-            out.fim_grad[q * 216 + j * 36 + pc * 6 + pr] = g6[j];
-          }
-        }
-        if (out.trace || (GRAD && out.trace_grad)) {
-          const bool dg = on && kIsDiag[lane];
-          const double tv = warp_sum(dg ? val : 0.0);
-          if (out.trace && lane == 0) out.trace[q] = tv;
-          if (GRAD && out.trace_grad) {
-            const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
-#pragma unroll
-            for (int j = 0; j < 6; ++j) {
-              const double sgl = warp_sum(dg ? g6[j] : 0.0);
-              if (lane == j) out.trace_grad[q * 6 + j] = sgl;
-            }
-          }
-        }
-        if (METRIC) {
-          __syncwarp();
-          double mv_det = 0, mv_lmin = 0;
-          if (lane < NC) {
-            double a[36];
-            for (int j = 0; j < 21; ++j) {
-              const double v = cfim[lane * 21 + j];
-              a[kPackR[j] * 6 + kPackC[j]] = v;
-              a[kPackC[j] * 6 + kPackR[j]] = v;
-            }
-            if (rows[q * 8 + lane] >= 0) {
-              if (out.det) mv_det = det6(a);
-              if (out.lmin) mv_lmin = lmin6(a);
-            }
-          }
-          double mdet = 0, mlmin = 0;
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            const double dd = __shfl_sync(0xffffffffu, mv_det, c), ll = __shfl_sync(0xffffffffu, mv_lmin, c);
-            if (w[c] != 0.0) {
-              mdet = fma(w[c], dd, mdet);
-              mlmin = fma(w[c], ll, mlmin);
-            }
-          }
-          if (lane == 0) {
-            if (out.det) out.det[q] = mdet;
-            if (out.lmin) out.lmin[q] = mlmin;
-          }
+        const double dd = __shfl_sync(0xffffffffu, mv_det, c), ll = __shfl_sync(0xffffffffu, mv_lmin, c);
+        if (w[c] != 0.0) {
+          mdet = fma(w[c], dd, mdet);
+          mlmin = fma(w[c], ll, mlmin);
         }
       }
-      if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+      if (lane == 0) {
+        if (out.det) out.det[q] = mdet;
+        if (out.lmin) out.lmin[q] = mlmin;
+      }
     }
-    __syncthreads();  // partials consumed before the next query overwrites them
+    if (out.status && lane == 0) out.status[q] = (uint8_t)st;
   }
 }
 
 // ───────────────────────── contraction: trace fields ────────────────────
+constexpr int QC_WARPS = 8;
 // Rows of n_v scalars: lanes stride over k, per-lane partial sums, warp reduction.
 template <typename T, int NC, bool GRAD>
 __global__ void __launch_bounds__(QC_WARPS * 32) k_query_trace(int nv, const T* __restrict__ field,
@@ -525,7 +558,7 @@ __global__ void __launch_bounds__(QC_WARPS * 32) k_query_trace(int nv, const T* 
                                                               const uint8_t* __restrict__ status,
                                                               const int32_t* __restrict__ rows,
                                                               const double4* __restrict__ cw,
-                                                              const double* __restrict__ wt, QueryOut out) {
+                                                              const double4* __restrict__ wt, QueryOut out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t q = blockIdx.x * (int64_t)QC_WARPS + warp; q < nq; q += (int64_t)gridDim.x * QC_WARPS) {
     const int st = status[q];
@@ -535,7 +568,7 @@ __global__ void __launch_bounds__(QC_WARPS * 32) k_query_trace(int nv, const T* 
       if (out.status && lane == 0) out.status[q] = (uint8_t)st;
       continue;
     }
-    const double* wq = wt + q * 4 * nv;
+    const double4* wq = wt + q * nv;
     int32_t r[NC];
     double w[NC];
 #pragma unroll
@@ -551,16 +584,16 @@ __global__ void __launch_bounds__(QC_WARPS * 32) k_query_trace(int nv, const T* 
       double s[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) s[c] = r[c] >= 0 ? (double)__ldg(field + (int64_t)r[c] * nv + k) : 0.0;
-      const double om = wq[k];
+      const double4 om = wq[k];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) G[c] = fma(om, s[c], G[c]);
+      for (int c = 0; c < NC; ++c) G[c] = fma(om.x, s[c], G[c]);
       if (GRAD) {
         double b = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c) b = fma(w[c], s[c], b);
-        R0 = fma(wq[nv + k], b, R0);
-        R1 = fma(wq[2 * nv + k], b, R1);
-        R2 = fma(wq[3 * nv + k], b, R2);
+        R0 = fma(om.y, b, R0);
+        R1 = fma(om.z, b, R1);
+        R2 = fma(om.w, b, R2);
       }
     }
     double val = 0, pgx = 0, pgy = 0, pgz = 0;
@@ -594,14 +627,28 @@ static unsigned query_blocks(int64_t q) {
   return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
 
+template <typename T, int NC, int STAGES, bool GRAD, bool METRIC>
+static void launch_info(int nv, const T* f, const double* axes, int64_t q, const uint8_t* status, const int32_t* rows,
+                        const double4* cw, const double4* wt, const QueryOut& out, cudaStream_t st) {
+  auto kern = k_query_info<T, NC, STAGES, GRAD, METRIC>;
+  const size_t smem = ((QWShape<T>::CHUNK + 127) & ~127u) +
+                      (size_t)QW_WARPS * ((qw_warp_bytes<T, NC, STAGES, METRIC>() + 127) & ~127u);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, QW_WARPS * 32, smem);
+  const int64_t need = (q + QW_WARPS - 1) / QW_WARPS;
+  const int64_t cap = (int64_t)kSMs * (per_sm > 0 ? per_sm : 1);
+  kern<<<(unsigned)(need < cap ? need : cap), QW_WARPS * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out);
+}
+
 template <typename T>
 static int launch_contract(int kind, bool trilinear, bool grad, bool metric, int nv, const void* field,
                            const double* axes, int64_t q, const uint8_t* status, const int32_t* rows,
-                           const double4* cw, const double* wt, const QueryOut& out, cudaStream_t st) {
+                           const double4* cw, const double4* wt, const QueryOut& out, cudaStream_t st) {
   const T* f = reinterpret_cast<const T*>(field);
-  const unsigned blocks = query_blocks(q);
-  const int threads = QC_WARPS * 32;
   if (kind == FIF_KIND_TRACE) {
+    const unsigned blocks = query_blocks(q);
+    const int threads = QC_WARPS * 32;
 #define QT(NC, G) k_query_trace<T, NC, G><<<blocks, threads, 0, st>>>(nv, f, axes, q, status, rows, cw, wt, out)
     if (trilinear) { if (grad) QT(8, true); else QT(8, false); }
     else { if (grad) QT(1, true); else QT(1, false); }
@@ -609,21 +656,11 @@ static int launch_contract(int kind, bool trilinear, bool grad, bool metric, int
     FIF_CHECK_LAUNCH("k_query_trace");
     return FIF_OK;
   }
-  const size_t rw_bytes = (size_t)nv * 21 * sizeof(T);
-  const size_t rowcap = ((rw_bytes + 16) + 15) & ~(size_t)15;
-  const int nc = trilinear ? 8 : 1;
-  const size_t smem = 128 + nc * rowcap + sizeof(double) * (4 * nv + QB_WARPS * (nc + 3) * 32 + 8 * 21);
-  FIF_CHECK_ARG(smem <= 220 * 1024, "fif_query: a %zu-byte field row does not fit the shared-memory pipeline",
-                rw_bytes);
-  const int per_sm = (int)((228 * 1024) / (smem + 1024));
-  int64_t cap = (int64_t)kSMs * (per_sm > 0 ? per_sm : 1);
-  const unsigned blocks_i = (unsigned)(q < cap ? q : cap);
-#define QI(NC, G, M)                                                                                      \
-  do {                                                                                                    \
-    auto kern = k_query_info<T, NC, G, M>;                                                                \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                   \
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                      \
-    kern<<<blocks_i, QB_WARPS * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out);              \
+  static const int stages_env = getenv("FIF_QW_STAGES") ? atoi(getenv("FIF_QW_STAGES")) : 2;
+#define QI(NC, G, M)                                                                   \
+  do {                                                                                 \
+    if (stages_env == 3) launch_info<T, NC, 3, G, M>(nv, f, axes, q, status, rows, cw, wt, out, st); \
+    else launch_info<T, NC, 2, G, M>(nv, f, axes, q, status, rows, cw, wt, out, st);   \
   } while (0)
   if (trilinear) {
     if (metric) { if (grad) QI(8, true, true); else QI(8, false, true); }
@@ -676,7 +713,7 @@ extern "C" int fif_query(int factor_kind, const fif_model* model, const fif_grid
   const size_t b_status = ((size_t)q + 255) & ~(size_t)255;
   const size_t b_rows = (size_t)q * 8 * sizeof(int32_t);
   const size_t b_cw = (size_t)q * 8 * sizeof(double4);
-  const size_t b_wt = (size_t)q * 4 * nv * sizeof(double);
+  const size_t b_wt = (size_t)q * nv * sizeof(double4);
   static bool pool_set = false;
   if (!pool_set) {
     int dev = 0;
@@ -696,8 +733,8 @@ extern "C" int fif_query(int factor_kind, const fif_model* model, const fif_grid
   uint8_t* s_status = scratch;
   double4* s_cw = reinterpret_cast<double4*>(scratch + b_status);
   int32_t* s_rows = reinterpret_cast<int32_t*>(scratch + b_status + b_cw);
-  double* s_wt = reinterpret_cast<double*>(scratch + b_status + b_cw + ((b_rows + 255) & ~(size_t)255));
-  const size_t prep_smem = sizeof(double) * QP_Q * 4 * nv;
+  double4* s_wt = reinterpret_cast<double4*>(scratch + b_status + b_cw + ((b_rows + 255) & ~(size_t)255));
+  const size_t prep_smem = sizeof(double) * (QP_Q + 3) * nv;
   if (prep_smem > 48 * 1024) cudaFuncSetAttribute(k_query_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem);
   k_query_prep<<<(unsigned)((q + QP_Q - 1) / QP_Q), QP_THREADS, prep_smem, st>>>(
       *model, gm, d_slots, d_positions, d_axes, q, trilinear ? 1 : 0, s_status, s_rows, s_cw, s_wt);

@@ -23,7 +23,7 @@ def main(rep, kernel=None):
         if k in seen:
             print(f"  {k:38s} {seen[k]}")
     raw = run(rep, "raw", kernel)
-    hdr, vals = raw[0], raw[2]
+    hdr, units, vals = raw[0], raw[1], raw[2]
     stalls = []
     keys = {}
     for h, v in zip(hdr, vals):
@@ -32,6 +32,7 @@ def main(rep, kernel=None):
                 stalls.append((float(v), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
             except ValueError:
                 pass
+        u = units[hdr.index(h)] if h in hdr else ""
         for k in ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
                   "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                   "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
@@ -39,7 +40,7 @@ def main(rep, kernel=None):
                   "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
                   "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum"):
             if h.startswith(k) and h not in keys:
-                keys[h] = v
+                keys[h] = f"{v} {u}"
     for h, v in keys.items():
         print(f"  {h:60s} {v}")
     tot = sum(v for v, _ in stalls) or 1

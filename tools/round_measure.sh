@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round-end measurement recipe (run under gpurun from the repo root).
+# Each ncu pass runs only after the same command exited 0 without ncu.
+set -u
+O=gpurun_out
+mkdir -p $O
+python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
+python bench.py > $O/bench.json 2> $O/bench.err || exit 1
+python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err
+python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $O/bench_short.json 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
+    python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $O/ncu_launch.log 2>&1
+python tools/prof_build.py --kind trace > $O/trace_build.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:k_gp_trace -c 1 -o $O/full_k_gp_trace -f \
+      python tools/prof_build.py --kind trace --reps 1 > $O/ncu_full_k_gp_trace.log 2>&1
+for k in k_gp_info_tc k_query_info k_pc_fim k_query_prep; do
+  ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o $O/full_$k -f \
+      python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_full_$k.log 2>&1
+done
