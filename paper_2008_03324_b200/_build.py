@@ -12,7 +12,9 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libfif_b200.so")
+# FIF_LIB points the loader at another build of the same sources (tuning variants
+# made by tools/build_variant.py); the default is the in-tree library.
+LIB = os.environ.get("FIF_LIB") or os.path.join(HERE, "libfif_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 

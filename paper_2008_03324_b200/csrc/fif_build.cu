@@ -675,7 +675,9 @@ k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc s
 // flushed to FP64 (shared memory) every GC_FLUSH landmarks.  B fragments (entries,
 // pre-split into TF32 hi/lo by phase A) are read from a bank-conflict-free layout.
 constexpr int GC_TILE = 64;       // landmarks per smem tile
-constexpr int GC_FLUSH_TILES = 4; // FP32 accumulators span 256 landmarks
+#ifndef GC_FLUSH_TILES
+#define GC_FLUSH_TILES 8          // FP32 accumulators span 512 landmarks, then FP64
+#endif
 constexpr int GC_MT = 5;          // m16 tiles per warp (80 samples)
 constexpr int GC_WARPS = 4;
 constexpr int GC_NT = 3;          // n8 tiles (24 >= 21 entries)
