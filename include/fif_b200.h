@@ -133,6 +133,28 @@ int fif_query(int factor_kind, const fif_model* model, const fif_grid* grid, con
               uint32_t flags, double* d_trace, double* d_trace_grad, double* d_fim, double* d_fim_grad,
               double* d_det, double* d_lmin, uint8_t* d_status, void* stream);
 
+/* Output set of fif_query_ex; every pointer is optional (NULL = not written).
+ * Shapes as in fif_query, plus d/d[t; theta] of the blended metrics:
+ *   det_grad (Q,6), lmin_grad (Q,6)  (with FIF_Q_GRAD and FIF_Q_DET / FIF_Q_LMIN).
+ * Per corner: d det F = det F tr(F^-1 dF) (0 for a singular corner),
+ * d lambda_min = v^T dF v (v the unit eigenvector); blended like the values.  */
+typedef struct fif_query_out {
+  double* trace;
+  double* trace_grad;
+  double* fim;
+  double* fim_grad;
+  double* det;
+  double* det_grad;
+  double* lmin;
+  double* lmin_grad;
+  uint8_t* status;
+} fif_query_out;
+
+/* fif_query with the output set passed as a struct (adds the metric gradients). */
+int fif_query_ex(int factor_kind, const fif_model* model, const fif_grid* grid, const void* d_field,
+                 const int32_t* d_slots, const double* d_positions, const double* d_axes, int64_t q, int mode,
+                 uint32_t flags, const fif_query_out* out, void* stream);
+
 /* Point-cloud brute force — replaces kernels.exact_fim_batch
  * (kernels.py:1638-1645 -> _nb_exact_fim 571-599).  R (Q,9) row-major
  * world-from-camera rotations, t (Q,3), landmarks (N,3), all f64.

@@ -24,7 +24,7 @@ BUILD_SIMT = 2
 
 EXPORTED = (
     "fif_abi_version", "fif_last_error", "fif_grid_centers", "fif_build_scratch_bytes", "fif_build",
-    "fif_export_reference", "fif_query", "fif_pc_fim", "fif_launch_count",
+    "fif_export_reference", "fif_query", "fif_query_ex", "fif_pc_fim", "fif_launch_count",
 )
 
 
@@ -44,6 +44,12 @@ class Model(ctypes.Structure):
         ("sig2", ctypes.c_double), ("ell", ctypes.c_double),
         ("zs", ctypes.c_void_p), ("kinv", ctypes.c_void_p),
     ]
+
+
+class QueryOut(ctypes.Structure):
+    """fif_query_out: device output pointers of fif_query_ex (NULL = not written)."""
+    _fields_ = [(n, ctypes.c_void_p) for n in ("trace", "trace_grad", "fim", "fim_grad", "det", "det_grad",
+                                                 "lmin", "lmin_grad", "status")]
 
 
 class Camera(ctypes.Structure):
@@ -82,6 +88,9 @@ def load():
         L.fif_query.restype = _int
         L.fif_query.argtypes = [_int, ctypes.POINTER(Model), ctypes.POINTER(Grid), _p, _p, _p, _p, _i64, _int,
                                 ctypes.c_uint32, _p, _p, _p, _p, _p, _p, _p, _p]
+        L.fif_query_ex.restype = _int
+        L.fif_query_ex.argtypes = [_int, ctypes.POINTER(Model), ctypes.POINTER(Grid), _p, _p, _p, _p, _i64, _int,
+                                   ctypes.c_uint32, ctypes.POINTER(QueryOut), _p]
         L.fif_pc_fim.restype = _int
         L.fif_pc_fim.argtypes = [_p, _p, _i64, _p, _i64, ctypes.POINTER(Camera), _d, _p, _p, _p]
         if L.fif_abi_version() != 1:

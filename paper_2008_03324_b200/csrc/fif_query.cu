@@ -139,6 +139,98 @@ __device__ double lmin6(const double* a_in) {
   return m;
 }
 
+// det6 plus F^-1 from the same LU (multipliers kept below the diagonal, rows
+// swapped whole, so P A = L U); returns det (identical to det6) and ok = false
+// for a singular matrix (inv untouched).
+__device__ double det6_inv(const double* a_in, double* inv, bool& ok) {
+  double a[36];
+  int perm[6];
+  for (int i = 0; i < 36; ++i) a[i] = a_in[i];
+  for (int i = 0; i < 6; ++i) perm[i] = i;
+  double det = 1.0;
+  ok = false;
+  for (int c = 0; c < 6; ++c) {
+    int p = c;
+    double best = fabs(a[6 * c + c]);
+    for (int r = c + 1; r < 6; ++r)
+      if (fabs(a[6 * r + c]) > best) { best = fabs(a[6 * r + c]); p = r; }
+    if (best == 0.0) return 0.0;
+    if (p != c) {
+      for (int k = 0; k < 6; ++k) { double t = a[6 * c + k]; a[6 * c + k] = a[6 * p + k]; a[6 * p + k] = t; }
+      int t = perm[c]; perm[c] = perm[p]; perm[p] = t;
+      det = -det;
+    }
+    double piv = a[6 * c + c];
+    det *= piv;
+    for (int r = c + 1; r < 6; ++r) {
+      double f = a[6 * r + c] / piv;
+      for (int k = c + 1; k < 6; ++k) a[6 * r + k] -= f * a[6 * c + k];
+      a[6 * r + c] = f;
+    }
+  }
+  for (int j = 0; j < 6; ++j) {  // column j of A^-1: solve L U x = P e_j
+    double x[6];
+    for (int i = 0; i < 6; ++i) {
+      double y = perm[i] == j ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) y -= a[6 * i + k] * x[k];
+      x[i] = y;
+    }
+    for (int i = 5; i >= 0; --i) {
+      double y = x[i];
+      for (int k = i + 1; k < 6; ++k) y -= a[6 * i + k] * x[k];
+      x[i] = y / a[6 * i + i];
+    }
+    for (int i = 0; i < 6; ++i) inv[6 * i + j] = x[i];
+  }
+  ok = true;
+  return det;
+}
+// lmin6 plus the unit eigenvector of the smallest eigenvalue (Jacobi rotations
+// accumulated into V); the eigenvalue is identical to lmin6's.
+__device__ double lmin6_vec(const double* a_in, double* vec) {
+  double a[36], V[36];
+  for (int i = 0; i < 36; ++i) { a[i] = a_in[i]; V[i] = (i % 7 == 0) ? 1.0 : 0.0; }
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int r = 0; r < 6; ++r)
+      for (int c = 0; c < 6; ++c) {
+        double v = a[6 * r + c] * a[6 * r + c];
+        tot += v;
+        if (r != c) off += v;
+      }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int p = 0; p < 5; ++p)
+      for (int q = p + 1; q < 6; ++q) {
+        double apq = a[6 * p + q];
+        if (apq == 0.0) continue;
+        double theta = (a[6 * q + q] - a[6 * p + p]) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < 6; ++k) {
+          double akp = a[6 * k + p], akq = a[6 * k + q];
+          a[6 * k + p] = cs * akp - sn * akq;
+          a[6 * k + q] = sn * akp + cs * akq;
+          double vkp = V[6 * k + p], vkq = V[6 * k + q];
+          V[6 * k + p] = cs * vkp - sn * vkq;
+          V[6 * k + q] = sn * vkp + cs * vkq;
+        }
+        for (int k = 0; k < 6; ++k) {
+          double apk = a[6 * p + k], aqk = a[6 * q + k];
+          a[6 * p + k] = cs * apk - sn * aqk;
+          a[6 * q + k] = sn * apk + cs * aqk;
+        }
+      }
+  }
+  double m = a[0];
+  int im = 0;
+  for (int k = 1; k < 6; ++k)
+    if (a[7 * k] < m) { m = a[7 * k]; im = k; }
+  m = a[0];
+  for (int k = 1; k < 6; ++k) m = fmin(m, a[7 * k]);
+  for (int i = 0; i < 6; ++i) vec[i] = V[6 * i + im];
+  return m;
+}
+
 __constant__ int kPackR[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
 __constant__ int kPackC[21] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5};
 __constant__ int kIsDiag[21] = {1, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 1, 0, 1};
@@ -150,7 +242,9 @@ struct QueryOut {
   double* fim;
   double* fim_grad;
   double* det;
+  double* det_grad;
   double* lmin;
+  double* lmin_grad;
   uint8_t* status;
 };
 
@@ -310,12 +404,17 @@ struct QWShape {
   static constexpr uint32_t CHUNK = KC * 21 * sizeof(T);
   static constexpr uint32_t CAP = (CHUNK + 32 + 15) & ~15u;  // + alignment slack both ends
 };
-template <typename T, int NC, int STAGES, bool METRIC>
+// per-warp METRIC scratch: per corner G (21) and, with metric gradients, H_a (3 x 21)
+template <bool METRIC, bool MGRAD>
+__host__ __device__ constexpr uint32_t qw_cf() {
+  return METRIC ? (MGRAD ? 84u : 21u) : 0u;
+}
+template <typename T, int NC, int STAGES, bool METRIC, bool MGRAD>
 __host__ __device__ constexpr uint32_t qw_warp_bytes() {
-  return 64 + STAGES * (NC * QWShape<T>::CAP + QWShape<T>::KC * 32) + (METRIC ? 8 * 21 * 8 : 0);
+  return 64 + STAGES * (NC * QWShape<T>::CAP + QWShape<T>::KC * 32) + 8 * 8 * qw_cf<METRIC, MGRAD>();
 }
 
-template <typename T, int NC, int STAGES, bool GRAD, bool METRIC>
+template <typename T, int NC, int STAGES, bool GRAD, bool METRIC, bool MGRAD>
 __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_info(int nv, const T* __restrict__ field,
                                                              const double* __restrict__ axes, int64_t nq,
                                                              const uint8_t* __restrict__ status,
@@ -327,13 +426,15 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
   constexpr uint32_t CAP = SH::CAP;
   constexpr uint32_t STAGE = NC * CAP + KC * 32;
   constexpr unsigned FULL = 0xffffffffu;
+  constexpr uint32_t CF = qw_cf<METRIC, MGRAD>();
+  static_assert(!MGRAD || (METRIC && GRAD), "metric gradients need METRIC and GRAD");
   extern __shared__ __align__(128) unsigned char qraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const T* zero_row = reinterpret_cast<const T*>(qraw);  // [CHUNK] zeros, shared
-  unsigned char* wbase = qraw + ((SH::CHUNK + 127) & ~127u) + (size_t)warp * ((qw_warp_bytes<T, NC, STAGES, METRIC>() + 127) & ~127u);
+  unsigned char* wbase = qraw + ((SH::CHUNK + 127) & ~127u) + (size_t)warp * ((qw_warp_bytes<T, NC, STAGES, METRIC, MGRAD>() + 127) & ~127u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(wbase);
   unsigned char* stages = wbase + 64;
-  double* cfim = reinterpret_cast<double*>(stages + STAGES * STAGE);  // METRIC: [8][21]
+  double* cfim = reinterpret_cast<double*>(stages + STAGES * STAGE);  // METRIC: [8][CF]
   for (int i = threadIdx.x; i < (int)(SH::CHUNK / 4); i += blockDim.x) reinterpret_cast<float*>(qraw)[i] = 0.f;
   if (lane == 0) {
     for (int b = 0; b < STAGES; ++b) mbar_init(&bars[b], 1);
@@ -414,6 +515,9 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
       c_st = status[qof(i + 1)];
     }
     double R0 = 0, R1 = 0, R2 = 0;
+    double H[MGRAD ? NC : 1][3];
+#pragma unroll
+    for (int c = 0; c < (MGRAD ? NC : 1); ++c) H[c][0] = H[c][1] = H[c][2] = 0.0;
     for (int j = 0; j < nch; ++j) {
       __syncwarp();  // every lane is done with the stage produce() refills next
       if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -436,7 +540,15 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
           for (int c = 0; c < NC; ++c) sv[c] = (double)src[c][kk * 21];
 #pragma unroll
           for (int c = 0; c < NC; ++c) G[c] = fma(om.x, sv[c], G[c]);
-          if (GRAD) {
+          if (MGRAD) {
+            // per-corner rotation derivatives (the metric gradients need each corner's dF)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              H[c][0] = fma(om.y, sv[c], H[c][0]);
+              H[c][1] = fma(om.z, sv[c], H[c][1]);
+              H[c][2] = fma(om.w, sv[c], H[c][2]);
+            }
+          } else if (GRAD) {
             // blend over corners as two independent chains (halves the DFMA dependency depth)
             double b0 = 0.0, b1 = 0.0;
 #pragma unroll
@@ -473,8 +585,23 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
         if (out.lmin) out.lmin[q] = 0.0;
       }
       if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
+      if (out.det_grad && lane < 6) out.det_grad[q * 6 + lane] = 0.0;
+      if (out.lmin_grad && lane < 6) out.lmin_grad[q * 6 + lane] = 0.0;
       if (out.status && lane == 0) out.status[q] = (uint8_t)st;
       continue;
+    }
+    if (MGRAD) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        R0 = fma(w[c], H[c][0], R0);
+        R1 = fma(w[c], H[c][1], R1);
+        R2 = fma(w[c], H[c][2], R2);
+        if (on) {
+          cfim[c * CF + 21 + lane] = H[c][0];
+          cfim[c * CF + 42 + lane] = H[c][1];
+          cfim[c * CF + 63 + lane] = H[c][2];
+        }
+      }
     }
     double val = 0, pgx = 0, pgy = 0, pgz = 0;
 #pragma unroll
@@ -485,7 +612,7 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
         pgy = fma(__shfl_sync(FULL, my_cw.z, c), G[c], pgy);
         pgz = fma(__shfl_sync(FULL, my_cw.w, c), G[c], pgz);
       }
-      if (METRIC && on) cfim[c * 21 + lane] = G[c];
+      if (METRIC && on) cfim[c * CF + lane] = G[c];
     }
     const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
     const double tgx = zy * R2 - zz * R1, tgy = zz * R0 - zx * R2, tgz = zx * R1 - zy * R0;  // z x d/dz
@@ -518,17 +645,50 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
     }
     if (METRIC) {
       __syncwarp();
-      double mv_det = 0, mv_lmin = 0;
+      double mv_det = 0, mv_lmin = 0, gd[3] = {0, 0, 0}, gl[3] = {0, 0, 0};
       if (lane < NC) {
+        const double* cf = cfim + lane * CF;
         double a[36];
         for (int x = 0; x < 21; ++x) {
-          const double v = cfim[lane * 21 + x];
+          const double v = cf[x];
           a[kPackR[x] * 6 + kPackC[x]] = v;
           a[kPackC[x] * 6 + kPackR[x]] = v;
         }
         if (rows[q * 8 + lane] >= 0) {
-          if (out.det) mv_det = det6(a);
-          if (out.lmin) mv_lmin = lmin6(a);
+          if (out.det) {
+            if (MGRAD && out.det_grad) {
+              double inv[36];
+              bool ok;
+              mv_det = det6_inv(a, inv, ok);
+              if (ok)
+                for (int ax = 0; ax < 3; ++ax) {  // d det = det tr(F^-1 dF), dF packed symmetric
+                  double t = 0.0;
+                  for (int x = 0; x < 21; ++x) {
+                    const int r = kPackR[x], c = kPackC[x];
+                    t = fma(r == c ? inv[7 * r] : inv[6 * r + c] + inv[6 * c + r], cf[21 * (1 + ax) + x], t);
+                  }
+                  gd[ax] = mv_det * t;
+                }
+            } else {
+              mv_det = det6(a);
+            }
+          }
+          if (out.lmin) {
+            if (MGRAD && out.lmin_grad) {
+              double v6[6];
+              mv_lmin = lmin6_vec(a, v6);
+              for (int ax = 0; ax < 3; ++ax) {  // d lambda = v^T dF v
+                double t = 0.0;
+                for (int x = 0; x < 21; ++x) {
+                  const int r = kPackR[x], c = kPackC[x];
+                  t = fma(r == c ? v6[r] * v6[r] : 2.0 * v6[r] * v6[c], cf[21 * (1 + ax) + x], t);
+                }
+                gl[ax] = t;
+              }
+            } else {
+              mv_lmin = lmin6(a);
+            }
+          }
         }
       }
       double mdet = 0, mlmin = 0;
@@ -543,6 +703,17 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
       if (lane == 0) {
         if (out.det) out.det[q] = mdet;
         if (out.lmin) out.lmin[q] = mlmin;
+      }
+      if (MGRAD) {
+        // lane c < NC holds its corner's (w, dw) in my_cw; other lanes hold zeros
+        auto blend_grad = [&](double val_c, const double (&gz)[3], double* dst) {
+          const double tx = warp_sum(my_cw.y * val_c), ty = warp_sum(my_cw.z * val_c), tz = warp_sum(my_cw.w * val_c);
+          const double zxg = warp_sum(my_cw.x * gz[0]), zyg = warp_sum(my_cw.x * gz[1]), zzg = warp_sum(my_cw.x * gz[2]);
+          const double g6[6] = {tx, ty, tz, zy * zzg - zz * zyg, zz * zxg - zx * zzg, zx * zyg - zy * zxg};
+          if (lane < 6) dst[q * 6 + lane] = g6[lane];
+        };
+        if (out.det_grad) blend_grad(mv_det, gd, out.det_grad);
+        if (out.lmin_grad) blend_grad(mv_lmin, gl, out.lmin_grad);
       }
     }
     if (out.status && lane == 0) out.status[q] = (uint8_t)st;
@@ -627,12 +798,12 @@ static unsigned query_blocks(int64_t q) {
   return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
 
-template <typename T, int NC, int STAGES, bool GRAD, bool METRIC>
+template <typename T, int NC, int STAGES, bool GRAD, bool METRIC, bool MGRAD>
 static void launch_info(int nv, const T* f, const double* axes, int64_t q, const uint8_t* status, const int32_t* rows,
                         const double4* cw, const double4* wt, const QueryOut& out, cudaStream_t st) {
-  auto kern = k_query_info<T, NC, STAGES, GRAD, METRIC>;
+  auto kern = k_query_info<T, NC, STAGES, GRAD, METRIC, MGRAD>;
   const size_t smem = ((QWShape<T>::CHUNK + 127) & ~127u) +
-                      (size_t)QW_WARPS * ((qw_warp_bytes<T, NC, STAGES, METRIC>() + 127) & ~127u);
+                      (size_t)QW_WARPS * ((qw_warp_bytes<T, NC, STAGES, METRIC, MGRAD>() + 127) & ~127u);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, QW_WARPS * 32, smem);
@@ -641,8 +812,28 @@ static void launch_info(int nv, const T* f, const double* axes, int64_t q, const
   kern<<<(unsigned)(need < cap ? need : cap), QW_WARPS * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out);
 }
 
+template <typename T, int NC>
+static void launch_info_nc(bool grad, bool metric, bool mgrad, int nv, const T* f, const double* axes, int64_t q,
+                           const uint8_t* status, const int32_t* rows, const double4* cw, const double4* wt,
+                           const QueryOut& out, cudaStream_t st) {
+  // value/gradient streaming: 2 stages, 3 CTAs/SM; metric variants (det/lmin, LU and
+  // Jacobi per corner, more registers): 3 stages, 2 CTAs/SM
+  static const int stages_env = getenv("FIF_QW_STAGES") ? atoi(getenv("FIF_QW_STAGES")) : 2;
+  if (metric) {
+    if (mgrad) launch_info<T, NC, 3, true, true, true>(nv, f, axes, q, status, rows, cw, wt, out, st);
+    else if (grad) launch_info<T, NC, 3, true, true, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+    else launch_info<T, NC, 3, false, true, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+  } else if (stages_env == 3) {
+    if (grad) launch_info<T, NC, 3, true, false, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+    else launch_info<T, NC, 3, false, false, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+  } else {
+    if (grad) launch_info<T, NC, 2, true, false, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+    else launch_info<T, NC, 2, false, false, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+  }
+}
+
 template <typename T>
-static int launch_contract(int kind, bool trilinear, bool grad, bool metric, int nv, const void* field,
+static int launch_contract(int kind, bool trilinear, bool grad, bool metric, bool mgrad, int nv, const void* field,
                            const double* axes, int64_t q, const uint8_t* status, const int32_t* rows,
                            const double4* cw, const double4* wt, const QueryOut& out, cudaStream_t st) {
   const T* f = reinterpret_cast<const T*>(field);
@@ -656,20 +847,8 @@ static int launch_contract(int kind, bool trilinear, bool grad, bool metric, int
     FIF_CHECK_LAUNCH("k_query_trace");
     return FIF_OK;
   }
-  static const int stages_env = getenv("FIF_QW_STAGES") ? atoi(getenv("FIF_QW_STAGES")) : 2;
-#define QI(NC, G, M)                                                                   \
-  do {                                                                                 \
-    if (stages_env == 3) launch_info<T, NC, 3, G, M>(nv, f, axes, q, status, rows, cw, wt, out, st); \
-    else launch_info<T, NC, 2, G, M>(nv, f, axes, q, status, rows, cw, wt, out, st);   \
-  } while (0)
-  if (trilinear) {
-    if (metric) { if (grad) QI(8, true, true); else QI(8, false, true); }
-    else { if (grad) QI(8, true, false); else QI(8, false, false); }
-  } else {
-    if (metric) { if (grad) QI(1, true, true); else QI(1, false, true); }
-    else { if (grad) QI(1, true, false); else QI(1, false, false); }
-  }
-#undef QI
+  if (trilinear) launch_info_nc<T, 8>(grad, metric, mgrad, nv, f, axes, q, status, rows, cw, wt, out, st);
+  else launch_info_nc<T, 1>(grad, metric, mgrad, nv, f, axes, q, status, rows, cw, wt, out, st);
   FIF_CHECK_LAUNCH("k_query_info");
   return FIF_OK;
 }
@@ -682,7 +861,14 @@ extern "C" int fif_query(int factor_kind, const fif_model* model, const fif_grid
                          const int32_t* d_slots, const double* d_positions, const double* d_axes, int64_t q, int mode,
                          uint32_t flags, double* d_trace, double* d_trace_grad, double* d_fim, double* d_fim_grad,
                          double* d_det, double* d_lmin, uint8_t* d_status, void* stream) {
-  FIF_CHECK_ARG(model && grid, "fif_query: NULL model/grid");
+  fif_query_out o{d_trace, d_trace_grad, d_fim, d_fim_grad, d_det, nullptr, d_lmin, nullptr, d_status};
+  return fif_query_ex(factor_kind, model, grid, d_field, d_slots, d_positions, d_axes, q, mode, flags, &o, stream);
+}
+
+extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_grid* grid, const void* d_field,
+                            const int32_t* d_slots, const double* d_positions, const double* d_axes, int64_t q,
+                            int mode, uint32_t flags, const fif_query_out* o, void* stream) {
+  FIF_CHECK_ARG(model && grid && o, "fif_query: NULL model/grid/outputs");
   FIF_CHECK_ARG(factor_kind == FIF_KIND_INFO || factor_kind == FIF_KIND_TRACE, "fif_query: bad factor_kind");
   FIF_CHECK_ARG(mode == FIF_MODE_NEAREST || mode == FIF_MODE_TRILINEAR, "fif_query: bad mode %d", mode);
   FIF_CHECK_ARG(q >= 0, "fif_query: q < 0");
@@ -691,21 +877,26 @@ extern "C" int fif_query(int factor_kind, const fif_model* model, const fif_grid
   FIF_CHECK_ARG(model->kind == FIF_MODEL_QUAD || (model->kind == FIF_MODEL_GP && model->zs && model->kinv),
                 "fif_query: bad model");
   const bool info = factor_kind == FIF_KIND_INFO;
-  FIF_CHECK_ARG(info || !(d_fim || d_fim_grad || d_det || d_lmin),
+  const bool want_g = (flags & FIF_Q_GRAD) != 0;
+  FIF_CHECK_ARG(info || !((o->fim && (flags & FIF_Q_FULL)) || (o->fim_grad && (flags & FIF_Q_FULL) && want_g) ||
+                          (o->det && (flags & FIF_Q_DET)) || (o->lmin && (flags & FIF_Q_LMIN))),
                 "fif_query: full FIM / det / lmin need an info field (WrongFactorKind)");
   FIF_CHECK_ARG(grid->voxel_size > 0, "fif_query: voxel_size <= 0");
   const int nv = model->kind == FIF_MODEL_QUAD ? 10 : model->n_v;
   FIF_CHECK_ARG(nv >= 1 && nv <= 1024, "fif_query: n_v out of range");
   QueryGeom gm{grid->origin[0], grid->origin[1], grid->origin[2], grid->voxel_size,
                grid->dims[0],   grid->dims[1],   grid->dims[2]};
-  QueryOut out{(flags & FIF_Q_TRACE) ? d_trace : nullptr,
-               (flags & FIF_Q_TRACE) && (flags & FIF_Q_GRAD) ? d_trace_grad : nullptr,
-               (flags & FIF_Q_FULL) ? d_fim : nullptr,
-               (flags & FIF_Q_FULL) && (flags & FIF_Q_GRAD) ? d_fim_grad : nullptr,
-               (flags & FIF_Q_DET) ? d_det : nullptr,
-               (flags & FIF_Q_LMIN) ? d_lmin : nullptr,
-               d_status};
-  const bool grad = (flags & FIF_Q_GRAD) && (out.trace_grad || out.fim_grad);
+  QueryOut out{(flags & FIF_Q_TRACE) ? o->trace : nullptr,
+               (flags & FIF_Q_TRACE) && want_g ? o->trace_grad : nullptr,
+               (flags & FIF_Q_FULL) ? o->fim : nullptr,
+               (flags & FIF_Q_FULL) && want_g ? o->fim_grad : nullptr,
+               (flags & FIF_Q_DET) ? o->det : nullptr,
+               (flags & FIF_Q_DET) && want_g ? o->det_grad : nullptr,
+               (flags & FIF_Q_LMIN) ? o->lmin : nullptr,
+               (flags & FIF_Q_LMIN) && want_g ? o->lmin_grad : nullptr,
+               o->status};
+  const bool mgrad = info && (out.det_grad || out.lmin_grad);
+  const bool grad = want_g && (out.trace_grad || out.fim_grad || mgrad);
   const bool metric = info && (out.det || out.lmin);
   const bool trilinear = mode == FIF_MODE_TRILINEAR;
   cudaStream_t st = (cudaStream_t)stream;
@@ -740,10 +931,10 @@ extern "C" int fif_query(int factor_kind, const fif_model* model, const fif_grid
       *model, gm, d_slots, d_positions, d_axes, q, trilinear ? 1 : 0, s_status, s_rows, s_cw, s_wt);
   FIF_CHECK_LAUNCH("k_query_prep");
   const bool f64 = model->kind == FIF_MODEL_QUAD || (flags & FIF_Q_FIELD_F64);
-  int rc = f64 ? launch_contract<double>(factor_kind, trilinear, grad, metric, nv, d_field, d_axes, q, s_status,
-                                         s_rows, s_cw, s_wt, out, st)
-               : launch_contract<float>(factor_kind, trilinear, grad, metric, nv, d_field, d_axes, q, s_status,
-                                        s_rows, s_cw, s_wt, out, st);
+  int rc = f64 ? launch_contract<double>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q,
+                                         s_status, s_rows, s_cw, s_wt, out, st)
+               : launch_contract<float>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q,
+                                        s_status, s_rows, s_cw, s_wt, out, st);
   cudaFreeAsync(scratch, st);
   return rc;
 }

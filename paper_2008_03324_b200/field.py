@@ -396,7 +396,7 @@ class Field:
             return t
 
         flags = 0
-        tr_t = trg_t = fim_t = fimg_t = det_t = lmin_t = None
+        tr_t = trg_t = fim_t = fimg_t = det_t = lmin_t = detg_t = lming_t = None
         if trace:
             flags |= _lib.Q_TRACE
             tr_t = buf("trace", ())
@@ -412,16 +412,20 @@ class Field:
         if det:
             flags |= _lib.Q_DET
             det_t = buf("det", ())
+            if grad:
+                detg_t = buf("det_grad", (6,))
         if lmin:
             flags |= _lib.Q_LMIN
             lmin_t = buf("lmin", ())
+            if grad:
+                lming_t = buf("lmin_grad", (6,))
         st_t = buf("status", (), torch.uint8)
         field_t, is64 = self._field_ptr(field_f64)
         if is64 and isinstance(self.model, GpVisibility):
             flags |= _lib.Q_FIELD_F64
         kind = _lib.KIND_INFO if self._is_info else _lib.KIND_TRACE
         if self.rows == 0:
-            for t in (tr_t, trg_t, fim_t, fimg_t, det_t, lmin_t):
+            for t in (tr_t, trg_t, fim_t, fimg_t, det_t, lmin_t, detg_t, lming_t):
                 if t is not None:
                     t.zero_()
             # every voxel is empty: status still follows the grid geometry
@@ -430,12 +434,11 @@ class Field:
         slots = None if self._dense else self._slots_dev
         if self.rows == 0:
             slots = torch.full((self.config.voxel_count,), -1, dtype=torch.int32, device=dev)
-        _lib.check(_lib.load().fif_query(kind, self._dm.c, self._grid_c, _lib.ptr(field_t), _lib.ptr(slots),
-                                         _lib.ptr(positions), _lib.ptr(axes), q,
-                                         _lib.MODE_TRILINEAR if trilinear else _lib.MODE_NEAREST, flags,
-                                         _lib.ptr(tr_t), _lib.ptr(trg_t), _lib.ptr(fim_t), _lib.ptr(fimg_t),
-                                         _lib.ptr(det_t), _lib.ptr(lmin_t), _lib.ptr(st_t),
-                                         _device.stream_handle(dev)), "fif_query")
+        o = _lib.QueryOut(*(_lib.ptr(t) for t in (tr_t, trg_t, fim_t, fimg_t, det_t, detg_t, lmin_t, lming_t, st_t)))
+        _lib.check(_lib.load().fif_query_ex(kind, self._dm.c, self._grid_c, _lib.ptr(field_t), _lib.ptr(slots),
+                                            _lib.ptr(positions), _lib.ptr(axes), q,
+                                            _lib.MODE_TRILINEAR if trilinear else _lib.MODE_NEAREST, flags, o,
+                                            _device.stream_handle(dev)), "fif_query")
         return out
 
     def query_batch(self, positions, rotations=None, axes=None, outputs=("trace", "full"), grad: bool = False,
@@ -443,7 +446,8 @@ class Field:
         """Batched query with optional analytic pose gradients (new in this build).
 
         outputs subset of {"trace", "full", "det", "lmin"}.  Gradients are d/d[t; theta]
-        for t' = t + dt, R' = exp(dtheta^) R; shapes: trace_grad (Q,6), fim_grad (Q,6,6,6).
+        for t' = t + dt, R' = exp(dtheta^) R; shapes: trace_grad / det_grad / lmin_grad (Q,6),
+        fim_grad (Q,6,6,6).  det/lmin gradients: per corner det F tr(F^-1 dF) and v^T dF v.
         """
         dev = self.device
         pos = _device.to_device_f64(positions, dev, (3,))
@@ -459,7 +463,7 @@ class Field:
                                 det="det" in outs, lmin="lmin" in outs)
         q = pos.shape[0]
         ret = {"in_field": res["status"] == 0}
-        for k in ("trace", "trace_grad", "det", "lmin"):
+        for k in ("trace", "trace_grad", "det", "det_grad", "lmin", "lmin_grad"):
             if k in res:
                 ret[k] = res[k]
         if "fim" in res:

@@ -206,3 +206,53 @@ def test_factorization_exact_at_voxel_centres(models):
             direct = sum(float(vr @ vp[i]) * F.landmark_fim(c, pts[i]) for i in range(len(pts)))
             tol = 1e-9 if mname == "quad" else 1e-5
             assert np.linalg.norm(got - direct) <= tol * np.linalg.norm(direct)
+
+
+@pytest.mark.parametrize("mname", ["quad", "gp70"])
+@pytest.mark.parametrize("metric", ["det", "lmin"])
+def test_metric_gradients_vs_finite_difference(oracle, g_small, models, small_grid, mname, metric):
+    """d det / d lambda_min w.r.t. [t; theta] against central FD of
+    the oracle's blended metric (kernels.py:1429-1472), h = 1e-6."""
+    m = models[mname]
+    factors = g_small[f"factors_{mname}_info"]
+    f = field_from_reference(small_grid, m, "info", factors)
+    rng = np.random.default_rng(23)
+    c = small_grid.centers()
+    pos = rng.uniform(c[0], c[-1], size=(60, 3))
+    g = (pos - small_grid.origin) / small_grid.voxel_size - 0.5
+    frac = g - np.floor(g)
+    pos = pos[((frac > 1e-3) & (frac < 1 - 1e-3)).all(axis=1)]
+    rots = np.stack([F.random_rotation(rng) for _ in range(pos.shape[0])])
+    slots = np.arange(small_grid.voxel_count, dtype=np.int32)
+    om = oracle_model(m)
+
+    def ev(p, r):
+        v, _ = oracle.metric_batch(slots, factors, small_grid.origin, small_grid.voxel_size, small_grid.dims, p,
+                                   np.ascontiguousarray(r[:, :, 2]), om, metric, False, True)
+        return v
+
+    h = 1e-6
+    fd = np.zeros((pos.shape[0], 6))
+    for j in range(6):
+        if j < 3:
+            d = np.zeros(3)
+            d[j] = h
+            fd[:, j] = (ev(pos + d, rots) - ev(pos - d, rots)) / (2 * h)
+        else:
+            w = np.zeros(3)
+            w[j - 3] = h
+            fd[:, j] = (ev(pos, np.einsum("ij,qjk->qik", so3_exp(w), rots)) -
+                        ev(pos, np.einsum("ij,qjk->qik", so3_exp(-w), rots))) / (2 * h)
+    val = ev(pos, rots)
+    for f64 in (True, False):
+        dev = torch.device("cuda")
+        res = f.query_device(torch.tensor(pos, device=dev), torch.tensor(np.ascontiguousarray(rots[:, :, 2]), device=dev),
+                             "trilinear", trace=False, grad=True, det=metric == "det", lmin=metric == "lmin",
+                             field_f64=f64)
+        mine_v = res[metric].cpu().numpy()
+        mine_g = res[f"{metric}_grad"].cpu().numpy()
+        tol = TOL if (f64 or isinstance(m, F.QuadraticVisibility)) else 5 * TOL
+        ev_err = np.abs(mine_v - val) / np.abs(val)
+        assert ev_err.max() <= tol, (f64, ev_err.max())
+        err = np.linalg.norm(mine_g - fd, axis=1) / np.linalg.norm(fd, axis=1)
+        assert err.max() <= tol, (f64, err.max())
