@@ -163,6 +163,23 @@ int fif_query_ex(int factor_kind, const fif_model* model, const fif_grid* grid, 
 int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, const double* d_points, int64_t n_points,
                const fif_camera* cam, double sigma, double* d_out, uint8_t* d_mask, void* stream);
 
+/* Matchability gates — replaces the range and view-cone parts of
+ * Matchability.mask (field.py:143-165).  d_mask (rows, n_points) uint8, row-major:
+ * 1 = the (centre, landmark) pair contributes.  FP64, bit-identical with the
+ * reference's numpy arithmetic (norm order (x^2 + y^2) + z^2; einsum order
+ * (x + z) + y).  Occlusion and Python predicates stay on the host.          */
+#define FIF_MATCH_NEAR 1u  /* dist >= d_near     */
+#define FIF_MATCH_FAR 2u   /* dist <= d_far      */
+#define FIF_MATCH_CONE 4u  /* cos(angle to view_dir) >= cos_beta (needs d_view_dirs (N,3)) */
+typedef struct fif_match {
+  double d_near;
+  double d_far;
+  double cos_beta;
+  uint32_t flags;
+} fif_match;
+int fif_match_mask(const fif_match* match, const double* d_centers, int64_t rows, const double* d_points,
+                   const double* d_view_dirs, int64_t n_points, uint8_t* d_mask, void* stream);
+
 /* Number of kernel launches issued by this library since load (for bench
  * accounting of gpu_launches). */
 int64_t fif_launch_count(void);

@@ -24,7 +24,8 @@ BUILD_SIMT = 2
 
 EXPORTED = (
     "fif_abi_version", "fif_last_error", "fif_grid_centers", "fif_build_scratch_bytes", "fif_build",
-    "fif_export_reference", "fif_query", "fif_query_ex", "fif_pc_fim", "fif_launch_count",
+    "fif_export_reference", "fif_query", "fif_query_ex", "fif_pc_fim", "fif_match_mask",
+    "fif_launch_count",
 )
 
 
@@ -50,6 +51,14 @@ class QueryOut(ctypes.Structure):
     """fif_query_out: device output pointers of fif_query_ex (NULL = not written)."""
     _fields_ = [(n, ctypes.c_void_p) for n in ("trace", "trace_grad", "fim", "fim_grad", "det", "det_grad",
                                                  "lmin", "lmin_grad", "status")]
+
+
+class Match(ctypes.Structure):
+    _fields_ = [("d_near", ctypes.c_double), ("d_far", ctypes.c_double), ("cos_beta", ctypes.c_double),
+                ("flags", ctypes.c_uint32)]
+
+
+MATCH_NEAR, MATCH_FAR, MATCH_CONE = 1, 2, 4
 
 
 class Camera(ctypes.Structure):
@@ -91,6 +100,8 @@ def load():
         L.fif_query_ex.restype = _int
         L.fif_query_ex.argtypes = [_int, ctypes.POINTER(Model), ctypes.POINTER(Grid), _p, _p, _p, _p, _i64, _int,
                                    ctypes.c_uint32, ctypes.POINTER(QueryOut), _p]
+        L.fif_match_mask.restype = _int
+        L.fif_match_mask.argtypes = [ctypes.POINTER(Match), _p, _i64, _p, _p, _i64, _p, _p]
         L.fif_pc_fim.restype = _int
         L.fif_pc_fim.argtypes = [_p, _p, _i64, _p, _i64, ctypes.POINTER(Camera), _d, _p, _p, _p]
         if L.fif_abi_version() != 1:

@@ -147,7 +147,48 @@ class Matchability:
             parts.append("custom")
         return "+".join(parts)
 
+    @property
+    def gpu_gates(self) -> bool:
+        """Range / view-cone gates present (evaluated on the GPU by fif_match_mask)."""
+        return self.d_near is not None or self.d_far is not None or self.view_cone_beta is not None
+
+    @property
+    def host_gates(self) -> bool:
+        """Occlusion / Python predicate present (host only, as in the reference)."""
+        return self.occluders is not None or self.predicate is not None
+
+    def device_mask(self, centers: torch.Tensor, points: torch.Tensor, view_dirs=None) -> torch.Tensor:
+        """(V, N) uint8 mask on the device: the range / view-cone gates on the GPU
+        (fif_match_mask, bit-identical with `mask`), AND the host-only gates."""
+        dev = points.device
+        V, N = centers.shape[0], points.shape[0]
+        if self.gpu_gates:
+            m = _lib.Match()
+            m.flags = 0
+            if self.d_near is not None:
+                m.d_near, m.flags = float(self.d_near), m.flags | _lib.MATCH_NEAR
+            if self.d_far is not None:
+                m.d_far, m.flags = float(self.d_far), m.flags | _lib.MATCH_FAR
+            vd = None
+            if self.view_cone_beta is not None:
+                if view_dirs is None:
+                    raise ValueError("view_cone_beta requires landmark view directions")
+                m.cos_beta, m.flags = float(np.cos(self.view_cone_beta)), m.flags | _lib.MATCH_CONE
+                vd = _device.to_device_f64(view_dirs, dev, (3,))
+            out = torch.empty((V, N), dtype=torch.uint8, device=dev)
+            _lib.check(_lib.load().fif_match_mask(m, _lib.ptr(centers), V, _lib.ptr(points), _lib.ptr(vd), N,
+                                                  _lib.ptr(out), _device.stream_handle(dev)), "fif_match_mask")
+        else:
+            out = torch.ones((V, N), dtype=torch.uint8, device=dev)
+        if self.host_gates:
+            host = Matchability(occluders=self.occluders, predicate=self.predicate)
+            hm = host.mask(_device.to_numpy(centers), _device.to_numpy(points), view_dirs)
+            out &= torch.from_numpy(hm).to(dev)
+        return out
+
     def mask(self, centers, points, view_dirs=None):
+        """Host restatement of the reference's mask (field.py:143-177); the build uses
+        `device_mask`, this is the parity reference for it."""
         if self.is_trivial:
             return None
         d = points[None, :, :] - centers[:, None, :]
@@ -212,6 +253,10 @@ class _DeviceModel:
             m.zs, m.kinv = zs.data_ptr(), kinv.data_ptr()
         self.c = m
 
+
+# masked builds evaluate the matchability gates for at most this many (voxel, landmark)
+# pairs at a time (one byte each), bounding device memory for large maps
+_MASK_CHUNK_BYTES = 1 << 30
 
 # GP info builds run on the tensor pipe (mma.sync TF32x3) unless this is set; the FP32
 # SIMT kernel is kept as a cross-check and for models the tensor kernel does not cover.
@@ -349,18 +394,33 @@ class Field:
         if matchability.is_trivial:
             s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, grid=config, exact=exact)
             return Field(config, model, factor_kind, sigma, s64, s32, None, matchability, dense=True)
-        pts_np = points.cpu().numpy() if isinstance(points, torch.Tensor) else points
+        # matchability-masked build: gates on the GPU, voxel chunks bounded to
+        # _MASK_CHUNK_BYTES of mask, occupied rows kept in the reference's linear order
         centers = config.centers()
-        mask = matchability.mask(centers, pts_np, view_dirs)
-        occupied = mask.any(axis=1)
-        lin = np.nonzero(occupied)[0]
-        sub_c = torch.from_numpy(np.ascontiguousarray(centers[occupied])).to(dev)
-        sub_m = torch.from_numpy(np.ascontiguousarray(mask[occupied])).to(dev)
-        if lin.size:
-            s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, centers=sub_c, mask=sub_m, exact=exact)
+        n = points.shape[0]
+        chunk = max(1, min(config.voxel_count, _MASK_CHUNK_BYTES // max(1, n)))
+        parts64, parts32, lins = [], [], []
+        for c0 in range(0, config.voxel_count, chunk):
+            c1 = min(config.voxel_count, c0 + chunk)
+            cen = torch.from_numpy(np.ascontiguousarray(centers[c0:c1])).to(dev)
+            mask = matchability.device_mask(cen, pts_dev, view_dirs)
+            occ = torch.nonzero(mask.any(dim=1)).flatten()
+            if occ.numel() == 0:
+                continue
+            s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, centers=cen[occ].contiguous(),
+                                  mask=mask[occ].contiguous(), exact=exact)
+            parts64.append(s64)
+            if s32 is not None:
+                parts32.append(s32)
+            lins.append(occ.cpu().numpy() + c0)
+        if parts64:
+            s64 = torch.cat(parts64)
+            s32 = torch.cat(parts32) if parts32 else None
+            lin = np.concatenate(lins)
         else:
             s64 = torch.zeros((0, width), dtype=torch.float64, device=dev)
             s32 = s64.float() if gp else None
+            lin = np.zeros(0, dtype=np.int64)
         return Field(config, model, factor_kind, sigma, s64, s32, config.index3_of(lin).astype(np.int32),
                      matchability, dense=False)
 
@@ -561,15 +621,20 @@ class Field:
                                 dmodel=self._dm, f32_copy=False)
             self._s64.add_(inc, alpha=sign)
         else:
-            pts_np = pts.cpu().numpy() if isinstance(pts, torch.Tensor) else pts
             centers = self.config.centers()
-            mask = self.matchability.mask(centers, pts_np, vd if vd is not None else view_dirs)
-            touched = np.ones(self.config.voxel_count, bool) if mask is None else mask.any(axis=1)
+            cen = torch.from_numpy(np.ascontiguousarray(centers)).to(dev)
+            if self.matchability.is_trivial:
+                mask = None
+                touched = np.ones(self.config.voxel_count, bool)
+            else:
+                mask = self.matchability.device_mask(cen, pts_dev, vd if vd is not None else view_dirs)
+                touched = _device.to_numpy(mask.any(dim=1))
             if not touched.any():
                 return
             lin = np.nonzero(touched)[0]
-            sub_c = torch.from_numpy(np.ascontiguousarray(centers[touched])).to(dev)
-            sub_m = None if mask is None else torch.from_numpy(np.ascontiguousarray(mask[touched])).to(dev)
+            sel = torch.from_numpy(lin).to(dev)
+            sub_c = cen[sel].contiguous()
+            sub_m = None if mask is None else mask[sel].contiguous()
             inc, _ = build_rows(pts_dev, self.model, want_trace, self.sigma, dev, centers=sub_c, mask=sub_m,
                                 dmodel=self._dm, f32_copy=False)
             if self._dense:

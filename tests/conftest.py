@@ -56,3 +56,8 @@ def oracle():
 
     O.lib()
     return O
+
+
+@pytest.fixture(scope="session")
+def g_match():
+    return golden("match.npz")

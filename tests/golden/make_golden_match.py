@@ -1,0 +1,50 @@
+"""Golden fixtures for matchability (field.py:101-180) from the reference package.
+
+Run ONLY in the authoring container:
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/nbcache \
+        python tests/golden/make_golden_match.py
+Writes match.npz: the reference's Matchability.mask for range / view-cone gates
+(with pairs placed exactly on the range limits) and masked field builds
+(occupied rows + reference-layout factors) through fifield.build.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+import fifield
+from fifield.field import GridConfig, Matchability
+from fifield.scenes import Scene
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+rng = np.random.default_rng(31)
+cfg = GridConfig(np.array([-1.0, -1.0, 0.0]), 0.5, np.array([6, 5, 4]))
+centers = cfg.centers()
+n = 300
+pts = rng.uniform([-3, -3, -0.5], [3, 3, 2.5], size=(n, 3))
+vd = rng.standard_normal((n, 3))
+vd /= np.linalg.norm(vd, axis=1, keepdims=True)
+dist = np.linalg.norm(pts[None] - centers[:, None], axis=2)
+d_near = float(dist[7, 11])   # pairs exactly on the limits must be accepted (>=, <=)
+d_far = float(dist[23, 42])
+cases = {
+    "range": Matchability(d_near=d_near, d_far=d_far),
+    "near": Matchability(d_near=d_near),
+    "cone": Matchability(view_cone_beta=1.1),
+    "range_cone": Matchability(d_near=0.4, d_far=2.2, view_cone_beta=0.9),
+    "sparse": Matchability(d_near=0.3, d_far=0.75, view_cone_beta=0.8),
+}
+arrays = dict(centers=centers, points=pts, view_dirs=vd, d_near=np.array(d_near), d_far=np.array(d_far))
+for name, mt in cases.items():
+    arrays[f"mask_{name}"] = mt.mask(centers, pts, vd)
+scene = Scene(pts, vd)
+quad = fifield.build_quad_model(alpha=np.pi / 4, v_alpha=0.5)
+gp30 = fifield.build_gp_model(30)
+for mname, model in (("quad", quad), ("gp30", gp30)):
+    for kind in ("trace", "info"):
+        f = fifield.build(scene, cfg, model, kind, matchability=cases["sparse"])
+        arrays[f"occ3_{mname}_{kind}"] = f.occupied_index3
+        arrays[f"factors_{mname}_{kind}"] = f.factors
+np.savez_compressed(os.path.join(OUT, "match.npz"), **arrays)
+print("wrote match.npz", {k: np.asarray(v).shape for k, v in arrays.items()})
