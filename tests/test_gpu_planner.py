@@ -1,0 +1,100 @@
+"""Planner-facing helpers: metric + analytic d/d[x,y,z,yaw] at
+(position, yaw) states vs central differences of the oracle's metric, and the
+trajectory information cost gradient vs finite differences."""
+import numpy as np
+import pytest
+
+import paper_2008_03324_b200 as F
+from paper_2008_03324_b200 import planner as P
+from tests._helpers import models_from_golden, oracle_model
+from tests.test_gpu_query import field_from_reference
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_metric(oracle, g_small, grid, model, metric, pos, yaws, trilinear):
+    slots = np.arange(grid.voxel_count, dtype=np.int32)
+    v, st = oracle.metric_batch(slots, g_small[f"factors_{_name(model)}_info"], grid.origin, grid.voxel_size,
+                                grid.dims, pos, np.ascontiguousarray(P.yaw_axes(yaws)), oracle_model(model), metric,
+                                False, trilinear)
+    return v, st
+
+
+def _name(model):
+    return "quad" if isinstance(model, F.QuadraticVisibility) else f"gp{model.n_v}"
+
+
+@pytest.fixture(scope="module")
+def setup(g_small, g_models):
+    models = models_from_golden(g_models)
+    grid = F.GridConfig(g_small["origin"], float(np.asarray(g_small["voxel_size"]).reshape(-1)[0]), g_small["dims"])
+    return models, grid
+
+
+@pytest.mark.parametrize("metric", ["det", "lmin", "trace"])
+@pytest.mark.parametrize("mode", ["nearest", "trilinear"])
+def test_metric_yaw_gradient(oracle, g_small, setup, metric, mode):
+    models, grid = setup
+    m = models["gp70"]
+    f = field_from_reference(grid, m, "info", g_small["factors_gp70_info"])
+    rng = np.random.default_rng(5)
+    c = grid.centers()
+    pos = rng.uniform(c[0], c[-1], size=(40, 3))
+    g = (pos - grid.origin) / grid.voxel_size - (0.5 if mode == "trilinear" else 0.0)
+    frac = g - np.floor(g)
+    pos = pos[((frac > 1e-3) & (frac < 1 - 1e-3)).all(axis=1)]
+    yaws = rng.uniform(-np.pi, np.pi, pos.shape[0])
+    tri = mode == "trilinear"
+    v, st = _oracle_metric(oracle, g_small, grid, m, metric, pos, yaws, tri)
+    h = 1e-6
+    fd = np.zeros((pos.shape[0], 4))
+    for j in range(4):
+        if j < 3:
+            d = np.zeros(3)
+            d[j] = h
+            fd[:, j] = (_oracle_metric(oracle, g_small, grid, m, metric, pos + d, yaws, tri)[0] -
+                        _oracle_metric(oracle, g_small, grid, m, metric, pos - d, yaws, tri)[0]) / (2 * h)
+        else:
+            fd[:, j] = (_oracle_metric(oracle, g_small, grid, m, metric, pos, yaws + h, tri)[0] -
+                        _oracle_metric(oracle, g_small, grid, m, metric, pos, yaws - h, tri)[0]) / (2 * h)
+    for f64 in (True, False):
+        r = P.metric_yaw_batch(f, pos, yaws, metric, mode, grad=True, field_f64=f64)
+        assert np.array_equal(r["in_field"], st == 0)
+        assert np.allclose(r["values"], v, rtol=1e-4 if f64 else 5e-4, atol=0)
+        err = np.linalg.norm(r["grad"] - fd, axis=1) / np.maximum(np.linalg.norm(fd, axis=1), 1e-300)
+        # FP32 S copy: lambda_min's eigenvector (and so d lambda) is sensitive to 1/gap
+        tol = 1e-4 if f64 else (2e-3 if metric == "lmin" else 5e-4)
+        assert err.max() <= tol, (f64, err.max())
+
+
+def test_info_cost_gradient_and_gate(oracle, g_small, setup):
+    models, grid = setup
+    m = models["quad"]
+    f = field_from_reference(grid, m, "info", g_small["factors_quad_info"])
+    rng = np.random.default_rng(9)
+    c = grid.centers()
+    pos = rng.uniform(c[0], c[-1], size=(30, 3))
+    yaws = rng.uniform(-np.pi, np.pi, 30)
+    vals = P.metric_yaw_batch(f, pos, yaws, "det", "trilinear")["values"]
+    pot = P.PotentialParams(epsilon=float(np.median(vals)), k_q=2.0)
+    cost, g = P.info_cost_grad(f, pos, yaws, "det", pot, mu_v=0.7, dt=0.1, mode="trilinear")
+
+    def total(p, y):
+        v, st = _oracle_metric(oracle, g_small, grid, m, "det", p, y, True)
+        return 0.7 * 0.1 * np.where(st == 0, P.info_potential(v, pot), pot.b_l).sum()
+
+    assert cost == pytest.approx(total(pos, yaws), rel=1e-9)
+    h = 1e-6
+    for t in range(0, 30, 7):
+        for j in range(4):
+            pp, yp, pm, ym = pos.copy(), yaws.copy(), pos.copy(), yaws.copy()
+            if j < 3:
+                pp[t, j] += h
+                pm[t, j] -= h
+            else:
+                yp[t] += h
+                ym[t] -= h
+            fd = (total(pp, yp) - total(pm, ym)) / (2 * h)
+            assert g[t, j] == pytest.approx(fd, rel=1e-4, abs=1e-9 * max(1.0, abs(fd)))
+    ok = P.gate_ok(f, pos, yaws, "det", pot.epsilon, "trilinear")
+    assert np.array_equal(ok, vals >= pot.epsilon)
