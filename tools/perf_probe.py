@@ -26,7 +26,7 @@ for name, model, tr, ex in [('quad trace', quad, True, False), ('quad trace exac
                             ('gp70 trace', gp70, True, False), ('gp70 info', gp70, False, False)]:
     dm = FD._DeviceModel(model, dev)
     ms = timeit(lambda: FD.build_rows(pts, model, tr, 1.0, dev, grid=grid, dmodel=dm, exact=ex))
-    print(f'{name:18s} {ms:9.2f} ms  {pairs/ms/1e6:.3e} pairs/s', flush=True)
+    print(f'{name:18s} {ms:9.2f} ms  {pairs/ms*1e3:.3e} pairs/s', flush=True)
 
 # GP precision at config-2 scale on sampled voxels (explicit centres) vs the oracle
 rng = np.random.default_rng(5)
