@@ -355,6 +355,126 @@ __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeo
   }
 }
 
+// GP prep on the FP64 tensor core: Omega[(q, a)][k] = sum_g U[(q, a)][g] kinv[g][k],
+// U[(q, 0)] = v^r(q), U[(q, a)] = v^r(q) . zs_a / l^2, as mma.sync m8n8k4 f64 (DMMA,
+// IEEE FP64 products and sums): an m8 tile = 2 queries x 4 weight rows, kinv staged
+// once per CTA in smem (zero padded to a multiple of 8), v^r per query in smem.
+// Same outputs as k_query_prep; used when kinv fits in shared memory.
+constexpr int QD_Q = 32;
+constexpr int QD_THREADS = 256;
+
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, QueryGeom gm,
+                                                              const int32_t* __restrict__ slots,
+                                                              const double* __restrict__ pos,
+                                                              const double* __restrict__ axes, int64_t nq,
+                                                              int trilinear, uint8_t* __restrict__ status,
+                                                              int32_t* __restrict__ rows, double4* __restrict__ cw,
+                                                              double* __restrict__ wt) {
+  extern __shared__ double smd[];
+  constexpr int NP8 = 8 * NT, KS = NP8 / 4;
+  constexpr int MT_PER_WARP = QD_Q / 2 / (QD_THREADS / 32);
+  const int nv = m.n_v;
+  double* kf = smd;                  // kinv B fragments: [KS][NT][32] (fragment order, zero padded)
+  double* sv = kf + KS * NT * 32;    // [QD_Q][NP8] v^r
+  double* sa = sv + QD_Q * NP8;      // [NP8][4] {1, zs/l^2}
+  const int64_t q0 = blockIdx.x * (int64_t)QD_Q;
+  const int t = threadIdx.x;
+  if (t < QD_Q && q0 + t < nq) {  // corners and trilinear weights (FP64, reference order)
+    const int64_t q = q0 + t;
+    int nc = 0;
+    int64_t r[8];
+    double w[8], dw[8][3];
+    const int st = locate(gm, slots, pos[3 * q], pos[3 * q + 1], pos[3 * q + 2], trilinear != 0, nc, r, w, dw);
+    status[q] = (uint8_t)st;
+    for (int c = 0; c < 8; ++c) {
+      const bool ok = st == FIF_STATUS_OK && c < nc;
+      rows[q * 8 + c] = ok ? (int32_t)r[c] : -1;
+      cw[q * 8 + c] = ok ? make_double4(w[c], dw[c][0], dw[c][1], dw[c][2]) : make_double4(0, 0, 0, 0);
+    }
+  }
+  const double inv_l2 = 1.0 / (m.ell * m.ell);
+  for (int idx = t; idx < KS * NT * 32; idx += blockDim.x) {  // B[g][k] = kinv[g][k], g = 4ks+tq, k = 8nt+row
+    const int ln = idx & 31, f = idx >> 5, ks = f / NT, nt = f - ks * NT;
+    const int g = 4 * ks + (ln & 3), k = 8 * nt + (ln >> 2);
+    kf[idx] = (g < nv && k < nv) ? m.kinv[(int64_t)g * nv + k] : 0.0;
+  }
+  for (int g = t; g < NP8; g += blockDim.x) {
+    const bool ok = g < nv;
+    sa[4 * g] = ok ? 1.0 : 0.0;
+    sa[4 * g + 1] = ok ? m.zs[3 * g] * inv_l2 : 0.0;
+    sa[4 * g + 2] = ok ? m.zs[3 * g + 1] * inv_l2 : 0.0;
+    sa[4 * g + 3] = ok ? m.zs[3 * g + 2] * inv_l2 : 0.0;
+  }
+  for (int idx = t; idx < QD_Q * NP8; idx += blockDim.x) {  // v^r (kernels.py:652-657)
+    const int qi = idx / NP8, g = idx - qi * NP8;
+    const int64_t q = q0 + qi;
+    double v = 0.0;
+    if (q < nq && g < nv) {
+      const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * q], m.zs[3 * g]), __dmul_rn(axes[3 * q + 1], m.zs[3 * g + 1])),
+                                 __dmul_rn(axes[3 * q + 2], m.zs[3 * g + 2]));
+      v = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
+    }
+    sv[idx] = v;
+  }
+  __syncthreads();
+  const int warp = t >> 5, lane = t & 31;
+  const int row = lane >> 2, tq = lane & 3;  // A/C row; A col = B row = tq
+  const int qq = row >> 2, a = row & 3;     // m8 row -> (query of the pair, weight row)
+  // each warp owns MT_PER_WARP m-tiles (2 queries each) and all NT n-tiles: every B
+  // fragment load feeds MT_PER_WARP DMMAs, every A fragment NT DMMAs
+  double c[MT_PER_WARP][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT_PER_WARP; ++i)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) c[i][n][0] = c[i][n][1] = 0.0;
+  const double* kfl = kf + lane;
+#pragma unroll 1
+  for (int ks = 0; ks < KS; ++ks) {
+    const int g = 4 * ks + tq;
+    const double sg = sa[4 * g + a];
+    double av[MT_PER_WARP];
+#pragma unroll
+    for (int i = 0; i < MT_PER_WARP; ++i) {
+      const int qi = (warp + i * (QD_THREADS / 32)) * 2 + qq;
+      av[i] = sv[qi * NP8 + g] * sg;
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const double b = kfl[(ks * NT + n) * 32];
+#pragma unroll
+      for (int i = 0; i < MT_PER_WARP; ++i) dmma_884(c[i][n][0], c[i][n][1], av[i], b);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < MT_PER_WARP; ++i) {
+    const int64_t q = q0 + (warp + i * (QD_THREADS / 32)) * 2 + qq;
+    if (q >= nq) continue;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int k = n * 8 + 2 * tq;
+      if (k < nv) wt[(q * nv + k) * 4 + a] = c[i][n][0];
+      if (k + 1 < nv) wt[(q * nv + k + 1) * 4 + a] = c[i][n][1];
+    }
+  }
+}
+
+template <int NT>
+static void launch_prep_gp(size_t smem, int64_t q, cudaStream_t st, const fif_model& m, const QueryGeom& gm,
+                           const int32_t* slots, const double* pos, const double* axes, int trilinear,
+                           uint8_t* status, int32_t* rows, double4* cw, double* wt) {
+  auto kern = k_query_prep_gp<NT>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<(unsigned)((q + QD_Q - 1) / QD_Q), QD_THREADS, smem, st>>>(m, gm, slots, pos, axes, q, trilinear, status,
+                                                                     rows, cw, wt);
+}
+
 // ───────────────────────── contraction: info fields ─────────────────────
 // One warp per query, lane e < 21 owns packed entry e.  Each warp streams its
 // queries through a private QW_STAGES-deep ring of k-chunks: one chunk = KC
@@ -925,11 +1045,26 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
   double4* s_cw = reinterpret_cast<double4*>(scratch + b_status);
   int32_t* s_rows = reinterpret_cast<int32_t*>(scratch + b_status + b_cw);
   double4* s_wt = reinterpret_cast<double4*>(scratch + b_status + b_cw + ((b_rows + 255) & ~(size_t)255));
-  const size_t prep_smem = sizeof(double) * (QP_Q + 3) * nv;
-  if (prep_smem > 48 * 1024) cudaFuncSetAttribute(k_query_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem);
-  k_query_prep<<<(unsigned)((q + QP_Q - 1) / QP_Q), QP_THREADS, prep_smem, st>>>(
-      *model, gm, d_slots, d_positions, d_axes, q, trilinear ? 1 : 0, s_status, s_rows, s_cw, s_wt);
-  FIF_CHECK_LAUNCH("k_query_prep");
+  const int np8 = (nv + 7) & ~7, ntiles = np8 / 8;
+  const size_t dmma_smem = sizeof(double) * ((size_t)np8 * np8 + (size_t)QD_Q * np8 + 4 * (size_t)np8);
+  static const bool simt_prep = getenv("FIF_QUERY_PREP_SIMT") != nullptr;
+  if (model->kind == FIF_MODEL_GP && ntiles <= 12 && !simt_prep) {
+    double* wtd = reinterpret_cast<double*>(s_wt);
+    const int tri = trilinear ? 1 : 0;
+    switch (ntiles) {
+#define PG(NT) case NT: launch_prep_gp<NT>(dmma_smem, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows, s_cw, wtd); break;
+      PG(1) PG(2) PG(3) PG(4) PG(5) PG(6) PG(7) PG(8) PG(9) PG(10) PG(11) PG(12)
+#undef PG
+    }
+    FIF_CHECK_LAUNCH("k_query_prep_gp");
+  } else {
+    const size_t prep_smem = sizeof(double) * (QP_Q + 3) * nv;
+    if (prep_smem > 48 * 1024)
+      cudaFuncSetAttribute(k_query_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem);
+    k_query_prep<<<(unsigned)((q + QP_Q - 1) / QP_Q), QP_THREADS, prep_smem, st>>>(
+        *model, gm, d_slots, d_positions, d_axes, q, trilinear ? 1 : 0, s_status, s_rows, s_cw, s_wt);
+    FIF_CHECK_LAUNCH("k_query_prep");
+  }
   const bool f64 = model->kind == FIF_MODEL_QUAD || (flags & FIF_Q_FIELD_F64);
   int rc = f64 ? launch_contract<double>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q,
                                          s_status, s_rows, s_cw, s_wt, out, st)

@@ -256,3 +256,31 @@ def test_metric_gradients_vs_finite_difference(oracle, g_small, models, small_gr
         assert ev_err.max() <= tol, (f64, ev_err.max())
         err = np.linalg.norm(mine_g - fd, axis=1) / np.linalg.norm(fd, axis=1)
         assert err.max() <= tol, (f64, err.max())
+
+
+@pytest.mark.parametrize("ns", [7, 150])
+def test_gp_query_other_sizes(oracle, ns):
+    """GP query path at N_s = 7 (one k-chunk) and N_s = 150 (kinv too large for the DMMA
+    prep's shared-memory tile: SIMT prep) on a GPU-built field vs the oracle."""
+    from tests._helpers import oracle_field
+
+    m = F.build_gp_model(ns)
+    rng = np.random.default_rng(ns)
+    pts = rng.uniform([-3, -3, 0], [3, 3, 2], size=(250, 3))
+    grid = F.GridConfig(np.array([-1.0, -1.0, 0.25]), 0.5, np.array([4, 4, 3]))
+    f = F.Field.build(pts, grid, m, "info")
+    c = grid.centers()
+    pos = rng.uniform(c[0], c[-1], size=(50, 3))
+    rots = np.stack([F.random_rotation(rng) for _ in range(50)])
+    res = f.query_batch(pos, rotations=rots, outputs=("trace", "full"), grad=True, to_numpy=True)
+    rows = oracle_field(oracle, m, c, pts, "info")
+    slots = np.arange(grid.voxel_count, dtype=np.int32)
+    ax = np.ascontiguousarray(rots[:, :, 2])
+    rt, st = oracle.metric_batch(slots, rows, grid.origin, grid.voxel_size, grid.dims, pos, ax, oracle_model(m),
+                                 "trace", False, True)
+    rf, _ = oracle.query_fim_batch(slots, rows, grid.origin, grid.voxel_size, grid.dims, pos, ax, oracle_model(m),
+                                   True)
+    assert np.array_equal(res["in_field"], st == 0)
+    assert rel(res["trace"], rt).max() <= TOL
+    e = np.linalg.norm((res["fim"] - rf).reshape(50, -1), axis=1) / np.linalg.norm(rf.reshape(50, -1), axis=1)
+    assert e.max() <= TOL
