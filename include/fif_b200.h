@@ -52,6 +52,7 @@ extern "C" {
 /* fif_build flags */
 #define FIF_BUILD_EXACT 1u  /* quad: reproduce _nb_build_quad's FP64 operation order bit for bit     */
 #define FIF_BUILD_SIMT 2u   /* GP info: FP32 SIMT (FFMA2) kernel instead of the tensor-pipe kernel   */
+#define FIF_BUILD_TF32 4u   /* GP info: TF32x3 tensor kernel instead of the default FP16-split one    */
 
 /* Axis-aligned voxel grid (field.py:45-98 GridConfig). */
 typedef struct fif_grid {

@@ -21,6 +21,7 @@ MODE_NEAREST, MODE_TRILINEAR = 0, 1
 Q_TRACE, Q_FULL, Q_GRAD, Q_DET, Q_LMIN, Q_FIELD_F64 = 1, 2, 4, 8, 16, 32
 BUILD_EXACT = 1
 BUILD_SIMT = 2
+BUILD_TF32 = 4
 
 EXPORTED = (
     "fif_abi_version", "fif_last_error", "fif_grid_centers", "fif_build_scratch_bytes", "fif_build",

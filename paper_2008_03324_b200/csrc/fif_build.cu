@@ -16,6 +16,8 @@
 #include <cstdarg>
 #include <mutex>
 
+#include <cuda_fp16.h>
+
 #include "fif_common.cuh"
 
 namespace fif {
@@ -872,6 +874,228 @@ k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSr
   }
 }
 
+// ─────────────────── GP, info on the tensor pipe: FP16 split ─────────────
+// Same contraction as k_gp_info_tc, as mma.sync m16n8k16 with FP16 operands: one MMA
+// covers 16 landmarks (twice the TF32 k8 step at the same instruction cost), with the
+// same 3-term split (hi*hi + hi*lo + lo*hi: ~22-bit products, FP32 accumulation).
+// FP16's range is managed by exact power-of-two scales:
+//   A' = 2^12 vs (sigmoid in (0, 1]; the scale folds into the reciprocal's argument),
+//   B' = s E with s = 2^(13 - floor(log2 max|E|)) per voxel, lowered (and the FP32
+//   accumulators rescaled by the same power of two) whenever a landmark tile holds a
+//   larger entry, reset after every FP64 flush; the flush divides by 2^12 s exactly.
+// Entries below max|E| 2^-17 keep an absolute error <= 2^-37 max|E| (FP16 subnormal
+// spacing), far under the FP32 accumulation error of the voxel's sums.
+__device__ __forceinline__ void h16_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 b = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - b.x, x1 - b.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+__device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+constexpr int H16_BEXP = 13;  // |B'| < 2^14
+
+template <bool HAS_MASK, bool DEAD_TOP>
+__global__ void __launch_bounds__(GC_WARPS * 32, 2)
+k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1,
+              int ns, int wpv, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax,
+              float bx, double* __restrict__ out64, float* __restrict__ out32) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int vpc = GC_WARPS / wpv;                                   // voxels per CTA
+  float* eh = reinterpret_cast<float*>(smem_raw);                   // [vpc][GC_TILE][24] entries (FP32)
+  float4* uu = reinterpret_cast<float4*>(eh + vpc * GC_TILE * 24);  // [vpc][GC_TILE] bearings
+  float4* tile = uu + vpc * GC_TILE;                                // [GC_TILE][2] landmarks
+  float* cs = reinterpret_cast<float*>(tile + GC_TILE * 2);         // [vpc][6] centre hi/lo
+  int* tmax = reinterpret_cast<int*>(cs + 6 * GC_WARPS);            // [vpc] max |entry| of the tile (bits)
+  double* acc = reinterpret_cast<double*>(tmax + 2 * GC_WARPS);     // [GC_WARPS][GC_MT*GC_NT*4][32]
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int vl = warp / wpv, mg = warp - vl * wpv;
+  const int64_t vbase = v0 + blockIdx.x * (int64_t)vpc;
+  const int64_t myv = vbase + vl;
+  if (t < vpc) {
+    const int64_t v = vbase + t;
+    float ch[3], cl[3];
+    voxel_split(src, v < v1 ? v : v0, ch, cl);
+    for (int k = 0; k < 3; ++k) {
+      cs[6 * t + k] = ch[k];
+      cs[6 * t + 3 + k] = cl[k];
+    }
+  }
+  double* myacc = acc + (size_t)warp * GC_MT * GC_NT * 4 * 32;
+  for (int i = 0; i < GC_MT * GC_NT * 4; ++i) myacc[i * 32 + lane] = 0.0;
+  float zr[GC_MT][2][3];
+#pragma unroll
+  for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = (mg * GC_MT + m) * 16 + gid + 8 * h;
+      const bool ok = g < ns;
+      zr[m][h][0] = ok ? (float)(ax * zs[3 * g]) : 0.f;
+      zr[m][h][1] = ok ? (float)(ax * zs[3 * g + 1]) : 0.f;
+      zr[m][h][2] = ok ? (float)(ax * zs[3 * g + 2]) : 0.f;
+    }
+  float c[GC_MT][GC_NT][4];
+#pragma unroll
+  for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+    for (int n = 0; n < GC_NT; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[m][n][i] = 0.f;
+  float s_cur = 0x1p100f;  // B scale of the current FP32 accumulation span (power of two)
+  const int npairs = vpc * GC_TILE;
+  int tiles = 0;
+  for (int64_t base = 0; base < n_pad; base += GC_TILE) {
+    __syncthreads();
+    for (int j = t; j < GC_TILE * 2; j += blockDim.x) tile[j] = lm[2 * base + j];
+    if (t < vpc) tmax[t] = 0;
+    __syncthreads();
+    // phase A: per (voxel, landmark) bearing + 21 entries, and the voxel's max |entry|
+    for (int pidx = t; pidx < npairs; pidx += blockDim.x) {
+      const int pv = pidx / GC_TILE, pj = pidx - pv * GC_TILE;  // warp-uniform pv (32 | GC_TILE)
+      float4 a = tile[2 * pj], b = tile[2 * pj + 1];
+      if ((vbase + pv) >= v1) b.w = 0.f;
+      if (HAS_MASK) {
+        const int64_t i = base + pj;
+        if (b.w != 0.f && mask[(vbase + pv - v0) * n_real + i] == 0) b.w = 0.f;
+      }
+      const float* cc = cs + 6 * pv;
+      const float ch[3] = {cc[0], cc[1], cc[2]}, cl[3] = {cc[3], cc[4], cc[5]};
+      const PairF q = pair_prologue(a, b, ch, cl, inv_s2);
+      float e[21];
+      entries21(q, a, e);
+      float mx = 0.f;
+#pragma unroll
+      for (int k = 0; k < 21; ++k) mx = fmaxf(mx, fabsf(e[k]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) atomicMax(&tmax[pv], __float_as_int(mx));
+      float4* dh = reinterpret_cast<float4*>(eh + (pv * GC_TILE + pj) * 24);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) dh[k] = make_float4(e[4 * k], e[4 * k + 1], e[4 * k + 2], e[4 * k + 3]);
+      dh[5] = make_float4(e[20], 0.f, 0.f, 0.f);
+      uu[pv * GC_TILE + pj] = make_float4(q.ux, q.uy, q.uz, 0.f);
+    }
+    __syncthreads();
+    if (vl < vpc) {
+      const float tm = __int_as_float(tmax[vl]);
+      if (tm > 0.f) {  // lower the B scale if this tile holds a larger entry (exact rescale)
+        const int ex = ((__float_as_int(tm) >> 23) & 0xff) - 127;
+        const int be = min(254, max(1, 127 + H16_BEXP - ex));
+        const float s_need = __int_as_float(be << 23);
+        if (s_need < s_cur) {
+          const float r = s_need / s_cur;
+#pragma unroll
+          for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+            for (int n = 0; n < GC_NT; ++n)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) c[m][n][i] *= r;
+          s_cur = s_need;
+        }
+      }
+      const float* ehv = eh + vl * GC_TILE * 24;
+      const float4* uv = uu + vl * GC_TILE;
+      // A fragment (m16n8k16, f16): reg0 (row gid, k 2tig..+1), reg1 (row gid+8, k 2tig..+1),
+      // reg2 (row gid, k 2tig+8..+9), reg3 (row gid+8, k 2tig+8..+9); low half = lower k
+      auto afrag_m = [&](int k0, int m, uint32_t (&ah)[4], uint32_t (&al)[4]) {
+        const float4 u[4] = {uv[k0 + 2 * tig], uv[k0 + 2 * tig + 1], uv[k0 + 2 * tig + 8], uv[k0 + 2 * tig + 9]};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int h = r & 1, kb = (r >> 1) * 2;
+          if (DEAD_TOP && h == 1 && m == GC_MT - 1) {
+            ah[r] = al[r] = 0u;
+            continue;
+          }
+          float sg[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const float4 uj = u[kb + j];
+            const float x = fmaf(uj.x, zr[m][h][0], fmaf(uj.y, zr[m][h][1], fmaf(uj.z, zr[m][h][2], bx)));
+            sg[j] = rcp_approx(fmaf(ex2_approx(x), 0x1p-12f, 0x1p-12f));  // 2^12 / (1 + 2^x)
+          }
+          h16_split2(sg[0], sg[1], ah[r], al[r]);
+        }
+      };
+      uint32_t ah[GC_MT][4], al[GC_MT][4];
+#pragma unroll
+      for (int m = 0; m < GC_MT; ++m) afrag_m(0, m, ah[m], al[m]);
+#pragma unroll 1
+      for (int k0 = 0; k0 < GC_TILE; k0 += 16) {
+        // B fragment (f16): reg0 (k 2tig..+1, col gid), reg1 (k 2tig+8..+9, col gid)
+        uint32_t bh[GC_NT][2], bl[GC_NT][2];
+#pragma unroll
+        for (int n = 0; n < GC_NT; ++n) {
+          const float* eb = ehv + 8 * n + gid;
+          h16_split2(eb[(k0 + 2 * tig) * 24] * s_cur, eb[(k0 + 2 * tig + 1) * 24] * s_cur, bh[n][0], bl[n][0]);
+          h16_split2(eb[(k0 + 2 * tig + 8) * 24] * s_cur, eb[(k0 + 2 * tig + 9) * 24] * s_cur, bh[n][1], bl[n][1]);
+        }
+        const int kn = (k0 + 16) & (GC_TILE - 1);  // next step (wraps harmlessly on the last)
+        uint32_t nh[GC_MT][4], nl[GC_MT][4];
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int n = 0; n < GC_NT; ++n) mma_f16(c[m][n], ah[m], bh[n][0], bh[n][1]);
+        afrag_m(kn, 0, nh[0], nl[0]);
+        afrag_m(kn, 1, nh[1], nl[1]);
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int n = 0; n < GC_NT; ++n) mma_f16(c[m][n], ah[m], bl[n][0], bl[n][1]);
+        afrag_m(kn, 2, nh[2], nl[2]);
+        afrag_m(kn, 3, nh[3], nl[3]);
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int n = 0; n < GC_NT; ++n) mma_f16(c[m][n], al[m], bh[n][0], bh[n][1]);
+        afrag_m(kn, 4, nh[4], nl[4]);
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            ah[m][i] = nh[m][i];
+            al[m][i] = nl[m][i];
+          }
+      }
+      if (++tiles == GC_FLUSH_TILES || base + GC_TILE >= n_pad) {
+        tiles = 0;
+        const double unscale = 0x1p-12 / (double)s_cur;  // exact power of two
+#pragma unroll
+        for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+          for (int n = 0; n < GC_NT; ++n)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              myacc[((m * GC_NT + n) * 4 + i) * 32 + lane] += (double)c[m][n][i] * unscale;
+              c[m][n][i] = 0.f;
+            }
+        s_cur = 0x1p100f;
+      }
+    }
+  }
+  if (vl < vpc && myv < v1) {
+    const int64_t r = myv - v0;
+#pragma unroll
+    for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+      for (int n = 0; n < GC_NT; ++n)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int g = (mg * GC_MT + m) * 16 + gid + ((i >> 1) << 3);
+          const int en = 8 * n + 2 * tig + (i & 1);
+          if (g >= ns || en >= 21) continue;
+          const double v = myacc[((m * GC_NT + n) * 4 + i) * 32 + lane];
+          out64[(r * ns + g) * 21 + en] = v;
+          if (out32) out32[(r * ns + g) * 21 + en] = (float)v;
+        }
+  }
+}
+
 // ─────────────────────────── exports ───────────────────────────────────
 // Expand packed (rows, nv, 21) to the reference's (rows, nv*36).
 __global__ void k_expand36(const double* __restrict__ in, int64_t blocks, double* __restrict__ out) {
@@ -1024,6 +1248,33 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
       k_gp_trace<false><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns,
                                                            model->zs, d_mask, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
+  } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32))) {
+    // tensor-pipe path, FP16 split (mma.sync m16n8k16): a warp covers 80 samples of one voxel
+    const int wpv = (ns + 16 * GC_MT - 1) / (16 * GC_MT);
+    FIF_CHECK_ARG(wpv >= 1 && wpv <= GC_WARPS, "fif_build: N_s=%d too large for k_gp_info_h16", ns);
+    const int vpc = GC_WARPS / wpv;
+    const unsigned blocks_c = (unsigned)((rows + vpc - 1) / vpc);
+    size_t smem = sizeof(float) * (vpc * GC_TILE * 24) + sizeof(float4) * (vpc * GC_TILE + GC_TILE * 2) +
+                  sizeof(float) * 6 * GC_WARPS + sizeof(int) * 2 * GC_WARPS +
+                  sizeof(double) * GC_WARPS * GC_MT * GC_NT * 4 * 32;
+    static bool carve_h = false;
+    if (!carve_h) {
+      for (auto f : {k_gp_info_h16<true, true>, k_gp_info_h16<false, true>, k_gp_info_h16<true, false>,
+                     k_gp_info_h16<false, false>}) {
+        cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      }
+      carve_h = true;
+    }
+    const bool dead_top = wpv == 1 && (GC_MT - 1) * 16 + 8 >= ns;
+#define GH_LAUNCH(M, D)                                                                                        \
+  k_gp_info_h16<M, D><<<blocks_c, GC_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv, \
+                                                            model->zs, d_mask, (float)inv_s2, (float)ax, (float)bx, \
+                                                            d_out64, d_out32)
+    if (has_mask) { if (dead_top) GH_LAUNCH(true, true); else GH_LAUNCH(true, false); }
+    else { if (dead_top) GH_LAUNCH(false, true); else GH_LAUNCH(false, false); }
+#undef GH_LAUNCH
+    FIF_CHECK_LAUNCH("k_gp_info_h16");
   } else if (!(build_flags & FIF_BUILD_SIMT)) {
     // tensor-pipe path (mma.sync TF32x3): a warp covers 80 samples of one voxel
     const int wpv = (ns + 16 * GC_MT - 1) / (16 * GC_MT);

@@ -258,9 +258,10 @@ class _DeviceModel:
 # pairs at a time (one byte each), bounding device memory for large maps
 _MASK_CHUNK_BYTES = 1 << 30
 
-# GP info builds run on the tensor pipe (mma.sync TF32x3) unless this is set; the FP32
-# SIMT kernel is kept as a cross-check and for models the tensor kernel does not cover.
-GP_INFO_SIMT = False
+# GP info kernel: "h16" (default; mma.sync FP16 split, k16 per MMA), "tf32" (mma.sync
+# TF32x3) or "simt" (FP32 FFMA2); the alternatives are kept as cross-checks.
+GP_INFO_KERNEL = "h16"
+_GP_INFO_FLAGS = {"h16": 0, "tf32": _lib.BUILD_TF32, "simt": _lib.BUILD_SIMT}
 
 
 def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, device: torch.device, grid=None,
@@ -283,7 +284,7 @@ def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, devi
     g = _lib.make_grid(grid.origin, grid.voxel_size, grid.dims) if grid is not None else None
     kind = _lib.KIND_TRACE if want_trace else _lib.KIND_INFO
     st = _lib.load().fif_build(kind, dm.c, _lib.ptr(points), n, g, _lib.ptr(centers), v_begin, v_end, _lib.ptr(mask),
-                               float(sigma), (_lib.BUILD_EXACT if exact else 0) | (_lib.BUILD_SIMT if GP_INFO_SIMT else 0),
+                               float(sigma), (_lib.BUILD_EXACT if exact else 0) | _GP_INFO_FLAGS[GP_INFO_KERNEL],
                                _lib.ptr(scratch), _lib.ptr(out64),
                                _lib.ptr(out32), _device.stream_handle(device))
     _lib.check(st, "fif_build")

@@ -40,10 +40,10 @@ def test_centers_bit_exact(oracle, small_grid, order):
     assert np.array_equal(out.cpu().numpy(), ref)
 
 
-@pytest.fixture(params=["tensor", "simt"])
+@pytest.fixture(params=["h16", "tf32", "simt"])
 def gp_info_kernel(request, monkeypatch):
-    """Both GP-info kernels (mma.sync TF32x3 default, FP32 FFMA2 SIMT) must meet parity."""
-    monkeypatch.setattr(FD, "GP_INFO_SIMT", request.param == "simt")
+    """Every GP-info kernel (mma.sync FP16-split default, TF32x3, FP32 FFMA2 SIMT) must meet parity."""
+    monkeypatch.setattr(FD, "GP_INFO_KERNEL", request.param)
     return request.param
 
 
