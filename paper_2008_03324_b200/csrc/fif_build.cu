@@ -15,6 +15,7 @@
 // because the kinv epilogue amplifies S errors ~200x.
 #include <cstdarg>
 #include <mutex>
+#include <type_traits>
 
 #include <cuda_fp16.h>
 
@@ -1025,8 +1026,11 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       uint32_t ah[GC_MT][4], al[GC_MT][4];
 #pragma unroll
       for (int m = 0; m < GC_MT; ++m) afrag_m(0, m, ah[m], al[m]);
-#pragma unroll 1
-      for (int k0 = 0; k0 < GC_TILE; k0 += 16) {
+      // one k16 step; NEXT: the following step's sigmoids are evaluated between the MMA
+      // passes (the tile's last step has no successor: its passes run back to back, so
+      // no sigmoid is computed twice)
+      auto kstep = [&](int k0, auto next_tag) {
+        constexpr bool NEXT = decltype(next_tag)::value;
         // B fragment (f16): reg0 (k 2tig..+1, col gid), reg1 (k 2tig+8..+9, col gid)
         uint32_t bh[GC_NT][2], bl[GC_NT][2];
 #pragma unroll
@@ -1035,33 +1039,42 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
           h16_split2(eb[(k0 + 2 * tig) * 24] * s_cur, eb[(k0 + 2 * tig + 1) * 24] * s_cur, bh[n][0], bl[n][0]);
           h16_split2(eb[(k0 + 2 * tig + 8) * 24] * s_cur, eb[(k0 + 2 * tig + 9) * 24] * s_cur, bh[n][1], bl[n][1]);
         }
-        const int kn = (k0 + 16) & (GC_TILE - 1);  // next step (wraps harmlessly on the last)
+        const int kn = k0 + 16;
         uint32_t nh[GC_MT][4], nl[GC_MT][4];
 #pragma unroll
         for (int m = 0; m < GC_MT; ++m)
 #pragma unroll
           for (int n = 0; n < GC_NT; ++n) mma_f16(c[m][n], ah[m], bh[n][0], bh[n][1]);
-        afrag_m(kn, 0, nh[0], nl[0]);
-        afrag_m(kn, 1, nh[1], nl[1]);
+        if (NEXT) {
+          afrag_m(kn, 0, nh[0], nl[0]);
+          afrag_m(kn, 1, nh[1], nl[1]);
+        }
 #pragma unroll
         for (int m = 0; m < GC_MT; ++m)
 #pragma unroll
           for (int n = 0; n < GC_NT; ++n) mma_f16(c[m][n], ah[m], bl[n][0], bl[n][1]);
-        afrag_m(kn, 2, nh[2], nl[2]);
-        afrag_m(kn, 3, nh[3], nl[3]);
+        if (NEXT) {
+          afrag_m(kn, 2, nh[2], nl[2]);
+          afrag_m(kn, 3, nh[3], nl[3]);
+        }
 #pragma unroll
         for (int m = 0; m < GC_MT; ++m)
 #pragma unroll
           for (int n = 0; n < GC_NT; ++n) mma_f16(c[m][n], al[m], bh[n][0], bh[n][1]);
-        afrag_m(kn, 4, nh[4], nl[4]);
+        if (NEXT) {
+          afrag_m(kn, 4, nh[4], nl[4]);
 #pragma unroll
-        for (int m = 0; m < GC_MT; ++m)
+          for (int m = 0; m < GC_MT; ++m)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            ah[m][i] = nh[m][i];
-            al[m][i] = nl[m][i];
-          }
-      }
+            for (int i = 0; i < 4; ++i) {
+              ah[m][i] = nh[m][i];
+              al[m][i] = nl[m][i];
+            }
+        }
+      };
+#pragma unroll 1
+      for (int k0 = 0; k0 < GC_TILE - 16; k0 += 16) kstep(k0, std::true_type{});
+      kstep(GC_TILE - 16, std::false_type{});
       if (++tiles == GC_FLUSH_TILES || base + GC_TILE >= n_pad) {
         tiles = 0;
         const double unscale = 0x1p-12 / (double)s_cur;  // exact power of two
