@@ -274,7 +274,7 @@ def run_ours(args, rank, world, local):
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get("k_gp_info", {}).get("dram_bytes_per_launch")
+        traffic = prof.get("k_gp_info_h16", {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
     line = {
@@ -293,7 +293,7 @@ def run_ours(args, rank, world, local):
                 "path": "host float64 landmarks (pinned) -> H2D -> fif_build -> D2H checksum"},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": traffic,
-                     "kernel": "k_gp_info", "flops_per_pair": GP_INFO_FLOPS_PER_PAIR(model.n_v),
+                     "kernel": "k_gp_info_h16", "flops_per_pair": GP_INFO_FLOPS_PER_PAIR(model.n_v),
                      "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
                      "mufu_frac": (rows * N * GP_INFO_MUFU_PER_PAIR(model.n_v)) / (k_ms / 1e3)
                                   / (sms * 16 * max_mhz * 1e6)},
@@ -338,6 +338,12 @@ def secondary(args, F, FD, SC, w2, grid, model, dm, pts, dev, stream, flush, wor
         b.synchronize()
         times.append(a.elapsed_time(b))
     qms = float(np.mean(times))
+    q_traffic = None
+    try:  # ncu dram bytes of k_query_prep_gp + k_query_info per query (profiles/ncu_summary.json)
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        q_traffic = prof["query_per_query"]["dram_bytes"]
+    except (OSError, ValueError, KeyError):
+        pass
     nq = q1 - q0
     row = QUERY_ROW_BYTES_GP_INFO(model.n_v)
     bytes_q = 8 * row + 48 + 8 * (1 + 6 + 36 + 216)  # 8 corner rows + pose in + outputs
@@ -346,7 +352,7 @@ def secondary(args, F, FD, SC, w2, grid, model, dm, pts, dev, stream, flush, wor
         "workload": "config2: 100000 poses, trilinear, full 6x6 + trace + analytic d/d[t;theta], GP-70 info field",
         "value": nq * world / (qms / 1e3), "unit": "queries/s", "ms": qms,
         "roofline": {"bound": "hbm", "achieved": nq * bytes_q / (qms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-                     "frac": nq * bytes_q / (qms / 1e3) / 1e9 / hbm, "traffic": None,
+                     "frac": nq * bytes_q / (qms / 1e3) / 1e9 / hbm, "traffic": q_traffic,
                      "bytes_per_query": bytes_q},
     }
     # point cloud (config 3): poses sharded across ranks

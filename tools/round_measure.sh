@@ -14,7 +14,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 python tools/prof_build.py --kind trace > $O/trace_build.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:k_gp_trace -c 1 -o $O/full_k_gp_trace -f \
       python tools/prof_build.py --kind trace --reps 1 > $O/ncu_full_k_gp_trace.log 2>&1
-for k in k_gp_info_tc k_query_info k_pc_fim k_query_prep; do
+for k in k_gp_info_h16 k_query_info k_pc_fim k_query_prep_gp; do
   ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o $O/full_$k -f \
       python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_full_$k.log 2>&1
 done
+python tools/ncu_json.py $O > $O/ncu_json.log 2>&1
