@@ -177,10 +177,18 @@ def run_ours(args, rank, world, local):
     from paper_2008_03324_b200 import field as FD
     from paper_2008_03324_b200.parallel import slab_range
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # FIF_BENCH_BACKEND=gloo with more ranks than GPUs only exercises the multi-rank code
+    # path (ranks share a device; their kernels never wait on each other); numbers from
+    # such a run are not measurements
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("FIF_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     w2 = SC.config2(100000)
     grid = F.GridConfig(*w2.grid)
     V, N = grid.voxel_count, w2.points.shape[0]
@@ -210,7 +218,7 @@ def run_ours(args, rank, world, local):
         step()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local % ndev) as clocks:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()

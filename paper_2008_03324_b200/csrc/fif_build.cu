@@ -338,13 +338,16 @@ constexpr int GT_TILE = 64;
 constexpr int GT_FLUSH = 8;
 constexpr int GT_G = 4;
 constexpr int GT_THREADS = 256;
+#ifndef GT_MINB
+#define GT_MINB 2
+#endif
 struct __align__(16) PairT {
   double ux, uy, uz;
   float tr, pad;
 };
 
 template <bool HAS_MASK>
-__global__ void __launch_bounds__(GT_THREADS) k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSrc src,
+__global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSrc src,
                                                          int64_t v0, int64_t v1, int vb, int ns,
                                                          const double* __restrict__ zs, const uint8_t* __restrict__ mask,
                                                          double inv_s2, double ax, double bx,
