@@ -339,7 +339,7 @@ constexpr int GT_FLUSH = 8;
 constexpr int GT_G = 4;
 constexpr int GT_THREADS = 256;
 #ifndef GT_MINB
-#define GT_MINB 2
+#define GT_MINB 3
 #endif
 struct __align__(16) PairT {
   double ux, uy, uz;
