@@ -2,7 +2,10 @@
 //
 // Replaces _nb_exact_fim / _nb_exact_fim_batch (kernels.py:571-599, 743-749).
 // One warp per pose, lanes over landmarks; landmark tiles are staged once per
-// CTA in shared memory and shared by its 16 poses.  The visibility test is the
+// CTA in shared memory and shared by its 16 poses.  A producer warp streams the
+// tiles with TMA bulk copies into a PC_NBUF-deep ring (mbarrier full/empty pairs),
+// so pose warps never wait on each other: a warp with many visible landmarks may
+// lag the others by up to PC_NBUF - 1 tiles.  The visibility test is the
 // reference's FP64 arithmetic in its exact operation order (no FMA), with the
 // two IEEE divisions replaced by sign tests on fma residuals wherever the
 // residual is far from zero — the decision is then provably identical — and
@@ -12,8 +15,12 @@
 
 namespace fif {
 
-constexpr int PC_WARPS = 16;
-constexpr int PC_TILE = 2048;
+constexpr int PC_WARPS = 15;  // pose warps; + 1 producer warp = 4 warps per SM sub-partition
+#ifndef PC_TILE_N
+#define PC_TILE_N 1024
+#endif
+constexpr int PC_TILE = PC_TILE_N;
+constexpr int PC_NBUF = 4096 / PC_TILE;  // 128 KB ring (hi + lo)
 constexpr int PC_QCAP = 64;
 
 struct PoseR {
@@ -89,7 +96,7 @@ __device__ __forceinline__ void fim21(float dx, float dy, float dz, float px, fl
 __constant__ int kPR[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
 __constant__ int kPC[21] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5};
 
-// Landmark table for the FP32 pre-test: p = hi + lo (float4 {hi.xyz, 0}, {lo.xyz, 0}).
+// Landmark tables: hi[i] = {p_hi.xyz, |p_hi|_1}, lo[i] = {p_lo.xyz, 0}, p = p_hi + p_lo.
 __global__ void k_pc_prep(const double* __restrict__ pts, int64_t n, float4* __restrict__ tab) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -97,99 +104,142 @@ __global__ void k_pc_prep(const double* __restrict__ pts, int64_t n, float4* __r
   split_f32(pts[3 * i], hx, lx);
   split_f32(pts[3 * i + 1], hy, ly);
   split_f32(pts[3 * i + 2], hz, lz);
-  tab[2 * i] = make_float4(hx, hy, hz, 0.f);
-  tab[2 * i + 1] = make_float4(lx, ly, lz, 0.f);
+  tab[i] = make_float4(hx, hy, hz, fabsf(hx) + fabsf(hy) + fabsf(hz));
+  tab[n + i] = make_float4(lx, ly, lz, 0.f);
 }
 
-// FP32 pre-test with rigorous margins, branch-free: returns +1 (certainly visible
-// under the reference's FP64 test), -1 (certainly invisible) or 0 (within the error
-// band of z = 0 or of an image border: decide with the exact FP64 test).
-// d = p - t is exact to ~1 ulp of |d| (hi/lo parts); every FP32 rounding below is
-// bounded by a few ulp of |f| |d|_1, and the margins are 8-16 ulp of that.
-struct PoseF {
-  float r00, r01, r02, r10, r11, r12, r20, r21, r22, thx, thy, thz, tlx, tly, tlz;
+// FP32 pre-test with rigorous margins, branch-free.  Every quantity the reference
+// compares is an affine function of the landmark position p for a fixed pose:
+//   zc = R2 . (p - t),  b0 = zc (u - 0) = (fx R0 + cx R2) . (p - t),  b1 = zc (u - W),
+//   c0 = zc (v - 0),    c1 = zc (v - H)                 (u, v the pixel coordinates)
+// so each is one 3-FMA dot product w_k . p_hi + C_k with per-pose FP32 coefficients
+// (formed in FP64).  The FP32 evaluation differs from the exact value by at most
+// ~6 u W_k (|p|_1 + |t|_1) (u = 2^-24, W_k = max |w_k|: coefficient and constant
+// rounding, p_lo dropped, three FMA roundings), and the reference's FP64 decision by
+// far less, so outside the margin 16 u W_k (|p|_1 + |t|_1) the sign — hence the
+// reference's decision — is certain.  Returns +1 certainly visible, -1 certainly not,
+// 0 within a margin: run the reference's exact FP64 test.
+struct PoseAff {
+  float w[5][3], c[5], mg[5], m0[5];  // rows: zc, b0, b1, c0, c1; margin = mg |p|_1 + m0
 };
-struct CamF {
-  float fx, fy, cx, cy, cxw, cyh, mz, mu, mv;
-};
-__device__ __forceinline__ int pc_pretest(const PoseF& P, float4 ph, float4 pl, const CamF& C, float& dx, float& dy,
-                                          float& dz) {
-  dx = (ph.x - P.thx) + (pl.x - P.tlx);
-  dy = (ph.y - P.thy) + (pl.y - P.tly);
-  dz = (ph.z - P.thz) + (pl.z - P.tlz);
-  const float l1 = fabsf(dx) + fabsf(dy) + fabsf(dz);
-  const float zc = fmaf(P.r02, dx, fmaf(P.r12, dy, P.r22 * dz));
-  const float xc = fmaf(P.r00, dx, fmaf(P.r10, dy, P.r20 * dz));
-  const float yc = fmaf(P.r01, dx, fmaf(P.r11, dy, P.r21 * dz));
-  const float a = C.fx * xc, b = C.fy * yc;
-  const float b0 = fmaf(C.cx, zc, a), b1 = fmaf(C.cxw, zc, a);
-  const float c0 = fmaf(C.cy, zc, b), c1 = fmaf(C.cyh, zc, b);
-  const float mz = C.mz * l1, m1 = C.mu * l1, m2 = C.mv * l1;
-  const bool zpos = zc > mz, zneg = zc < -mz;
-  const bool out = (b0 < -m1) | (b1 > m1) | (c0 < -m2) | (c1 > m2);
-  const bool in = (b0 > m1) & (b1 < -m1) & (c0 > m2) & (c1 < -m2);
+__device__ __forceinline__ int pc_pretest(const PoseAff& A, float4 ph) {
+  float v[5], m[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    v[k] = fmaf(A.w[k][0], ph.x, fmaf(A.w[k][1], ph.y, fmaf(A.w[k][2], ph.z, A.c[k])));
+    m[k] = fmaf(A.mg[k], ph.w, A.m0[k]);
+  }
+  const bool zpos = v[0] > m[0], zneg = v[0] < -m[0];
+  const bool out = (v[1] < -m[1]) | (v[2] > m[2]) | (v[3] < -m[3]) | (v[4] > m[4]);
+  const bool in = (v[1] > m[1]) & (v[2] < -m[2]) & (v[3] > m[3]) & (v[4] < -m[4]);
   return (zpos & in) ? 1 : ((zneg | (zpos & out)) ? -1 : 0);
 }
 
 template <bool MASK>
-__global__ void __launch_bounds__(PC_WARPS * 32) k_pc_fim(const double* __restrict__ rot, const double* __restrict__ tr,
+__global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double* __restrict__ rot, const double* __restrict__ tr,
                                                           int64_t nq, const double* __restrict__ pts,
                                                           const float4* __restrict__ ptab, int64_t n, fif_camera cam,
                                                           float inv_s2, double* __restrict__ out,
                                                           uint8_t* __restrict__ mask) {
   extern __shared__ float4 pcsm[];
-  float4 (*tile)[PC_TILE] = reinterpret_cast<float4 (*)[PC_TILE]>(pcsm);                     // [2][PC_TILE]
-  float4 (*queue)[PC_QCAP][2] = reinterpret_cast<float4 (*)[PC_QCAP][2]>(pcsm + 2 * PC_TILE);  // [warps][cap][2]
+  float4* ring_hi = pcsm;                                  // [PC_NBUF][PC_TILE]
+  float4* ring_lo = pcsm + PC_NBUF * PC_TILE;              // [PC_NBUF][PC_TILE]
+  float4* queues = pcsm + 2 * PC_NBUF * PC_TILE;           // [PC_WARPS][PC_QCAP][2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(queues + PC_WARPS * PC_QCAP * 2);  // [PC_NBUF]
+  uint64_t* empty = full + PC_NBUF;                                                 // [PC_NBUF]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < PC_NBUF; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], PC_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (n + PC_TILE - 1) / PC_TILE;
+  const int64_t qstride = (int64_t)gridDim.x * PC_WARPS;
+  const int64_t npi = blockIdx.x * (int64_t)PC_WARPS < nq ? (nq - blockIdx.x * (int64_t)PC_WARPS + qstride - 1) / qstride : 0;
+  if (warp == PC_WARPS) {  // producer: every tile of every pose group, in consumption order
+    if (lane == 0) {
+      int64_t seq = 0;
+      for (int64_t it = 0; it < npi; ++it)
+        for (int64_t t = 0; t < ntiles; ++t, ++seq) {
+          const int b = (int)(seq % PC_NBUF);
+          mbar_wait(&empty[b], (uint32_t)(((seq / PC_NBUF) & 1) ^ 1));
+          const int64_t base = t * PC_TILE;
+          const uint32_t bytes = (uint32_t)(min((int64_t)PC_TILE, n - base) * sizeof(float4));
+          mbar_expect_tx(&full[b], 2 * bytes);
+          tma_bulk_g2s(ring_hi + b * PC_TILE, ptab + base, bytes, &full[b]);
+          tma_bulk_g2s(ring_lo + b * PC_TILE, ptab + n + base, bytes, &full[b]);
+        }
+    }
+    return;
+  }
+  float4* qd = queues + warp * PC_QCAP * 2;  // (d, p) of queued visible landmarks
   const double cxw = cam.cx - cam.width, cyh = cam.cy - cam.height;
-  // margins: 16 ulp(fp32) x (|f| + |c| + |w|) per unit of |d|_1 (bounds every rounding
-  // of the FP32 evaluation plus the FP64 reference's own roundings)
-  CamF CF;
-  CF.fx = (float)cam.fx; CF.fy = (float)cam.fy; CF.cx = (float)cam.cx; CF.cy = (float)cam.cy;
-  CF.cxw = (float)cxw; CF.cyh = (float)cyh;
-  CF.mz = 8.0f * 5.96e-8f;
-  CF.mu = 16.0f * 5.96e-8f * (float)(fabs(cam.fx) + fabs(cam.cx) + fabs(cam.width));
-  CF.mv = 16.0f * 5.96e-8f * (float)(fabs(cam.fy) + fabs(cam.cy) + fabs(cam.height));
   const unsigned lt_mask = (1u << lane) - 1u;
-  for (int64_t q0 = blockIdx.x * (int64_t)PC_WARPS; q0 < nq; q0 += (int64_t)gridDim.x * PC_WARPS) {
+  int64_t seq = 0;
+  for (int64_t it = 0; it < npi; ++it) {
+    const int64_t q0 = blockIdx.x * (int64_t)PC_WARPS + it * qstride;
     const int64_t q = q0 + warp;
     const bool has_pose = q < nq;
-    PoseR P;
-    PoseF PF;
+    PoseAff A;
+    float thx, thy, thz, tlx, tly, tlz;
     {
       const int64_t qq = has_pose ? q : q0;
       const double* R = rot + 9 * qq;
-      P.r00 = R[0]; P.r01 = R[1]; P.r02 = R[2];
-      P.r10 = R[3]; P.r11 = R[4]; P.r12 = R[5];
-      P.r20 = R[6]; P.r21 = R[7]; P.r22 = R[8];
-      P.tx = tr[3 * qq]; P.ty = tr[3 * qq + 1]; P.tz = tr[3 * qq + 2];
-      PF.r00 = (float)P.r00; PF.r01 = (float)P.r01; PF.r02 = (float)P.r02;
-      PF.r10 = (float)P.r10; PF.r11 = (float)P.r11; PF.r12 = (float)P.r12;
-      PF.r20 = (float)P.r20; PF.r21 = (float)P.r21; PF.r22 = (float)P.r22;
-      split_f32(P.tx, PF.thx, PF.tlx);
-      split_f32(P.ty, PF.thy, PF.tly);
-      split_f32(P.tz, PF.thz, PF.tlz);
+      const double tx = tr[3 * qq], ty = tr[3 * qq + 1], tz = tr[3 * qq + 2];
+      split_f32(tx, thx, tlx);
+      split_f32(ty, thy, tly);
+      split_f32(tz, thz, tlz);
+      // affine rows in FP64: world-frame coefficients of zc, b0, b1, c0, c1
+      const double R0[3] = {R[0], R[3], R[6]}, R1[3] = {R[1], R[4], R[7]}, R2[3] = {R[2], R[5], R[8]};
+      const double lt = fabs(tx) + fabs(ty) + fabs(tz);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        double w[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          w[i] = k == 0 ? R2[i]
+                        : k == 1 ? cam.fx * R0[i] + cam.cx * R2[i]
+                                 : k == 2 ? cam.fx * R0[i] + cxw * R2[i]
+                                          : k == 3 ? cam.fy * R1[i] + cam.cy * R2[i] : cam.fy * R1[i] + cyh * R2[i];
+        const double c = -(w[0] * tx + w[1] * ty + w[2] * tz);
+        const double wm = fmax(fabs(w[0]), fmax(fabs(w[1]), fabs(w[2])));
+#pragma unroll
+        for (int i = 0; i < 3; ++i) A.w[k][i] = (float)w[i];
+        A.c[k] = (float)c;
+        A.mg[k] = (float)(16.0 * 0x1p-24 * wm * 1.0000001);
+        A.m0[k] = (float)(16.0 * 0x1p-24 * (wm * lt + fabs(c)) * 1.0000001);
+      }
     }
     float acc[21];
 #pragma unroll
     for (int e = 0; e < 21; ++e) acc[e] = 0.f;
     int qn = 0;  // queued entries (warp-uniform)
-    for (int64_t base = 0; base < n; base += PC_TILE) {
+    for (int64_t t = 0; t < ntiles; ++t, ++seq) {
+      const int64_t base = t * PC_TILE;
       const int cnt = (int)min((int64_t)PC_TILE, n - base);
-      __syncthreads();
-      for (int j = threadIdx.x; j < cnt * 2; j += blockDim.x) tile[j & 1][j >> 1] = ptab[2 * base + j];
-      __syncthreads();
-      if (!has_pose) continue;
+      const int bsel = (int)(seq % PC_NBUF);
+      const float4* tile_hi = ring_hi + bsel * PC_TILE;
+      const float4* tile_lo = ring_lo + bsel * PC_TILE;
+      mbar_wait(&full[bsel], (uint32_t)((seq / PC_NBUF) & 1));
+      if (!has_pose) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[bsel]);
+        continue;
+      }
       for (int j0 = 0; j0 < cnt; j0 += 32) {
         const int j = j0 + lane;
         bool vis = false;
-        float dx = 0.f, dy = 0.f, dz = 0.f;
         float4 ph = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < cnt) {
-          ph = tile[0][j];
-          const int pre = pc_pretest(PF, ph, tile[1][j], CF, dx, dy, dz);
-          if (pre == 0) {
+          ph = tile_hi[j];
+          const int pre = pc_pretest(A, ph);
+          if (pre == 0) {  // within a margin: the reference's FP64 test (pose re-read: rare path)
             const int64_t i = base + j;
+            const double* R = rot + 9 * q;
+            const PoseR P{R[0], R[1], R[2], R[3], R[4], R[5], R[6], R[7], R[8], tr[3 * q], tr[3 * q + 1], tr[3 * q + 2]};
             vis = pc_visible(P, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], cam, cxw, cyh);
           } else {
             vis = pre > 0;
@@ -198,14 +248,18 @@ __global__ void __launch_bounds__(PC_WARPS * 32) k_pc_fim(const double* __restri
         }
         const unsigned bal = __ballot_sync(0xffffffffu, vis);
         if (vis) {
+          // d = p - t, exact to ~1 ulp of |d| from the hi / lo parts
+          const float4 pl = tile_lo[j];
+          const float dx = (ph.x - thx) + (pl.x - tlx), dy = (ph.y - thy) + (pl.y - tly),
+                      dz = (ph.z - thz) + (pl.z - tlz);
           const int slot = qn + __popc(bal & lt_mask);
-          queue[warp][slot][0] = make_float4(dx, dy, dz, 0.f);
-          queue[warp][slot][1] = ph;
+          qd[2 * slot] = make_float4(dx, dy, dz, 0.f);
+          qd[2 * slot + 1] = ph;
         }
         qn += __popc(bal);
         if (qn >= 32) {
           __syncwarp();
-          const float4 d = queue[warp][lane][0], p = queue[warp][lane][1];
+          const float4 d = qd[2 * lane], p = qd[2 * lane + 1];
           float e[21];
           fim21(d.x, d.y, d.z, p.x, p.y, p.z, inv_s2, e);
 #pragma unroll
@@ -213,17 +267,19 @@ __global__ void __launch_bounds__(PC_WARPS * 32) k_pc_fim(const double* __restri
           __syncwarp();
           qn -= 32;
           if (lane < qn) {  // move the overflow to the front
-            queue[warp][lane][0] = queue[warp][32 + lane][0];
-            queue[warp][lane][1] = queue[warp][32 + lane][1];
+            qd[2 * lane] = qd[2 * (32 + lane)];
+            qd[2 * lane + 1] = qd[2 * (32 + lane) + 1];
           }
           __syncwarp();
         }
       }
+      __syncwarp();  // every lane is done reading this tile
+      if (lane == 0) mbar_arrive(&empty[bsel]);
     }
     if (has_pose) {
       __syncwarp();
       if (lane < qn) {
-        const float4 d = queue[warp][lane][0], p = queue[warp][lane][1];
+        const float4 d = qd[2 * lane], p = qd[2 * lane + 1];
         float e[21];
         fim21(d.x, d.y, d.z, p.x, p.y, p.z, inv_s2, e);
 #pragma unroll
@@ -266,17 +322,17 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
   }
   FIF_CHECK_ARG(d_points != nullptr, "fif_pc_fim: NULL points");
   int64_t need = (q + PC_WARPS - 1) / PC_WARPS;
-  int64_t cap = (int64_t)kSMs * 2;
+  int64_t cap = (int64_t)kSMs;  // persistent: one CTA (16 warps, ~190 KB smem) per SM
   unsigned blocks = (unsigned)(need < cap ? need : cap);
   const float inv_s2 = (float)(1.0 / (sigma * sigma));
   float4* ptab = nullptr;
-  if (cudaMallocAsync(&ptab, sizeof(float4) * 2 * n_points, st) != cudaSuccess) {
+  if (cudaMallocAsync(&ptab, sizeof(float4) * 2 * n_points, st) != cudaSuccess) {  // hi[n], lo[n]
     set_error("fif_pc_fim: cudaMallocAsync failed");
     return FIF_ERR_CUDA;
   }
   k_pc_prep<<<(unsigned)((n_points + 255) / 256), 256, 0, st>>>(d_points, n_points, ptab);
   FIF_CHECK_LAUNCH("k_pc_prep");
-  const size_t smem = sizeof(float4) * (2 * PC_TILE + PC_WARPS * PC_QCAP * 2);
+  const size_t smem = sizeof(float4) * (2 * PC_NBUF * PC_TILE + PC_WARPS * PC_QCAP * 2) + 2 * PC_NBUF * sizeof(uint64_t);
   static bool attr = false;
   if (!attr) {
     for (auto f : {k_pc_fim<true>, k_pc_fim<false>}) {
@@ -286,10 +342,10 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
     attr = true;
   }
   if (d_mask)
-    k_pc_fim<true><<<blocks, PC_WARPS * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2, d_out,
+    k_pc_fim<true><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2, d_out,
                                                         d_mask);
   else
-    k_pc_fim<false><<<blocks, PC_WARPS * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2,
+    k_pc_fim<false><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2,
                                                          d_out, d_mask);
   cudaFreeAsync(ptab, st);
   FIF_CHECK_LAUNCH("k_pc_fim");
