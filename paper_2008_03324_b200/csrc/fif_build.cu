@@ -903,20 +903,23 @@ __device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], u
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 constexpr int H16_BEXP = 13;  // |B'| < 2^14
+#ifndef GH_MINB
+#define GH_MINB 3  // 12 warps per SM when the shared memory allows it (N_s <= 70)
+#endif
 
 template <bool HAS_MASK, bool DEAD_TOP>
-__global__ void __launch_bounds__(GC_WARPS * 32, 2)
+__global__ void __launch_bounds__(GC_WARPS * 32, GH_MINB)
 k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1,
               int ns, int wpv, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax,
               float bx, double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int vpc = GC_WARPS / wpv;                                   // voxels per CTA
-  float* eh = reinterpret_cast<float*>(smem_raw);                   // [vpc][GC_TILE][24] entries (FP32)
-  float4* uu = reinterpret_cast<float4*>(eh + vpc * GC_TILE * 24);  // [vpc][GC_TILE] bearings
+  float* eh = reinterpret_cast<float*>(smem_raw);                   // [vpc][GC_TILE][21] entries (FP32)
+  float4* uu = reinterpret_cast<float4*>(eh + ((vpc * GC_TILE * 21 + 3) & ~3));  // [vpc][GC_TILE] bearings
   float4* tile = uu + vpc * GC_TILE;                                // [GC_TILE][2] landmarks
   float* cs = reinterpret_cast<float*>(tile + GC_TILE * 2);         // [vpc][6] centre hi/lo
   int* tmax = reinterpret_cast<int*>(cs + 6 * GC_WARPS);            // [vpc] max |entry| of the tile (bits)
-  double* acc = reinterpret_cast<double*>(tmax + 2 * GC_WARPS);     // [GC_WARPS][GC_MT*GC_NT*4][32]
+  double* acc = reinterpret_cast<double*>(tmax + 2 * GC_WARPS);     // [GC_WARPS][rw][21] FP64 sums (valid rows only)
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int vl = warp / wpv, mg = warp - vl * wpv;
@@ -931,8 +934,10 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       cs[6 * t + 3 + k] = cl[k];
     }
   }
-  double* myacc = acc + (size_t)warp * GC_MT * GC_NT * 4 * 32;
-  for (int i = 0; i < GC_MT * GC_NT * 4; ++i) myacc[i * 32 + lane] = 0.0;
+  const int rw = min(GC_MT * 16, ns);                               // sample rows per warp slot
+  const int g0 = mg * GC_MT * 16;                                   // first sample row of this warp
+  double* myacc = acc + (size_t)warp * rw * 21;
+  for (int i = lane; i < rw * 21; i += 32) myacc[i] = 0.0;
   float zr[GC_MT][2][3];
 #pragma unroll
   for (int m = 0; m < GC_MT; ++m)
@@ -979,10 +984,9 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       if (lane == 0) atomicMax(&tmax[pv], __float_as_int(mx));
-      float4* dh = reinterpret_cast<float4*>(eh + (pv * GC_TILE + pj) * 24);
+      float* dh = eh + (pv * GC_TILE + pj) * 21;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) dh[k] = make_float4(e[4 * k], e[4 * k + 1], e[4 * k + 2], e[4 * k + 3]);
-      dh[5] = make_float4(e[20], 0.f, 0.f, 0.f);
+      for (int k = 0; k < 21; ++k) dh[k] = e[k];
       uu[pv * GC_TILE + pj] = make_float4(q.ux, q.uy, q.uz, 0.f);
     }
     __syncthreads();
@@ -1003,7 +1007,9 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
           s_cur = s_need;
         }
       }
-      const float* ehv = eh + vl * GC_TILE * 24;
+      // entries 21..23 of an n8 tile read the next pair's values: they only feed the
+      // discarded accumulator columns 21..23 (each MMA output column is independent)
+      const float* ehv = eh + vl * GC_TILE * 21;
       const float4* uv = uu + vl * GC_TILE;
       // A fragment (m16n8k16, f16): reg0 (row gid, k 2tig..+1), reg1 (row gid+8, k 2tig..+1),
       // reg2 (row gid, k 2tig+8..+9), reg3 (row gid+8, k 2tig+8..+9); low half = lower k
@@ -1039,8 +1045,8 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
 #pragma unroll
         for (int n = 0; n < GC_NT; ++n) {
           const float* eb = ehv + 8 * n + gid;
-          h16_split2(eb[(k0 + 2 * tig) * 24] * s_cur, eb[(k0 + 2 * tig + 1) * 24] * s_cur, bh[n][0], bl[n][0]);
-          h16_split2(eb[(k0 + 2 * tig + 8) * 24] * s_cur, eb[(k0 + 2 * tig + 9) * 24] * s_cur, bh[n][1], bl[n][1]);
+          h16_split2(eb[(k0 + 2 * tig) * 21] * s_cur, eb[(k0 + 2 * tig + 1) * 21] * s_cur, bh[n][0], bl[n][0]);
+          h16_split2(eb[(k0 + 2 * tig + 8) * 21] * s_cur, eb[(k0 + 2 * tig + 9) * 21] * s_cur, bh[n][1], bl[n][1]);
         }
         const int kn = k0 + 16;
         uint32_t nh[GC_MT][4], nl[GC_MT][4];
@@ -1087,7 +1093,8 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
           for (int n = 0; n < GC_NT; ++n)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              myacc[((m * GC_NT + n) * 4 + i) * 32 + lane] += (double)c[m][n][i] * unscale;
+              const int gl = m * 16 + gid + ((i >> 1) << 3), en = 8 * n + 2 * tig + (i & 1);
+              if (g0 + gl < ns && en < 21) myacc[gl * 21 + en] += (double)c[m][n][i] * unscale;
               c[m][n][i] = 0.f;
             }
         s_cur = 0x1p100f;
@@ -1095,20 +1102,13 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
     }
   }
   if (vl < vpc && myv < v1) {
-    const int64_t r = myv - v0;
-#pragma unroll
-    for (int m = 0; m < GC_MT; ++m)
-#pragma unroll
-      for (int n = 0; n < GC_NT; ++n)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int g = (mg * GC_MT + m) * 16 + gid + ((i >> 1) << 3);
-          const int en = 8 * n + 2 * tig + (i & 1);
-          if (g >= ns || en >= 21) continue;
-          const double v = myacc[((m * GC_NT + n) * 4 + i) * 32 + lane];
-          out64[(r * ns + g) * 21 + en] = v;
-          if (out32) out32[(r * ns + g) * 21 + en] = (float)v;
-        }
+    const int64_t ob = ((myv - v0) * ns + g0) * 21;
+    const int tot = min(GC_MT * 16, ns - g0) * 21;
+    for (int i = lane; i < tot; i += 32) {
+      const double v = myacc[i];
+      out64[ob + i] = v;
+      if (out32) out32[ob + i] = (float)v;
+    }
   }
 }
 
@@ -1270,9 +1270,9 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     FIF_CHECK_ARG(wpv >= 1 && wpv <= GC_WARPS, "fif_build: N_s=%d too large for k_gp_info_h16", ns);
     const int vpc = GC_WARPS / wpv;
     const unsigned blocks_c = (unsigned)((rows + vpc - 1) / vpc);
-    size_t smem = sizeof(float) * (vpc * GC_TILE * 24) + sizeof(float4) * (vpc * GC_TILE + GC_TILE * 2) +
-                  sizeof(float) * 6 * GC_WARPS + sizeof(int) * 2 * GC_WARPS +
-                  sizeof(double) * GC_WARPS * GC_MT * GC_NT * 4 * 32;
+    const int rw = ns < GC_MT * 16 ? ns : GC_MT * 16;
+    size_t smem = sizeof(float) * ((vpc * GC_TILE * 21 + 3) & ~3) + sizeof(float4) * (vpc * GC_TILE + GC_TILE * 2) +
+                  sizeof(float) * 6 * GC_WARPS + sizeof(int) * 2 * GC_WARPS + sizeof(double) * GC_WARPS * rw * 21;
     static bool carve_h = false;
     if (!carve_h) {
       for (auto f : {k_gp_info_h16<true, true>, k_gp_info_h16<false, true>, k_gp_info_h16<true, false>,
