@@ -336,7 +336,10 @@ __global__ void __launch_bounds__(QI_THREADS) k_quad_info(const double4* __restr
 // tr * vs into FP32 partials flushed into double-float accumulators.
 constexpr int GT_TILE = 64;
 constexpr int GT_FLUSH = 8;
-constexpr int GT_G = 4;
+#ifndef GT_G_N
+#define GT_G_N 4
+#endif
+constexpr int GT_G = GT_G_N;
 constexpr int GT_THREADS = 256;
 #ifndef GT_MINB
 #define GT_MINB 3
