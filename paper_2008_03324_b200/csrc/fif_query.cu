@@ -16,6 +16,8 @@
 
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 namespace fif {
 
 
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeo
                                                           const double* __restrict__ pos, const double* __restrict__ axes,
                                                           int64_t nq, int trilinear, uint8_t* __restrict__ status,
                                                           int32_t* __restrict__ rows, double4* __restrict__ cw,
-                                                          double4* __restrict__ wt) {
+                                                          double4* __restrict__ wt, const int32_t* __restrict__ perm) {
   extern __shared__ double sv[];  // [QP_Q][nv] v^r, then zs [nv][3]
   const int nv = m.kind == FIF_MODEL_QUAD ? 10 : m.n_v;
   const int64_t q0 = blockIdx.x * (int64_t)QP_Q;
@@ -277,7 +279,8 @@ __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeo
     int nc = 0;
     int64_t r[8];
     double w[8], dw[8][3];
-    const int st = locate(gm, slots, pos[3 * q], pos[3 * q + 1], pos[3 * q + 2], trilinear != 0, nc, r, w, dw);
+    const int64_t qo = perm ? (int64_t)perm[q] : q;  // slot q holds query qo (locality order)
+    const int st = locate(gm, slots, pos[3 * qo], pos[3 * qo + 1], pos[3 * qo + 2], trilinear != 0, nc, r, w, dw);
     status[q] = (uint8_t)st;
     for (int c = 0; c < 8; ++c) {
       const bool ok = st == FIF_STATUS_OK && c < nc;
@@ -290,7 +293,8 @@ __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeo
       const int qi = idx / 10, k = idx - qi * 10;
       const int64_t q = q0 + qi;
       if (q >= nq) continue;
-      const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+      const int64_t qo = perm ? (int64_t)perm[q] : q;
+      const double zx = axes[3 * qo], zy = axes[3 * qo + 1], zz = axes[3 * qo + 2];
       const double k2 = m.k2, k1 = m.k1, k0 = m.k0, t2 = 2.0 * k2;
       double v = 0, gx = 0, gy = 0, gz = 0;
       switch (k) {
@@ -320,8 +324,9 @@ __global__ void __launch_bounds__(QP_THREADS) k_query_prep(fif_model m, QueryGeo
       sv[idx] = 0.0;
       continue;
     }
-    const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * q], m.zs[3 * g]), __dmul_rn(axes[3 * q + 1], m.zs[3 * g + 1])),
-                               __dmul_rn(axes[3 * q + 2], m.zs[3 * g + 2]));
+    const int64_t qo = perm ? (int64_t)perm[q] : q;
+    const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * qo], m.zs[3 * g]), __dmul_rn(axes[3 * qo + 1], m.zs[3 * g + 1])),
+                               __dmul_rn(axes[3 * qo + 2], m.zs[3 * g + 2]));
     sv[idx] = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
   }
   __syncthreads();
@@ -376,7 +381,8 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
                                                               const double* __restrict__ axes, int64_t nq,
                                                               int trilinear, uint8_t* __restrict__ status,
                                                               int32_t* __restrict__ rows, double4* __restrict__ cw,
-                                                              double* __restrict__ wt) {
+                                                              double* __restrict__ wt,
+                                                              const int32_t* __restrict__ perm) {
   extern __shared__ double smd[];
   constexpr int NP8 = 8 * NT, KS = NP8 / 4;
   constexpr int MT_PER_WARP = QD_Q / 2 / (QD_THREADS / 32);
@@ -391,7 +397,8 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
     int nc = 0;
     int64_t r[8];
     double w[8], dw[8][3];
-    const int st = locate(gm, slots, pos[3 * q], pos[3 * q + 1], pos[3 * q + 2], trilinear != 0, nc, r, w, dw);
+    const int64_t qo = perm ? (int64_t)perm[q] : q;  // slot q holds query qo (locality order)
+    const int st = locate(gm, slots, pos[3 * qo], pos[3 * qo + 1], pos[3 * qo + 2], trilinear != 0, nc, r, w, dw);
     status[q] = (uint8_t)st;
     for (int c = 0; c < 8; ++c) {
       const bool ok = st == FIF_STATUS_OK && c < nc;
@@ -417,8 +424,9 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
     const int64_t q = q0 + qi;
     double v = 0.0;
     if (q < nq && g < nv) {
-      const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * q], m.zs[3 * g]), __dmul_rn(axes[3 * q + 1], m.zs[3 * g + 1])),
-                                 __dmul_rn(axes[3 * q + 2], m.zs[3 * g + 2]));
+      const int64_t qo = perm ? (int64_t)perm[q] : q;
+      const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * qo], m.zs[3 * g]), __dmul_rn(axes[3 * qo + 1], m.zs[3 * g + 1])),
+                                 __dmul_rn(axes[3 * qo + 2], m.zs[3 * g + 2]));
       v = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
     }
     sv[idx] = v;
@@ -468,11 +476,11 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
 template <int NT>
 static void launch_prep_gp(size_t smem, int64_t q, cudaStream_t st, const fif_model& m, const QueryGeom& gm,
                            const int32_t* slots, const double* pos, const double* axes, int trilinear,
-                           uint8_t* status, int32_t* rows, double4* cw, double* wt) {
+                           uint8_t* status, int32_t* rows, double4* cw, double* wt, const int32_t* perm) {
   auto kern = k_query_prep_gp<NT>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<(unsigned)((q + QD_Q - 1) / QD_Q), QD_THREADS, smem, st>>>(m, gm, slots, pos, axes, q, trilinear, status,
-                                                                     rows, cw, wt);
+                                                                     rows, cw, wt, perm);
 }
 
 // ───────────────────────── contraction: info fields ─────────────────────
@@ -512,7 +520,8 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
                                                              const uint8_t* __restrict__ status,
                                                              const int32_t* __restrict__ rows,
                                                              const double4* __restrict__ cw,
-                                                             const double4* __restrict__ wt, QueryOut out) {
+                                                             const double4* __restrict__ wt, QueryOut out,
+                                                             const int32_t* __restrict__ perm) {
   using SH = QWShape<T>;
   constexpr int KC = SH::KC;
   constexpr uint32_t CAP = SH::CAP;
@@ -587,7 +596,8 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
   int cb = 0;
   uint32_t cphase = 0;
   for (int64_t i = 0; i < nmine; ++i) {
-    const int64_t q = qof(i);
+    const int64_t q = qof(i);                                // slot (locality order)
+    const int64_t qo = perm ? (int64_t)perm[q] : q;         // caller's query index
     const int st = c_st;
     int32_t r[NC];
     double w[NC], G[NC];
@@ -669,17 +679,17 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
     }
     // ── query complete: outputs ──
     if (st != FIF_STATUS_OK) {
-      if (out.fim) for (int i2 = lane; i2 < 36; i2 += 32) out.fim[q * 36 + i2] = 0.0;
-      if (out.fim_grad) for (int i2 = lane; i2 < 216; i2 += 32) out.fim_grad[q * 216 + i2] = 0.0;
+      if (out.fim) for (int i2 = lane; i2 < 36; i2 += 32) out.fim[qo * 36 + i2] = 0.0;
+      if (out.fim_grad) for (int i2 = lane; i2 < 216; i2 += 32) out.fim_grad[qo * 216 + i2] = 0.0;
       if (lane == 0) {
-        if (out.trace) out.trace[q] = 0.0;
-        if (out.det) out.det[q] = 0.0;
-        if (out.lmin) out.lmin[q] = 0.0;
+        if (out.trace) out.trace[qo] = 0.0;
+        if (out.det) out.det[qo] = 0.0;
+        if (out.lmin) out.lmin[qo] = 0.0;
       }
-      if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
-      if (out.det_grad && lane < 6) out.det_grad[q * 6 + lane] = 0.0;
-      if (out.lmin_grad && lane < 6) out.lmin_grad[q * 6 + lane] = 0.0;
-      if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+      if (out.trace_grad && lane < 6) out.trace_grad[qo * 6 + lane] = 0.0;
+      if (out.det_grad && lane < 6) out.det_grad[qo * 6 + lane] = 0.0;
+      if (out.lmin_grad && lane < 6) out.lmin_grad[qo * 6 + lane] = 0.0;
+      if (out.status && lane == 0) out.status[qo] = (uint8_t)st;
       continue;
     }
     if (MGRAD) {
@@ -706,32 +716,32 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
       }
       if (METRIC && on) cfim[c * CF + lane] = G[c];
     }
-    const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+    const double zx = axes[3 * qo], zy = axes[3 * qo + 1], zz = axes[3 * qo + 2];
     const double tgx = zy * R2 - zz * R1, tgy = zz * R0 - zx * R2, tgz = zx * R1 - zy * R0;  // z x d/dz
     if (out.fim && on) {
       const int pr = kPackR[lane], pc = kPackC[lane];
-      out.fim[q * 36 + pr * 6 + pc] = val;
-      out.fim[q * 36 + pc * 6 + pr] = val;
+      out.fim[qo * 36 + pr * 6 + pc] = val;
+      out.fim[qo * 36 + pc * 6 + pr] = val;
     }
     if (GRAD && out.fim_grad && on) {
       const int pr = kPackR[lane], pc = kPackC[lane];
       const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
 #pragma unroll
       for (int d = 0; d < 6; ++d) {
-        out.fim_grad[q * 216 + d * 36 + pr * 6 + pc] = g6[d];
-        out.fim_grad[q * 216 + d * 36 + pc * 6 + pr] = g6[d];
+        out.fim_grad[qo * 216 + d * 36 + pr * 6 + pc] = g6[d];
+        out.fim_grad[qo * 216 + d * 36 + pc * 6 + pr] = g6[d];
       }
     }
     if (out.trace || (GRAD && out.trace_grad)) {
       const bool dg = on && kIsDiag[lane];
       const double tv = warp_sum(dg ? val : 0.0);
-      if (out.trace && lane == 0) out.trace[q] = tv;
+      if (out.trace && lane == 0) out.trace[qo] = tv;
       if (GRAD && out.trace_grad) {
         const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
 #pragma unroll
         for (int d = 0; d < 6; ++d) {
           const double sgl = warp_sum(dg ? g6[d] : 0.0);
-          if (lane == d) out.trace_grad[q * 6 + d] = sgl;
+          if (lane == d) out.trace_grad[qo * 6 + d] = sgl;
         }
       }
     }
@@ -793,8 +803,8 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
         }
       }
       if (lane == 0) {
-        if (out.det) out.det[q] = mdet;
-        if (out.lmin) out.lmin[q] = mlmin;
+        if (out.det) out.det[qo] = mdet;
+        if (out.lmin) out.lmin[qo] = mlmin;
       }
       if (MGRAD) {
         // lane c < NC holds its corner's (w, dw) in my_cw; other lanes hold zeros
@@ -802,13 +812,13 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
           const double tx = warp_sum(my_cw.y * val_c), ty = warp_sum(my_cw.z * val_c), tz = warp_sum(my_cw.w * val_c);
           const double zxg = warp_sum(my_cw.x * gz[0]), zyg = warp_sum(my_cw.x * gz[1]), zzg = warp_sum(my_cw.x * gz[2]);
           const double g6[6] = {tx, ty, tz, zy * zzg - zz * zyg, zz * zxg - zx * zzg, zx * zyg - zy * zxg};
-          if (lane < 6) dst[q * 6 + lane] = g6[lane];
+          if (lane < 6) dst[qo * 6 + lane] = g6[lane];
         };
         if (out.det_grad) blend_grad(mv_det, gd, out.det_grad);
         if (out.lmin_grad) blend_grad(mv_lmin, gl, out.lmin_grad);
       }
     }
-    if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+    if (out.status && lane == 0) out.status[qo] = (uint8_t)st;
   }
 }
 
@@ -821,14 +831,16 @@ __global__ void __launch_bounds__(QC_WARPS * 32) k_query_trace(int nv, const T* 
                                                               const uint8_t* __restrict__ status,
                                                               const int32_t* __restrict__ rows,
                                                               const double4* __restrict__ cw,
-                                                              const double4* __restrict__ wt, QueryOut out) {
+                                                              const double4* __restrict__ wt, QueryOut out,
+                                                              const int32_t* __restrict__ perm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t q = blockIdx.x * (int64_t)QC_WARPS + warp; q < nq; q += (int64_t)gridDim.x * QC_WARPS) {
     const int st = status[q];
+    const int64_t qo = perm ? (int64_t)perm[q] : q;  // q: slot (locality order)
     if (st != FIF_STATUS_OK) {
-      if (lane == 0 && out.trace) out.trace[q] = 0.0;
-      if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
-      if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+      if (lane == 0 && out.trace) out.trace[qo] = 0.0;
+      if (out.trace_grad && lane < 6) out.trace_grad[qo * 6 + lane] = 0.0;
+      if (out.status && lane == 0) out.status[qo] = (uint8_t)st;
       continue;
     }
     const double4* wq = wt + q * nv;
@@ -871,16 +883,16 @@ __global__ void __launch_bounds__(QC_WARPS * 32) k_query_trace(int nv, const T* 
         pgz = fma(d.w, g, pgz);
       }
     }
-    if (lane == 0 && out.trace) out.trace[q] = val;
+    if (lane == 0 && out.trace) out.trace[qo] = val;
     if (GRAD && out.trace_grad) {
       R0 = warp_sum(R0);
       R1 = warp_sum(R1);
       R2 = warp_sum(R2);
-      const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+      const double zx = axes[3 * qo], zy = axes[3 * qo + 1], zz = axes[3 * qo + 2];
       const double g6[6] = {pgx, pgy, pgz, zy * R2 - zz * R1, zz * R0 - zx * R2, zx * R1 - zy * R0};
-      if (lane < 6) out.trace_grad[q * 6 + lane] = g6[lane];
+      if (lane < 6) out.trace_grad[qo * 6 + lane] = g6[lane];
     }
-    if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+    if (out.status && lane == 0) out.status[qo] = (uint8_t)st;
   }
 }
 
@@ -890,9 +902,37 @@ static unsigned query_blocks(int64_t q) {
   return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
 
+// Locality order for large batches: queries are processed in Morton order of their
+// base voxel (3 x 10 bits), so queries sharing corner rows run close in time and the
+// rows are re-read from L2 rather than HBM; results go back to the caller's order.
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+  v &= 1023u;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+__global__ void k_query_keys(QueryGeom gm, const double* __restrict__ pos, int64_t nq, uint32_t* __restrict__ keys,
+                             int32_t* __restrict__ idx) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double inv = 1.0 / gm.vs;
+  auto cell = [&](double x, double o, int64_t n) -> uint32_t {
+    double g = floor((x - o) * inv);
+    g = fmin(fmax(g, 0.0), (double)(n - 1));
+    return (uint32_t)((int64_t)g >> (n > 1024 ? 1 : 0));  // 10 bits per axis (coarsened for huge grids)
+  };
+  const uint32_t ix = cell(pos[3 * q], gm.ox, gm.nx), iy = cell(pos[3 * q + 1], gm.oy, gm.ny),
+                 iz = cell(pos[3 * q + 2], gm.oz, gm.nz);
+  keys[q] = (spread10(iz) << 2) | (spread10(iy) << 1) | spread10(ix);
+  idx[q] = (int32_t)q;
+}
+
 template <typename T, int NC, int STAGES, bool GRAD, bool METRIC, bool MGRAD>
 static void launch_info(int nv, const T* f, const double* axes, int64_t q, const uint8_t* status, const int32_t* rows,
-                        const double4* cw, const double4* wt, const QueryOut& out, cudaStream_t st) {
+                        const double4* cw, const double4* wt, const QueryOut& out, const int32_t* perm,
+                        cudaStream_t st) {
   auto kern = k_query_info<T, NC, STAGES, GRAD, METRIC, MGRAD>;
   const size_t smem = ((QWShape<T>::CHUNK + 127) & ~127u) +
                       (size_t)QW_WARPS * ((qw_warp_bytes<T, NC, STAGES, METRIC, MGRAD>() + 127) & ~127u);
@@ -901,46 +941,47 @@ static void launch_info(int nv, const T* f, const double* axes, int64_t q, const
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, QW_WARPS * 32, smem);
   const int64_t need = (q + QW_WARPS - 1) / QW_WARPS;
   const int64_t cap = (int64_t)kSMs * (per_sm > 0 ? per_sm : 1);
-  kern<<<(unsigned)(need < cap ? need : cap), QW_WARPS * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out);
+  kern<<<(unsigned)(need < cap ? need : cap), QW_WARPS * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out, perm);
 }
 
 template <typename T, int NC>
 static void launch_info_nc(bool grad, bool metric, bool mgrad, int nv, const T* f, const double* axes, int64_t q,
                            const uint8_t* status, const int32_t* rows, const double4* cw, const double4* wt,
-                           const QueryOut& out, cudaStream_t st) {
+                           const QueryOut& out, const int32_t* perm, cudaStream_t st) {
   // value/gradient streaming: 2 stages, 3 CTAs/SM; metric variants (det/lmin, LU and
   // Jacobi per corner, more registers): 3 stages, 2 CTAs/SM
   static const int stages_env = getenv("FIF_QW_STAGES") ? atoi(getenv("FIF_QW_STAGES")) : 2;
   if (metric) {
-    if (mgrad) launch_info<T, NC, 3, true, true, true>(nv, f, axes, q, status, rows, cw, wt, out, st);
-    else if (grad) launch_info<T, NC, 3, true, true, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
-    else launch_info<T, NC, 3, false, true, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+    if (mgrad) launch_info<T, NC, 3, true, true, true>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    else if (grad) launch_info<T, NC, 3, true, true, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    else launch_info<T, NC, 3, false, true, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
   } else if (stages_env == 3) {
-    if (grad) launch_info<T, NC, 3, true, false, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
-    else launch_info<T, NC, 3, false, false, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+    if (grad) launch_info<T, NC, 3, true, false, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    else launch_info<T, NC, 3, false, false, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
   } else {
-    if (grad) launch_info<T, NC, 2, true, false, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
-    else launch_info<T, NC, 2, false, false, false>(nv, f, axes, q, status, rows, cw, wt, out, st);
+    if (grad) launch_info<T, NC, 2, true, false, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    else launch_info<T, NC, 2, false, false, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
   }
 }
 
 template <typename T>
 static int launch_contract(int kind, bool trilinear, bool grad, bool metric, bool mgrad, int nv, const void* field,
                            const double* axes, int64_t q, const uint8_t* status, const int32_t* rows,
-                           const double4* cw, const double4* wt, const QueryOut& out, cudaStream_t st) {
+                           const double4* cw, const double4* wt, const QueryOut& out, const int32_t* perm,
+                           cudaStream_t st) {
   const T* f = reinterpret_cast<const T*>(field);
   if (kind == FIF_KIND_TRACE) {
     const unsigned blocks = query_blocks(q);
     const int threads = QC_WARPS * 32;
-#define QT(NC, G) k_query_trace<T, NC, G><<<blocks, threads, 0, st>>>(nv, f, axes, q, status, rows, cw, wt, out)
+#define QT(NC, G) k_query_trace<T, NC, G><<<blocks, threads, 0, st>>>(nv, f, axes, q, status, rows, cw, wt, out, perm)
     if (trilinear) { if (grad) QT(8, true); else QT(8, false); }
     else { if (grad) QT(1, true); else QT(1, false); }
 #undef QT
     FIF_CHECK_LAUNCH("k_query_trace");
     return FIF_OK;
   }
-  if (trilinear) launch_info_nc<T, 8>(grad, metric, mgrad, nv, f, axes, q, status, rows, cw, wt, out, st);
-  else launch_info_nc<T, 1>(grad, metric, mgrad, nv, f, axes, q, status, rows, cw, wt, out, st);
+  if (trilinear) launch_info_nc<T, 8>(grad, metric, mgrad, nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+  else launch_info_nc<T, 1>(grad, metric, mgrad, nv, f, axes, q, status, rows, cw, wt, out, perm, st);
   FIF_CHECK_LAUNCH("k_query_info");
   return FIF_OK;
 }
@@ -1017,6 +1058,29 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
   double4* s_cw = reinterpret_cast<double4*>(scratch + b_status);
   int32_t* s_rows = reinterpret_cast<int32_t*>(scratch + b_status + b_cw);
   double4* s_wt = reinterpret_cast<double4*>(scratch + b_status + b_cw + ((b_rows + 255) & ~(size_t)255));
+  // locality order (Morton order of the base voxel) for batches large enough to pay for the sort
+  int32_t* perm = nullptr;
+  unsigned char* sort_buf = nullptr;
+  static const int64_t sort_min = getenv("FIF_QUERY_SORT_MIN") ? atoll(getenv("FIF_QUERY_SORT_MIN")) : 262144;
+  if (q >= sort_min && q < (int64_t)INT32_MAX && sort_min > 0) {
+    size_t temp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)q, 0, 30, st);
+    const size_t b4 = ((size_t)q * 4 + 255) & ~(size_t)255;
+    if (cudaMallocAsync(&sort_buf, 4 * b4 + temp, st) != cudaSuccess) {
+      set_error("fif_query: cudaMallocAsync for the locality sort failed");
+      cudaFreeAsync(scratch, st);
+      return FIF_ERR_CUDA;
+    }
+    uint32_t* keys = reinterpret_cast<uint32_t*>(sort_buf);
+    uint32_t* keys2 = reinterpret_cast<uint32_t*>(sort_buf + b4);
+    int32_t* idx = reinterpret_cast<int32_t*>(sort_buf + 2 * b4);
+    perm = reinterpret_cast<int32_t*>(sort_buf + 3 * b4);
+    k_query_keys<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(gm, d_positions, q, keys, idx);
+    FIF_CHECK_LAUNCH("k_query_keys");
+    cub::DeviceRadixSort::SortPairs(sort_buf + 4 * b4, temp, keys, keys2, idx, perm, (int)q, 0, 30, st);
+    FIF_CHECK_LAUNCH("fif_query(locality sort)");
+  }
   const int np8 = (nv + 7) & ~7, ntiles = np8 / 8;
   const size_t dmma_smem = sizeof(double) * ((size_t)np8 * np8 + (size_t)QD_Q * np8 + 4 * (size_t)np8);
   static const bool simt_prep = getenv("FIF_QUERY_PREP_SIMT") != nullptr;
@@ -1024,7 +1088,7 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
     double* wtd = reinterpret_cast<double*>(s_wt);
     const int tri = trilinear ? 1 : 0;
     switch (ntiles) {
-#define PG(NT) case NT: launch_prep_gp<NT>(dmma_smem, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows, s_cw, wtd); break;
+#define PG(NT) case NT: launch_prep_gp<NT>(dmma_smem, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows, s_cw, wtd, perm); break;
       PG(1) PG(2) PG(3) PG(4) PG(5) PG(6) PG(7) PG(8) PG(9) PG(10) PG(11) PG(12)
 #undef PG
     }
@@ -1034,14 +1098,15 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
     if (prep_smem > 48 * 1024)
       cudaFuncSetAttribute(k_query_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem);
     k_query_prep<<<(unsigned)((q + QP_Q - 1) / QP_Q), QP_THREADS, prep_smem, st>>>(
-        *model, gm, d_slots, d_positions, d_axes, q, trilinear ? 1 : 0, s_status, s_rows, s_cw, s_wt);
+        *model, gm, d_slots, d_positions, d_axes, q, trilinear ? 1 : 0, s_status, s_rows, s_cw, s_wt, perm);
     FIF_CHECK_LAUNCH("k_query_prep");
   }
   const bool f64 = model->kind == FIF_MODEL_QUAD || (flags & FIF_Q_FIELD_F64);
   int rc = f64 ? launch_contract<double>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q,
-                                         s_status, s_rows, s_cw, s_wt, out, st)
+                                         s_status, s_rows, s_cw, s_wt, out, perm, st)
                : launch_contract<float>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q,
-                                        s_status, s_rows, s_cw, s_wt, out, st);
+                                        s_status, s_rows, s_cw, s_wt, out, perm, st);
+  if (sort_buf) cudaFreeAsync(sort_buf, st);
   cudaFreeAsync(scratch, st);
   return rc;
 }
