@@ -25,7 +25,7 @@ from .errors import WrongFactorKind
 from .field import Field
 
 __all__ = ["yaw_axes", "metric_yaw_batch", "gate_ok", "PotentialParams", "info_potential", "info_potential_grad",
-           "info_cost_grad"]
+           "info_cost_grad", "poly_eval", "poly_info_cost_grad"]
 
 
 def yaw_axes(yaws) -> np.ndarray:
@@ -108,3 +108,40 @@ def info_cost_grad(field: Field, positions, yaws, metric: str, potential: Potent
     dpot = np.where(ok, info_potential_grad(v, potential), 0.0)
     cost = float(mu_v * pot.sum() * dt)
     return cost, (mu_v * dt) * dpot[:, None] * r["grad"]
+
+
+def _poly_locate(durations: np.ndarray, times: np.ndarray):
+    """Segment index and local time of each sample (traj.py:113-118, PolyTrajectory._locate)."""
+    ends = np.cumsum(durations)
+    seg = np.minimum(np.searchsorted(ends, times, side="right"), len(durations) - 1)
+    return seg, times - (ends - durations)[seg]
+
+
+def poly_eval(coeffs, durations, times) -> np.ndarray:
+    """(K, 4) x, y, z, yaw of a piecewise polynomial with ascending-power coefficients
+    (4, S, 8) (PolyTrajectory.eval, traj.py:120-132, order 0)."""
+    coeffs = np.asarray(coeffs, dtype=np.float64)
+    times = np.atleast_1d(np.asarray(times, dtype=np.float64))
+    seg, tau = _poly_locate(np.asarray(durations, dtype=np.float64).reshape(-1), times)
+    basis = tau[:, None] ** np.arange(8)[None, :]
+    return np.einsum("ki,aki->ka", basis, coeffs[:, seg, :])
+
+
+def poly_info_cost_grad(field: Field, coeffs, durations, times, metric: str, potential: PotentialParams, mu_v: float,
+                        dt: float, mode: str = "nearest"):
+    """Information term of the sampled trajectory cost (traj.py:350-365) for a
+    PolyTrajectory given by its coefficients, and its exact gradient w.r.t. the
+    coefficients (4, S, 8): the chain rule through the power basis that replaces the
+    central differences of traj._FreeParamProblem.gradient (traj.py:383-398) for this
+    term.  Returns (cost, d cost / d coeffs)."""
+    coeffs = np.asarray(coeffs, dtype=np.float64)
+    durations = np.asarray(durations, dtype=np.float64).reshape(-1)
+    times = np.atleast_1d(np.asarray(times, dtype=np.float64))
+    vals = poly_eval(coeffs, durations, times)
+    cost, g = info_cost_grad(field, vals[:, :3], vals[:, 3], metric, potential, mu_v, dt, mode)
+    seg, tau = _poly_locate(durations, times)
+    basis = tau[:, None] ** np.arange(8)[None, :]
+    grad = np.zeros_like(coeffs)
+    for a in range(4):
+        np.add.at(grad[a], seg, g[:, a:a + 1] * basis)
+    return cost, grad

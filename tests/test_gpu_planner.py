@@ -98,3 +98,40 @@ def test_info_cost_gradient_and_gate(oracle, g_small, setup):
             assert g[t, j] == pytest.approx(fd, rel=1e-4, abs=1e-9 * max(1.0, abs(fd)))
     ok = P.gate_ok(f, pos, yaws, "det", pot.epsilon, "trilinear")
     assert np.array_equal(ok, vals >= pot.epsilon)
+
+
+def test_poly_trajectory_gradient(oracle, g_small, setup):
+    """Chain rule through the polynomial basis (traj.py:120-132) vs FD over the coefficients."""
+    models, grid = setup
+    m = models["quad"]
+    f = field_from_reference(grid, m, "info", g_small["factors_quad_info"])
+    rng = np.random.default_rng(13)
+    c = grid.centers()
+    lo, hi = c[0] + 0.3, c[-1] - 0.3
+    S = 2
+    coeffs = np.zeros((4, S, 8))
+    for s in range(S):
+        coeffs[:3, s, 0] = rng.uniform(lo, hi)
+        coeffs[:3, s, 1] = rng.uniform(-0.2, 0.2, 3)
+        coeffs[3, s, 0] = rng.uniform(-np.pi, np.pi)
+        coeffs[3, s, 1] = rng.uniform(-0.5, 0.5)
+    durations = np.array([1.0, 1.5])
+    times = np.arange(0.0, 2.5, 0.1)
+    vals = P.poly_eval(coeffs, durations, times)
+    v0 = P.metric_yaw_batch(f, vals[:, :3], vals[:, 3], "det", "trilinear")["values"]
+    pot = P.PotentialParams(epsilon=float(np.max(v0)) * 1.1, k_q=1.0)
+    cost, grad = P.poly_info_cost_grad(f, coeffs, durations, times, "det", pot, mu_v=0.5, dt=0.1, mode="trilinear")
+
+    def total(cf):
+        vv = P.poly_eval(cf, durations, times)
+        v, st = _oracle_metric(oracle, g_small, grid, m, "det", vv[:, :3], vv[:, 3], True)
+        return 0.5 * 0.1 * np.where(st == 0, P.info_potential(v, pot), pot.b_l).sum()
+
+    assert cost == pytest.approx(total(coeffs), rel=1e-9)
+    h = 1e-6
+    for (a, s, i) in [(0, 0, 0), (1, 1, 1), (2, 0, 2), (3, 1, 0), (3, 0, 3), (0, 1, 4)]:
+        cp, cm = coeffs.copy(), coeffs.copy()
+        cp[a, s, i] += h
+        cm[a, s, i] -= h
+        fd = (total(cp) - total(cm)) / (2 * h)
+        assert grad[a, s, i] == pytest.approx(fd, rel=1e-4, abs=1e-9 * max(1.0, abs(fd)))
