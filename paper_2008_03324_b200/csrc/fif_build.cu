@@ -981,9 +981,8 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       const PairF q = pair_prologue(a, b, ch, cl, inv_s2);
       float e[21];
       entries21(q, a, e);
-      float mx = 0.f;
-#pragma unroll
-      for (int k = 0; k < 21; ++k) mx = fmaxf(mx, fabsf(e[k]));
+      // |entry| <= w max(1, 2|p|, |p|^2) <= w (1 + |p|^2) (|c2| <= |p|); x2 covers FP32 rounding
+      float mx = fmaf(a.w, 2.0f * q.w, 2.0f * q.w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       if (lane == 0) atomicMax(&tmax[pv], __float_as_int(mx));
