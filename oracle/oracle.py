@@ -14,7 +14,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libfif_oracle.so")
+_FAST_PATH = os.path.join(_HERE, "libfif_cpu_fast.so")
 _lib = None
+_fast = None
 
 _d = ctypes.c_double
 _i64 = ctypes.c_int64
@@ -54,6 +56,29 @@ def lib():
         L.or_openmp_max_threads.restype = _int
         _lib = L
     return _lib
+
+
+def fast_lib():
+    """The blocked / vectorised CPU port of the GP build (bench CPU legs only)."""
+    global _fast
+    if _fast is None:
+        if not os.path.exists(_FAST_PATH):
+            build()
+        L = ctypes.CDLL(_FAST_PATH)
+        L.fp_build_gp.argtypes = [_p, _i64, _p, _i64, _d, _p, _int, _p, _d, _d, _int, _p, _int]
+        _fast = L
+    return _fast
+
+
+def build_gp_factors_fast(centers, points, sigma, zs, kinv, ks, cos_alpha, want_trace, nthreads=0):
+    """The reference GP build (kernels.py:471-524) as a fast CPU port (no mask)."""
+    c, p = _c(centers).reshape(-1, 3), _c(points).reshape(-1, 3)
+    zs, kinv = _c(zs), _c(kinv)
+    ns = zs.shape[0]
+    out = np.empty((c.shape[0], ns if want_trace else 36 * ns))
+    fast_lib().fp_build_gp(_ptr(c), c.shape[0], _ptr(p), p.shape[0], float(sigma), _ptr(zs), ns, _ptr(kinv),
+                           float(ks), float(cos_alpha), int(bool(want_trace)), _ptr(out), int(nthreads))
+    return out
 
 
 def _c(a, dtype=np.float64):

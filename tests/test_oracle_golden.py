@@ -117,3 +117,22 @@ def test_landmark_fim_kats(oracle, g_kats):
         f, tr = oracle.fim_flat(g_kats["p"][i], g_kats["t"][i], 1.0 / g_kats["sigma"][i] ** 2)
         np.testing.assert_allclose(f, g_kats["fim"][i], rtol=1e-13, atol=1e-15)
         assert tr == pytest.approx(np.trace(f), rel=1e-14)
+
+
+def test_fast_cpu_port_matches_reference(g_small, g_models):
+    """bench.py's CPU baseline (oracle/fif_cpu_fast.c, blocked + vectorised) computes the
+    reference's GP build: equal to the reference's own factors to ~1e-13."""
+    import numpy as np
+    from oracle import oracle as O
+
+    import paper_2008_03324_b200 as F
+    from tests._helpers import models_from_golden
+
+    m = models_from_golden(g_models)["gp30"]
+    c = F.GridConfig(g_small["origin"], float(np.asarray(g_small["voxel_size"]).reshape(-1)[0]),
+                     g_small["dims"]).centers()
+    for kind in ("trace", "info"):
+        ref = g_small[f"factors_gp30_{kind}"]
+        mine = O.build_gp_factors_fast(c, g_small["points"], 1.0, m.samples, m.kinv, m.k_s, np.cos(m.alpha),
+                                       kind == "trace", nthreads=2)
+        assert np.abs(mine - ref).max() <= 1e-12 * np.abs(ref).max()
