@@ -258,10 +258,11 @@ def test_metric_gradients_vs_finite_difference(oracle, g_small, models, small_gr
         assert err.max() <= tol, (f64, err.max())
 
 
-@pytest.mark.parametrize("ns", [7, 150])
+@pytest.mark.parametrize("ns", [7, 150, 220])
 def test_gp_query_other_sizes(oracle, ns):
-    """GP query path at N_s = 7 (one k-chunk) and N_s = 150 (kinv too large for the DMMA
-    prep's shared-memory tile: SIMT prep) on a GPU-built field vs the oracle."""
+    """GP query path at N_s = 7 (one k-chunk), 150 (kinv too large for the DMMA prep's
+    shared-memory tile: SIMT prep) and 220 (three warps per voxel in the info build) on a
+    GPU-built field vs the oracle."""
     from tests._helpers import oracle_field
 
     m = F.build_gp_model(ns)
