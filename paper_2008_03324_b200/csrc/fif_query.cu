@@ -374,8 +374,15 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
                : "d"(a), "d"(b));
 }
 
-template <int NT>
-__global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, QueryGeom gm,
+// QQ queries per CTA: 32 for streaming batches, 8 for small batches (more CTAs, so the
+// latency-bound prep spreads over more SMs)
+template <int QQ>
+struct QDShape {
+  static constexpr int THREADS = QQ == 32 ? QD_THREADS : 128;
+  static constexpr int MT_PER_WARP = QQ / 2 / (THREADS / 32);
+};
+template <int NT, int QQ>
+__global__ void __launch_bounds__(QDShape<QQ>::THREADS, 3) k_query_prep_gp(fif_model m, QueryGeom gm,
                                                               const int32_t* __restrict__ slots,
                                                               const double* __restrict__ pos,
                                                               const double* __restrict__ axes, int64_t nq,
@@ -385,14 +392,31 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
                                                               const int32_t* __restrict__ perm) {
   extern __shared__ double smd[];
   constexpr int NP8 = 8 * NT, KS = NP8 / 4;
-  constexpr int MT_PER_WARP = QD_Q / 2 / (QD_THREADS / 32);
+  constexpr int MT_PER_WARP = QDShape<QQ>::MT_PER_WARP;
+  constexpr int NWARPS = QDShape<QQ>::THREADS / 32;
   const int nv = m.n_v;
-  double* kf = smd;                  // kinv B fragments: [KS][NT][32] (fragment order, zero padded)
-  double* sv = kf + KS * NT * 32;    // [QD_Q][NP8] v^r
-  double* sa = sv + QD_Q * NP8;      // [NP8][4] {1, zs/l^2}
-  const int64_t q0 = blockIdx.x * (int64_t)QD_Q;
+  // kinv row-major (stride nv) landed by one TMA bulk copy; rows nv..NP8-1 read by the
+  // padded k-steps are zeroed (their A entries are zero too, and 0 x NaN would not be)
+  double* kf = smd;                                  // [NP8][nv] (+ tail)
+  double* sv = kf + ((NP8 * nv + 8 + 15) & ~15);     // [QQ][NP8] v^r
+  double* sa = sv + QQ * NP8;                        // [NP8][4] {1, zs/l^2}
+  __shared__ __align__(8) uint64_t kbar;
+  const int64_t q0 = blockIdx.x * (int64_t)QQ;
   const int t = threadIdx.x;
-  if (t < QD_Q && q0 + t < nq) {  // corners and trilinear weights (FP64, reference order)
+  const uint32_t kbytes = (uint32_t)(nv * nv * sizeof(double));
+  const bool use_tma = (kbytes % 16u) == 0 && (reinterpret_cast<uintptr_t>(m.kinv) & 15) == 0;
+  if (use_tma) {
+    if (t == 0) {
+      mbar_init(&kbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&kbar, kbytes);
+      tma_bulk_g2s(kf, m.kinv, kbytes, &kbar);
+    }
+  } else {
+    for (int idx = t; idx < nv * nv; idx += blockDim.x) kf[idx] = m.kinv[idx];
+  }
+  for (int idx = nv * nv + t; idx < NP8 * nv + 8; idx += blockDim.x) kf[idx] = 0.0;
+  if (t < QQ && q0 + t < nq) {  // corners and trilinear weights (FP64, reference order)
     const int64_t q = q0 + t;
     int nc = 0;
     int64_t r[8];
@@ -407,11 +431,6 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
     }
   }
   const double inv_l2 = 1.0 / (m.ell * m.ell);
-  for (int idx = t; idx < KS * NT * 32; idx += blockDim.x) {  // B[g][k] = kinv[g][k], g = 4ks+tq, k = 8nt+row
-    const int ln = idx & 31, f = idx >> 5, ks = f / NT, nt = f - ks * NT;
-    const int g = 4 * ks + (ln & 3), k = 8 * nt + (ln >> 2);
-    kf[idx] = (g < nv && k < nv) ? m.kinv[(int64_t)g * nv + k] : 0.0;
-  }
   for (int g = t; g < NP8; g += blockDim.x) {
     const bool ok = g < nv;
     sa[4 * g] = ok ? 1.0 : 0.0;
@@ -419,7 +438,7 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
     sa[4 * g + 2] = ok ? m.zs[3 * g + 1] * inv_l2 : 0.0;
     sa[4 * g + 3] = ok ? m.zs[3 * g + 2] * inv_l2 : 0.0;
   }
-  for (int idx = t; idx < QD_Q * NP8; idx += blockDim.x) {  // v^r (kernels.py:652-657)
+  for (int idx = t; idx < QQ * NP8; idx += blockDim.x) {  // v^r (kernels.py:652-657)
     const int qi = idx / NP8, g = idx - qi * NP8;
     const int64_t q = q0 + qi;
     double v = 0.0;
@@ -431,6 +450,7 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
     }
     sv[idx] = v;
   }
+  if (use_tma) mbar_wait(&kbar, 0);
   __syncthreads();
   const int warp = t >> 5, lane = t & 31;
   const int row = lane >> 2, tq = lane & 3;  // A/C row; A col = B row = tq
@@ -442,7 +462,9 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
   for (int i = 0; i < MT_PER_WARP; ++i)
 #pragma unroll
     for (int n = 0; n < NT; ++n) c[i][n][0] = c[i][n][1] = 0.0;
-  const double* kfl = kf + lane;
+  // B[g][k] = kinv[g][k] with g = 4 ks + tq, k = 8 n + row; columns k >= nv read the
+  // next row (finite) and only feed discarded outputs
+  const double* kfl = kf + tq * nv + row;
 #pragma unroll 1
   for (int ks = 0; ks < KS; ++ks) {
     const int g = 4 * ks + tq;
@@ -450,19 +472,19 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
     double av[MT_PER_WARP];
 #pragma unroll
     for (int i = 0; i < MT_PER_WARP; ++i) {
-      const int qi = (warp + i * (QD_THREADS / 32)) * 2 + qq;
+      const int qi = (warp + i * NWARPS) * 2 + qq;
       av[i] = sv[qi * NP8 + g] * sg;
     }
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
-      const double b = kfl[(ks * NT + n) * 32];
+      const double b = kfl[4 * ks * nv + 8 * n];
 #pragma unroll
       for (int i = 0; i < MT_PER_WARP; ++i) dmma_884(c[i][n][0], c[i][n][1], av[i], b);
     }
   }
 #pragma unroll
   for (int i = 0; i < MT_PER_WARP; ++i) {
-    const int64_t q = q0 + (warp + i * (QD_THREADS / 32)) * 2 + qq;
+    const int64_t q = q0 + (warp + i * NWARPS) * 2 + qq;
     if (q >= nq) continue;
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -473,13 +495,13 @@ __global__ void __launch_bounds__(QD_THREADS, 3) k_query_prep_gp(fif_model m, Qu
   }
 }
 
-template <int NT>
+template <int NT, int QQ>
 static void launch_prep_gp(size_t smem, int64_t q, cudaStream_t st, const fif_model& m, const QueryGeom& gm,
                            const int32_t* slots, const double* pos, const double* axes, int trilinear,
                            uint8_t* status, int32_t* rows, double4* cw, double* wt, const int32_t* perm) {
-  auto kern = k_query_prep_gp<NT>;
+  auto kern = k_query_prep_gp<NT, QQ>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<(unsigned)((q + QD_Q - 1) / QD_Q), QD_THREADS, smem, st>>>(m, gm, slots, pos, axes, q, trilinear, status,
+  kern<<<(unsigned)((q + QQ - 1) / QQ), QDShape<QQ>::THREADS, smem, st>>>(m, gm, slots, pos, axes, q, trilinear, status,
                                                                      rows, cw, wt, perm);
 }
 
@@ -496,6 +518,11 @@ static void launch_prep_gp(size_t smem, int64_t q, cudaStream_t st, const fif_mo
 // in FP64 from the smem copy.  No block-level synchronisation: warps are
 // independent streams, the block only shares a zero row used for absent corners.
 constexpr int QW_WARPS = 4;
+// warps per CTA: the streaming variants (2-3 stages) run 4 independent query warps per
+// CTA; the small-batch variant (QW_SMALL_STAGES: every k-chunk of a query in flight at
+// once, latency- rather than bandwidth-bound) runs one warp per CTA
+constexpr int QW_SMALL_STAGES = 8;
+__host__ __device__ constexpr int qw_wpb(int stages) { return stages >= QW_SMALL_STAGES ? 1 : QW_WARPS; }
 
 // k-chunk length: 840 bytes of each corner row per stage for FP32 and FP64 rows.
 template <typename T>
@@ -515,7 +542,8 @@ __host__ __device__ constexpr uint32_t qw_warp_bytes() {
 }
 
 template <typename T, int NC, int STAGES, bool GRAD, bool METRIC, bool MGRAD>
-__global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_info(int nv, const T* __restrict__ field,
+__global__ void __launch_bounds__(qw_wpb(STAGES) * 32, STAGES == 2 ? 3 : (STAGES == 3 ? 2 : 3))
+k_query_info(int nv, const T* __restrict__ field,
                                                              const double* __restrict__ axes, int64_t nq,
                                                              const uint8_t* __restrict__ status,
                                                              const int32_t* __restrict__ rows,
@@ -544,8 +572,9 @@ __global__ void __launch_bounds__(QW_WARPS * 32, STAGES == 2 ? 3 : 2) k_query_in
   __syncthreads();
   const int64_t rw = (int64_t)nv * 21;
   const int nch = (nv + KC - 1) / KC;
-  const int64_t tw = (int64_t)gridDim.x * QW_WARPS;
-  const int64_t qfirst = blockIdx.x * (int64_t)QW_WARPS + warp;
+  constexpr int WPB = qw_wpb(STAGES);
+  const int64_t tw = (int64_t)gridDim.x * WPB;
+  const int64_t qfirst = blockIdx.x * (int64_t)WPB + warp;
   const int64_t nmine = qfirst < nq ? (nq - qfirst + tw - 1) / tw : 0;
   auto qof = [&](int64_t i) { return qfirst + i * tw; };
   auto row_of = [&](int64_t i) -> int32_t {  // lane c < NC: corner c's row of my i-th query
@@ -935,13 +964,14 @@ static void launch_info(int nv, const T* f, const double* axes, int64_t q, const
                         cudaStream_t st) {
   auto kern = k_query_info<T, NC, STAGES, GRAD, METRIC, MGRAD>;
   const size_t smem = ((QWShape<T>::CHUNK + 127) & ~127u) +
-                      (size_t)QW_WARPS * ((qw_warp_bytes<T, NC, STAGES, METRIC, MGRAD>() + 127) & ~127u);
+                      (size_t)qw_wpb(STAGES) * ((qw_warp_bytes<T, NC, STAGES, METRIC, MGRAD>() + 127) & ~127u);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, QW_WARPS * 32, smem);
-  const int64_t need = (q + QW_WARPS - 1) / QW_WARPS;
+  constexpr int WPB = qw_wpb(STAGES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem);
+  const int64_t need = (q + WPB - 1) / WPB;
   const int64_t cap = (int64_t)kSMs * (per_sm > 0 ? per_sm : 1);
-  kern<<<(unsigned)(need < cap ? need : cap), QW_WARPS * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out, perm);
+  kern<<<(unsigned)(need < cap ? need : cap), WPB * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out, perm);
 }
 
 template <typename T, int NC>
@@ -951,6 +981,15 @@ static void launch_info_nc(bool grad, bool metric, bool mgrad, int nv, const T* 
   // value/gradient streaming: 2 stages, 3 CTAs/SM; metric variants (det/lmin, LU and
   // Jacobi per corner, more registers): 3 stages, 2 CTAs/SM
   static const int stages_env = getenv("FIF_QW_STAGES") ? atoi(getenv("FIF_QW_STAGES")) : 2;
+  if (q <= (int64_t)kSMs * 3) {  // small batch: one query per CTA, all k-chunks in flight
+    constexpr int S = QW_SMALL_STAGES;
+    if (mgrad) launch_info<T, NC, S, true, true, true>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    else if (metric && grad) launch_info<T, NC, S, true, true, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    else if (metric) launch_info<T, NC, S, false, true, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    else if (grad) launch_info<T, NC, S, true, false, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    else launch_info<T, NC, S, false, false, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
+    return;
+  }
   if (metric) {
     if (mgrad) launch_info<T, NC, 3, true, true, true>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
     else if (grad) launch_info<T, NC, 3, true, true, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
@@ -1082,13 +1121,21 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
     FIF_CHECK_LAUNCH("fif_query(locality sort)");
   }
   const int np8 = (nv + 7) & ~7, ntiles = np8 / 8;
-  const size_t dmma_smem = sizeof(double) * ((size_t)np8 * np8 + (size_t)QD_Q * np8 + 4 * (size_t)np8);
+  const size_t dmma_smem = sizeof(double) * ((size_t)((np8 * nv + 8 + 15) & ~15) + (size_t)QD_Q * np8 + 4 * (size_t)np8);
   static const bool simt_prep = getenv("FIF_QUERY_PREP_SIMT") != nullptr;
   if (model->kind == FIF_MODEL_GP && ntiles <= 12 && !simt_prep) {
     double* wtd = reinterpret_cast<double*>(s_wt);
     const int tri = trilinear ? 1 : 0;
+    const bool small = q <= 1024;
+    const size_t sm = small ? dmma_smem - sizeof(double) * (size_t)(QD_Q - 8) * np8 : dmma_smem;
     switch (ntiles) {
-#define PG(NT) case NT: launch_prep_gp<NT>(dmma_smem, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows, s_cw, wtd, perm); break;
+#define PG(NT)                                                                                                   \
+  case NT:                                                                                                       \
+    if (small) launch_prep_gp<NT, 8>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows,  \
+                                     s_cw, wtd, perm);                                                           \
+    else launch_prep_gp<NT, 32>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows, s_cw, \
+                                wtd, perm);                                                                      \
+    break;
       PG(1) PG(2) PG(3) PG(4) PG(5) PG(6) PG(7) PG(8) PG(9) PG(10) PG(11) PG(12)
 #undef PG
     }

@@ -502,6 +502,13 @@ class Field:
                                             _device.stream_handle(dev)), "fif_query")
         return out
 
+    def query_graph(self, batch: int, mode: str = "trilinear", outputs=("trace", "full"), grad: bool = False,
+                    field_f64: bool = False) -> "QueryGraph":
+        """A CUDA-graph-captured query of a fixed batch size (planner inner loops issue
+        many small batches, where launch latency dominates): static device input/output
+        buffers, one graph replay per call.  See QueryGraph.run."""
+        return QueryGraph(self, batch, mode, outputs, grad, field_f64)
+
     def query_batch(self, positions, rotations=None, axes=None, outputs=("trace", "full"), grad: bool = False,
                     mode: str = "trilinear", to_numpy: bool = False) -> dict:
         """Batched query with optional analytic pose gradients (new in this build).
@@ -789,3 +796,57 @@ def build(landmarks, config, model, factor_kind="info", matchability=ALWAYS_MATC
           parallel=False, device=None) -> Field:
     """Module-level alias for Field.build (field.py:645-648)."""
     return Field.build(landmarks, config, model, factor_kind, matchability, sigma, parallel, device)
+
+
+class QueryGraph:
+    """Fixed-size batched query captured once into a CUDA graph (Field.query_graph).
+
+    run(positions, axes) copies the inputs into the static device buffers (from host
+    or device tensors; a short batch is padded by repeating its last pose), replays the
+    graph and returns the static output tensors (valid until the next run); replay()
+    skips the copies when the caller writes self.positions / self.axes directly.  The
+    field must not change (add/remove landmarks) while the graph lives."""
+
+    def __init__(self, field: Field, batch: int, mode: str, outputs, grad: bool, field_f64: bool):
+        if batch <= 0:
+            raise ValueError("batch must be positive")
+        self.field, self.batch = field, int(batch)
+        dev = field.device
+        outs = set(outputs)
+        self._kw = dict(trace="trace" in outs, full="full" in outs, det="det" in outs, lmin="lmin" in outs,
+                        grad=grad, field_f64=field_f64)
+        field._check_mode(mode)
+        self._mode = mode
+        self.positions = torch.zeros((self.batch, 3), dtype=torch.float64, device=dev)
+        self.axes = torch.zeros((self.batch, 3), dtype=torch.float64, device=dev)
+        self.axes[:, 2] = 1.0
+        self.out: dict = {}
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):  # warm-up outside capture: allocations, function attributes
+            field.query_device(self.positions, self.axes, mode, out=self.out, **self._kw)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=s):
+            field.query_device(self.positions, self.axes, mode, out=self.out, **self._kw)
+
+    def replay(self) -> dict:
+        """Replay on the current contents of self.positions / self.axes (fill them in
+        place, e.g. from a planner's own kernels, to skip the input copies)."""
+        self.graph.replay()
+        return self.out
+
+    def run(self, positions, axes) -> dict:
+        n = positions.shape[0]
+        if n > self.batch or axes.shape[0] != n:
+            raise ValueError(f"batch of {n} poses does not fit the captured size {self.batch}")
+        p = positions if isinstance(positions, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(positions,
+                                                                                                        np.float64))
+        a = axes if isinstance(axes, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(axes, np.float64))
+        self.positions[:n].copy_(p.reshape(-1, 3), non_blocking=True)
+        self.axes[:n].copy_(a.reshape(-1, 3), non_blocking=True)
+        if n < self.batch and n > 0:
+            self.positions[n:].copy_(self.positions[n - 1:n].expand(self.batch - n, 3))
+            self.axes[n:].copy_(self.axes[n - 1:n].expand(self.batch - n, 3))
+        self.graph.replay()
+        return self.out

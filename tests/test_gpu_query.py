@@ -285,3 +285,21 @@ def test_gp_query_other_sizes(oracle, ns):
     assert rel(res["trace"], rt).max() <= TOL
     e = np.linalg.norm((res["fim"] - rf).reshape(50, -1), axis=1) / np.linalg.norm(rf.reshape(50, -1), axis=1)
     assert e.max() <= TOL
+
+
+def test_query_graph_matches_direct(g_small, models, small_grid):
+    """CUDA-graph-captured fixed-size queries (Field.query_graph) == direct queries."""
+    m = models["gp70"]
+    f = field_from_reference(small_grid, m, "info", g_small["factors_gp70_info"])
+    rng = np.random.default_rng(3)
+    c = small_grid.centers()
+    qg = f.query_graph(64, "trilinear", outputs=("trace", "full", "det"), grad=True)
+    for n in (64, 37):
+        pos = rng.uniform(c[0], c[-1], size=(n, 3))
+        rots = np.stack([F.random_rotation(rng) for _ in range(n)])
+        ax = np.ascontiguousarray(rots[:, :, 2])
+        got = {k: v[:n].cpu().numpy() for k, v in qg.run(pos, ax).items()}
+        ref = f.query_device(torch.tensor(pos, device="cuda"), torch.tensor(ax, device="cuda"), "trilinear",
+                             trace=True, full=True, det=True, grad=True)
+        for k in ("trace", "trace_grad", "fim", "fim_grad", "det", "det_grad", "status"):
+            assert np.array_equal(got[k], ref[k].cpu().numpy()), k
