@@ -1056,6 +1056,22 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
   FIF_CHECK_ARG(grid->voxel_size > 0, "fif_query: voxel_size <= 0");
   const int nv = model->kind == FIF_MODEL_QUAD ? 10 : model->n_v;
   FIF_CHECK_ARG(nv >= 1 && nv <= 1024, "fif_query: n_v out of range");
+  // bound the per-call scratch (32 nv bytes of rotation weights per query): very large
+  // batches run as consecutive slices of kQueryChunk queries on the same stream
+  constexpr int64_t kQueryChunk = 1 << 21;
+  if (q > kQueryChunk) {
+    for (int64_t q0 = 0; q0 < q; q0 += kQueryChunk) {
+      const int64_t n = q - q0 < kQueryChunk ? q - q0 : kQueryChunk;
+      auto sl = [&](double* p, int64_t w) { return p ? p + q0 * w : nullptr; };
+      fif_query_out os{sl(o->trace, 1),    sl(o->trace_grad, 6), sl(o->fim, 36),     sl(o->fim_grad, 216),
+                       sl(o->det, 1),      sl(o->det_grad, 6),   sl(o->lmin, 1),     sl(o->lmin_grad, 6),
+                       o->status ? o->status + q0 : nullptr};
+      const int rc = fif_query_ex(factor_kind, model, grid, d_field, d_slots, d_positions + 3 * q0, d_axes + 3 * q0,
+                                  n, mode, flags, &os, stream);
+      if (rc != FIF_OK) return rc;
+    }
+    return FIF_OK;
+  }
   QueryGeom gm{grid->origin[0], grid->origin[1], grid->origin[2], grid->voxel_size,
                grid->dims[0],   grid->dims[1],   grid->dims[2]};
   QueryOut out{(flags & FIF_Q_TRACE) ? o->trace : nullptr,

@@ -303,3 +303,20 @@ def test_query_graph_matches_direct(g_small, models, small_grid):
                              trace=True, full=True, det=True, grad=True)
         for k in ("trace", "trace_grad", "fim", "fim_grad", "det", "det_grad", "status"):
             assert np.array_equal(got[k], ref[k].cpu().numpy()), k
+
+
+def test_very_large_batch_is_sliced(g_small, models, small_grid):
+    """Batches above the per-call scratch bound run as slices (and in locality order):
+    every query's result equals the same query issued alone."""
+    m = models["gp30"]
+    f = field_from_reference(small_grid, m, "info", g_small["factors_gp30_info"])
+    rng = np.random.default_rng(8)
+    c = small_grid.centers()
+    n = (1 << 21) + 1500
+    pos = torch.tensor(rng.uniform(c[0] - 0.3, c[-1] + 0.3, size=(n, 3)), device="cuda")
+    ax = torch.nn.functional.normalize(torch.tensor(rng.standard_normal((n, 3)), device="cuda"), dim=1)
+    big = f.query_device(pos, ax, "trilinear", trace=True, full=True, grad=True)
+    for sl in (slice(0, 700), slice((1 << 21) - 300, (1 << 21) + 300), slice(n - 500, n)):
+        small = f.query_device(pos[sl].contiguous(), ax[sl].contiguous(), "trilinear", trace=True, full=True, grad=True)
+        for k in ("trace", "trace_grad", "fim", "fim_grad", "status"):
+            assert torch.equal(big[k][sl], small[k]), k
