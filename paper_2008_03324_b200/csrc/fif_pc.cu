@@ -13,6 +13,8 @@
 // per-warp smem queue so the FP32 6x6 accumulation runs on full warps.
 #include "fif_common.cuh"
 
+#include <cub/cub.cuh>
+
 namespace fif {
 
 constexpr int PC_WARPS = 15;  // pose warps; + 1 producer warp = 4 warps per SM sub-partition
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
                                                           int64_t nq, const double* __restrict__ pts,
                                                           const float4* __restrict__ ptab, int64_t n, fif_camera cam,
                                                           float inv_s2, double* __restrict__ out,
-                                                          uint8_t* __restrict__ mask) {
+                                                          uint8_t* __restrict__ mask, const int32_t* __restrict__ perm) {
   extern __shared__ float4 pcsm[];
   float4* ring_hi = pcsm;                                  // [PC_NBUF][PC_TILE]
   float4* ring_lo = pcsm + PC_NBUF * PC_TILE;              // [PC_NBUF][PC_TILE]
@@ -181,12 +183,13 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
   int64_t seq = 0;
   for (int64_t it = 0; it < npi; ++it) {
     const int64_t q0 = blockIdx.x * (int64_t)PC_WARPS + it * qstride;
-    const int64_t q = q0 + warp;
-    const bool has_pose = q < nq;
+    const int64_t qs = q0 + warp;                                  // slot (similar poses adjacent)
+    const int64_t q = qs < nq && perm ? (int64_t)perm[qs] : qs;  // caller's pose index
+    const bool has_pose = qs < nq;
     PoseAff A;
     float thx, thy, thz, tlx, tly, tlz;
     {
-      const int64_t qq = has_pose ? q : q0;
+      const int64_t qq = has_pose ? q : (perm ? (int64_t)perm[q0] : q0);
       const double* R = rot + 9 * qq;
       const double tx = tr[3 * qq], ty = tr[3 * qq + 1], tz = tr[3 * qq + 2];
       split_f32(tx, thx, tlx);
@@ -303,6 +306,69 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
   }
 }
 
+// Pose order for load balance: the 15 pose warps of a CTA share landmark tiles, so the
+// CTA runs at the pace of its slowest pose; grouping similar poses (coarse position cell
+// and optical-axis direction) into the same CTA evens their visible-landmark counts.
+// per-block min / max of the pose positions (pass 1), reduced by one block (pass 2)
+constexpr int PK_BLOCKS = 512;
+__global__ void k_pc_bbox(const double* __restrict__ tr, int64_t nq, double* __restrict__ part) {
+  __shared__ double lo[3][256], hi[3][256];
+  double l[3] = {1e300, 1e300, 1e300}, h[3] = {-1e300, -1e300, -1e300};
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x)
+    for (int a = 0; a < 3; ++a) {
+      l[a] = fmin(l[a], tr[3 * q + a]);
+      h[a] = fmax(h[a], tr[3 * q + a]);
+    }
+  for (int a = 0; a < 3; ++a) {
+    lo[a][threadIdx.x] = l[a];
+    hi[a][threadIdx.x] = h[a];
+  }
+  __syncthreads();
+  for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
+    if ((int)threadIdx.x < s2)
+      for (int a = 0; a < 3; ++a) {
+        lo[a][threadIdx.x] = fmin(lo[a][threadIdx.x], lo[a][threadIdx.x + s2]);
+        hi[a][threadIdx.x] = fmax(hi[a][threadIdx.x], hi[a][threadIdx.x + s2]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) {
+    part[blockIdx.x * 6 + threadIdx.x] = lo[threadIdx.x][0];
+    part[blockIdx.x * 6 + 3 + threadIdx.x] = hi[threadIdx.x][0];
+  }
+}
+__global__ void k_pc_keys(const double* __restrict__ rot, const double* __restrict__ tr, int64_t nq,
+                          const double* __restrict__ part, int nparts, uint32_t* __restrict__ keys,
+                          int32_t* __restrict__ idx) {
+  __shared__ double box[6];
+  if (threadIdx.x < 6) {
+    const bool is_lo = threadIdx.x < 3;
+    double v = is_lo ? 1e300 : -1e300;
+    for (int b = 0; b < nparts; ++b) v = is_lo ? fmin(v, part[b * 6 + threadIdx.x]) : fmax(v, part[b * 6 + threadIdx.x]);
+    box[threadIdx.x] = v;
+  }
+  __syncthreads();
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  auto cell = [&](int a) -> uint32_t {  // 16 cells per axis over the poses' bounding box
+    const double ext = box[3 + a] - box[a];
+    const double c = ext > 0 ? floor((tr[3 * q + a] - box[a]) / ext * 16.0) : 0.0;
+    return (uint32_t)fmin(fmax(c, 0.0), 15.0);
+  };
+  const uint32_t pc = (cell(2) << 8) | (cell(1) << 4) | cell(0);
+  // optical axis = R[:, 2]: dominant axis and sign (6 faces) x 4 x 4 face cells
+  const double ax = rot[9 * q + 2], ay = rot[9 * q + 5], az = rot[9 * q + 8];
+  const double fx = fabs(ax), fy = fabs(ay), fz = fabs(az);
+  int face;
+  double u, v;
+  if (fx >= fy && fx >= fz) { face = ax > 0 ? 0 : 1; u = ay / fx; v = az / fx; }
+  else if (fy >= fz) { face = ay > 0 ? 2 : 3; u = ax / fy; v = az / fy; }
+  else { face = az > 0 ? 4 : 5; u = ax / fz; v = ay / fz; }
+  const uint32_t ui = (uint32_t)fmin(3.0, (u + 1.0) * 2.0), vi = (uint32_t)fmin(3.0, (v + 1.0) * 2.0);
+  keys[q] = (((uint32_t)face * 16u + ui * 4u + vi) << 12) | pc;
+  idx[q] = (int32_t)q;
+}
+
 }  // namespace fif
 
 using namespace fif;
@@ -341,12 +407,36 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
     }
     attr = true;
   }
+  // similar poses share a CTA (load balance across its pose warps)
+  int32_t* perm = nullptr;
+  unsigned char* sbuf = nullptr;
+  if (q >= (int64_t)PC_WARPS * kSMs * 4 && q < (int64_t)INT32_MAX) {
+    size_t temp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)q, 0, 19, st);
+    const size_t b4 = ((size_t)q * 4 + 255) & ~(size_t)255, bp = sizeof(double) * 6 * PK_BLOCKS;
+    if (cudaMallocAsync(&sbuf, 4 * b4 + bp + temp, st) != cudaSuccess) {
+      cudaFreeAsync(ptab, st);
+      set_error("fif_pc_fim: cudaMallocAsync (pose order) failed");
+      return FIF_ERR_CUDA;
+    }
+    uint32_t* keys = reinterpret_cast<uint32_t*>(sbuf);
+    uint32_t* keys2 = reinterpret_cast<uint32_t*>(sbuf + b4);
+    int32_t* idx = reinterpret_cast<int32_t*>(sbuf + 2 * b4);
+    perm = reinterpret_cast<int32_t*>(sbuf + 3 * b4);
+    double* part = reinterpret_cast<double*>(sbuf + 4 * b4);
+    k_pc_bbox<<<PK_BLOCKS, 256, 0, st>>>(d_t, q, part);
+    k_pc_keys<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(d_rot, d_t, q, part, PK_BLOCKS, keys, idx);
+    FIF_CHECK_LAUNCH("k_pc_keys");
+    cub::DeviceRadixSort::SortPairs(sbuf + 4 * b4 + bp, temp, keys, keys2, idx, perm, (int)q, 0, 19, st);
+  }
   if (d_mask)
     k_pc_fim<true><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2, d_out,
-                                                        d_mask);
+                                                        d_mask, perm);
   else
     k_pc_fim<false><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2,
-                                                         d_out, d_mask);
+                                                         d_out, d_mask, perm);
+  if (sbuf) cudaFreeAsync(sbuf, st);
   cudaFreeAsync(ptab, st);
   FIF_CHECK_LAUNCH("k_pc_fim");
   return FIF_OK;

@@ -67,3 +67,23 @@ def test_pc_border_and_edge_cases(oracle):
     assert np.all(F.exact_pose_fim_batch(R, t, np.zeros((0, 3)), cam) == 0)
     single = F.exact_pose_fim(F.Pose(R[0], t[0]), pts, cam)
     assert np.allclose(single, out[0], rtol=1e-12, atol=0)
+
+
+def test_pc_pose_order_is_invisible():
+    """Large batches run similar poses together (load balance); per-pose results and masks
+    are bit-identical to batches below the reordering threshold."""
+    from paper_2008_03324_b200 import scenes
+
+    w = scenes.config3(12000)
+    cam = F.PinholeCamera.from_fov()
+    dev = torch.device("cuda")
+    r = torch.tensor(w.rotations.reshape(-1, 9), device=dev)
+    t = torch.tensor(w.positions, device=dev)
+    p = torch.tensor(w.points[:5000], device=dev)
+    m_all = torch.zeros((12000, 5000), dtype=torch.uint8, device=dev)
+    o_all = F.exact_pose_fim_batch_device(r, t, p, cam, mask=m_all)
+    for s in range(0, 12000, 4000):
+        m = torch.zeros((4000, 5000), dtype=torch.uint8, device=dev)
+        o = F.exact_pose_fim_batch_device(r[s:s + 4000].contiguous(), t[s:s + 4000].contiguous(), p, cam, mask=m)
+        assert torch.equal(o, o_all[s:s + 4000])
+        assert torch.equal(m, m_all[s:s + 4000])
