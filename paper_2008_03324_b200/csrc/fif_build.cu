@@ -380,10 +380,12 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
   for (int s = 0; s < GT_G; ++s) {
     const int g = gi + s * tpv;
     const bool ok = worker && g < ns;
-    zx[s] = ok ? ax * zs[3 * g] : 0.0;
-    zy[s] = ok ? ax * zs[3 * g + 1] : 0.0;
-    zz[s] = ok ? ax * zs[3 * g + 2] : 0.0;
+    // exact power-of-two pre-scale for the two-op FP64 -> FP32 conversion below
+    zx[s] = ok ? ax * zs[3 * g] * kF32Bias : 0.0;
+    zy[s] = ok ? ax * zs[3 * g + 1] * kF32Bias : 0.0;
+    zz[s] = ok ? ax * zs[3 * g + 2] * kF32Bias : 0.0;
   }
+  const double bxs = bx * kF32Bias;
   DF acc[GT_G];
 #pragma unroll
   for (int s = 0; s < GT_G; ++s) acc[s].init();
@@ -435,10 +437,9 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
           const PairT pr = pv[j];
 #pragma unroll
           for (int s = 0; s < GT_G; ++s) {
-            // -k_s (u.z - cos a) log2(e), FP64.  + 2^-60 keeps the argument off exact
-            // zero (which the ALU conversion cannot represent); |x| is either 0 or
-            // >= ~1e-15 here, so the shift is below FP32 resolution of 2^x.
-            const float x = f64_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bx))) + 0x1p-60);
+            // -k_s (u.z - cos a) log2(e) in FP64 (zx..bxs carry the exact 2^-896
+            // pre-scale of f64s_to_f32_alu), converted to FP32 with two ALU ops
+            const float x = f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs))));
             const float vs = rcp_approx(1.0f + ex2_approx(x));
             part[s] = fmaf(pr.tr, vs, part[s]);
           }
