@@ -82,155 +82,158 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // 6x6 determinant (partial-pivot LU) and smallest eigenvalue (cyclic Jacobi), FP64.
-__device__ double det6(const double* a_in) {
-  double a[36];
-  for (int i = 0; i < 36; ++i) a[i] = a_in[i];
-  double det = 1.0;
-  for (int c = 0; c < 6; ++c) {
-    int p = c;
-    double best = fabs(a[6 * c + c]);
-    for (int r = c + 1; r < 6; ++r)
-      if (fabs(a[6 * r + c]) > best) { best = fabs(a[6 * r + c]); p = r; }
-    if (best == 0.0) return 0.0;
-    if (p != c) {
-      for (int k = 0; k < 6; ++k) { double t = a[6 * c + k]; a[6 * c + k] = a[6 * p + k]; a[6 * p + k] = t; }
-      det = -det;
-    }
-    double piv = a[6 * c + c];
-    det *= piv;
-    for (int r = c + 1; r < 6; ++r) {
-      double f = a[6 * r + c] / piv;
-      for (int k = c + 1; k < 6; ++k) a[6 * r + k] -= f * a[6 * c + k];
-    }
-  }
-  return det;
-}
-__device__ double lmin6(const double* a_in) {
-  double a[36];
-  for (int i = 0; i < 36; ++i) a[i] = a_in[i];
-  for (int sweep = 0; sweep < 64; ++sweep) {
-    double off = 0.0, tot = 0.0;
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) {
-        double v = a[6 * r + c] * a[6 * r + c];
-        tot += v;
-        if (r != c) off += v;
-      }
-    if (off <= 1e-30 * tot || off == 0.0) break;
-    for (int p = 0; p < 5; ++p)
-      for (int q = p + 1; q < 6; ++q) {
-        double apq = a[6 * p + q];
-        if (apq == 0.0) continue;
-        double theta = (a[6 * q + q] - a[6 * p + p]) / (2.0 * apq);
-        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
-        for (int k = 0; k < 6; ++k) {
-          double akp = a[6 * k + p], akq = a[6 * k + q];
-          a[6 * k + p] = cs * akp - sn * akq;
-          a[6 * k + q] = sn * akp + cs * akq;
-        }
-        for (int k = 0; k < 6; ++k) {
-          double apk = a[6 * p + k], aqk = a[6 * q + k];
-          a[6 * p + k] = cs * apk - sn * aqk;
-          a[6 * q + k] = sn * apk + cs * aqk;
-        }
-      }
-  }
-  double m = a[0];
-  for (int k = 1; k < 6; ++k) m = fmin(m, a[7 * k]);
-  return m;
-}
+// Every loop is fully unrolled with compile-time indices (row swaps and the pivot
+// permutation as selects), so the matrices stay in registers instead of local memory.
+// Arithmetic order is that of the straightforward loops (and of the oracle's).
+__host__ __device__ constexpr int pack_r(int x) { return x < 6 ? 0 : x < 11 ? 1 : x < 15 ? 2 : x < 18 ? 3 : x < 20 ? 4 : 5; }
+__host__ __device__ constexpr int pack_c(int x) { return pack_r(x) + x - (pack_r(x) * 6 - pack_r(x) * (pack_r(x) - 1) / 2); }
 
-// det6 plus F^-1 from the same LU (multipliers kept below the diagonal, rows
-// swapped whole, so P A = L U); returns det (identical to det6) and ok = false
-// for a singular matrix (inv untouched).
-__device__ double det6_inv(const double* a_in, double* inv, bool& ok) {
-  double a[36];
+// LU with partial pivoting (rows swapped whole, multipliers kept below the diagonal so
+// P A = L U); returns det, or 0 with ok = false for a singular matrix.  INV: F^-1.
+template <bool INV>
+__device__ __forceinline__ double det6_core(double (&a)[36], double (&inv)[36], bool& ok) {
   int perm[6];
-  for (int i = 0; i < 36; ++i) a[i] = a_in[i];
+#pragma unroll
   for (int i = 0; i < 6; ++i) perm[i] = i;
   double det = 1.0;
   ok = false;
+#pragma unroll
   for (int c = 0; c < 6; ++c) {
     int p = c;
     double best = fabs(a[6 * c + c]);
+#pragma unroll
     for (int r = c + 1; r < 6; ++r)
       if (fabs(a[6 * r + c]) > best) { best = fabs(a[6 * r + c]); p = r; }
     if (best == 0.0) return 0.0;
-    if (p != c) {
-      for (int k = 0; k < 6; ++k) { double t = a[6 * c + k]; a[6 * c + k] = a[6 * p + k]; a[6 * p + k] = t; }
-      int t = perm[c]; perm[c] = perm[p]; perm[p] = t;
-      det = -det;
-    }
-    double piv = a[6 * c + c];
-    det *= piv;
+#pragma unroll
     for (int r = c + 1; r < 6; ++r) {
-      double f = a[6 * r + c] / piv;
+      const bool sw = p == r;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const double t = a[6 * c + k];
+        a[6 * c + k] = sw ? a[6 * r + k] : t;
+        a[6 * r + k] = sw ? t : a[6 * r + k];
+      }
+      if (INV) {
+        const int tp = perm[c];
+        perm[c] = sw ? perm[r] : tp;
+        perm[r] = sw ? tp : perm[r];
+      }
+    }
+    if (p != c) det = -det;
+    const double piv = a[6 * c + c];
+    det *= piv;
+#pragma unroll
+    for (int r = c + 1; r < 6; ++r) {
+      const double f = a[6 * r + c] / piv;
+#pragma unroll
       for (int k = c + 1; k < 6; ++k) a[6 * r + k] -= f * a[6 * c + k];
-      a[6 * r + c] = f;
+      if (INV) a[6 * r + c] = f;
     }
   }
-  for (int j = 0; j < 6; ++j) {  // column j of A^-1: solve L U x = P e_j
-    double x[6];
-    for (int i = 0; i < 6; ++i) {
-      double y = perm[i] == j ? 1.0 : 0.0;
-      for (int k = 0; k < i; ++k) y -= a[6 * i + k] * x[k];
-      x[i] = y;
+  if (INV) {
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {  // column j of A^-1: solve L U x = P e_j
+      double x[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        double y = perm[i] == j ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k) y -= a[6 * i + k] * x[k];
+        x[i] = y;
+      }
+#pragma unroll
+      for (int i = 5; i >= 0; --i) {
+        double y = x[i];
+#pragma unroll
+        for (int k = i + 1; k < 6; ++k) y -= a[6 * i + k] * x[k];
+        x[i] = y / a[6 * i + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 6; ++i) inv[6 * i + j] = x[i];
     }
-    for (int i = 5; i >= 0; --i) {
-      double y = x[i];
-      for (int k = i + 1; k < 6; ++k) y -= a[6 * i + k] * x[k];
-      x[i] = y / a[6 * i + i];
-    }
-    for (int i = 0; i < 6; ++i) inv[6 * i + j] = x[i];
   }
   ok = true;
   return det;
 }
-// lmin6 plus the unit eigenvector of the smallest eigenvalue (Jacobi rotations
-// accumulated into V); the eigenvalue is identical to lmin6's.
-__device__ double lmin6_vec(const double* a_in, double* vec) {
-  double a[36], V[36];
-  for (int i = 0; i < 36; ++i) { a[i] = a_in[i]; V[i] = (i % 7 == 0) ? 1.0 : 0.0; }
+
+// cyclic Jacobi; VEC: accumulate the rotations and return the unit eigenvector of the
+// smallest eigenvalue in vec
+template <bool VEC>
+__device__ __forceinline__ double lmin6_core(double (&a)[36], double (&vec)[6]) {
+  double V[VEC ? 36 : 1];
+  if (VEC) {
+#pragma unroll
+    for (int i = 0; i < (VEC ? 36 : 1); ++i) V[i] = (i % 7 == 0) ? 1.0 : 0.0;
+  }
   for (int sweep = 0; sweep < 64; ++sweep) {
     double off = 0.0, tot = 0.0;
+#pragma unroll
     for (int r = 0; r < 6; ++r)
+#pragma unroll
       for (int c = 0; c < 6; ++c) {
-        double v = a[6 * r + c] * a[6 * r + c];
+        const double v = a[6 * r + c] * a[6 * r + c];
         tot += v;
         if (r != c) off += v;
       }
     if (off <= 1e-30 * tot || off == 0.0) break;
+#pragma unroll
     for (int p = 0; p < 5; ++p)
+#pragma unroll
       for (int q = p + 1; q < 6; ++q) {
-        double apq = a[6 * p + q];
-        if (apq == 0.0) continue;
-        double theta = (a[6 * q + q] - a[6 * p + p]) / (2.0 * apq);
-        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
-        for (int k = 0; k < 6; ++k) {
-          double akp = a[6 * k + p], akq = a[6 * k + q];
-          a[6 * k + p] = cs * akp - sn * akq;
-          a[6 * k + q] = sn * akp + cs * akq;
-          double vkp = V[6 * k + p], vkq = V[6 * k + q];
-          V[6 * k + p] = cs * vkp - sn * vkq;
-          V[6 * k + q] = sn * vkp + cs * vkq;
-        }
-        for (int k = 0; k < 6; ++k) {
-          double apk = a[6 * p + k], aqk = a[6 * q + k];
-          a[6 * p + k] = cs * apk - sn * aqk;
-          a[6 * q + k] = sn * apk + cs * aqk;
+        const double apq = a[6 * p + q];
+        if (apq != 0.0) {
+          const double theta = (a[6 * q + q] - a[6 * p + p]) / (2.0 * apq);
+          const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            const double akp = a[6 * k + p], akq = a[6 * k + q];
+            a[6 * k + p] = cs * akp - sn * akq;
+            a[6 * k + q] = sn * akp + cs * akq;
+            if (VEC) {
+              const double vkp = V[6 * k + p], vkq = V[6 * k + q];
+              V[6 * k + p] = cs * vkp - sn * vkq;
+              V[6 * k + q] = sn * vkp + cs * vkq;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            const double apk = a[6 * p + k], aqk = a[6 * q + k];
+            a[6 * p + k] = cs * apk - sn * aqk;
+            a[6 * q + k] = sn * apk + cs * aqk;
+          }
         }
       }
   }
   double m = a[0];
-  int im = 0;
-  for (int k = 1; k < 6; ++k)
-    if (a[7 * k] < m) { m = a[7 * k]; im = k; }
-  m = a[0];
+#pragma unroll
   for (int k = 1; k < 6; ++k) m = fmin(m, a[7 * k]);
-  for (int i = 0; i < 6; ++i) vec[i] = V[6 * i + im];
+  if (VEC) {
+    double best = a[0];
+    int im = 0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k)
+      if (a[7 * k] < best) { best = a[7 * k]; im = k; }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      double v = V[6 * i];
+#pragma unroll
+      for (int k = 1; k < 6; ++k) v = im == k ? V[6 * i + k] : v;
+      vec[i] = v;
+    }
+  }
   return m;
+}
+
+// unpack a corner's 21 packed entries into a symmetric 6x6 (registers)
+__device__ __forceinline__ void unpack21(const double* cf, double (&a)[36]) {
+#pragma unroll
+  for (int x = 0; x < 21; ++x) {
+    const double v = cf[x];
+    a[pack_r(x) * 6 + pack_c(x)] = v;
+    a[pack_c(x) * 6 + pack_r(x)] = v;
+  }
 }
 
 __constant__ int kPackR[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
@@ -779,45 +782,45 @@ k_query_info(int nv, const T* __restrict__ field,
       double mv_det = 0, mv_lmin = 0, gd[3] = {0, 0, 0}, gl[3] = {0, 0, 0};
       if (lane < NC) {
         const double* cf = cfim + lane * CF;
-        double a[36];
-        for (int x = 0; x < 21; ++x) {
-          const double v = cf[x];
-          a[kPackR[x] * 6 + kPackC[x]] = v;
-          a[kPackC[x] * 6 + kPackR[x]] = v;
-        }
         if (rows[q * 8 + lane] >= 0) {
           if (out.det) {
+            double a[36], inv[36];
+            unpack21(cf, a);
+            bool ok;
             if (MGRAD && out.det_grad) {
-              double inv[36];
-              bool ok;
-              mv_det = det6_inv(a, inv, ok);
+              mv_det = det6_core<true>(a, inv, ok);
               if (ok)
+#pragma unroll
                 for (int ax = 0; ax < 3; ++ax) {  // d det = det tr(F^-1 dF), dF packed symmetric
                   double t = 0.0;
+#pragma unroll
                   for (int x = 0; x < 21; ++x) {
-                    const int r = kPackR[x], c = kPackC[x];
+                    const int r = pack_r(x), c = pack_c(x);
                     t = fma(r == c ? inv[7 * r] : inv[6 * r + c] + inv[6 * c + r], cf[21 * (1 + ax) + x], t);
                   }
                   gd[ax] = mv_det * t;
                 }
             } else {
-              mv_det = det6(a);
+              mv_det = det6_core<false>(a, inv, ok);
             }
           }
           if (out.lmin) {
+            double a[36], v6[6];
+            unpack21(cf, a);
             if (MGRAD && out.lmin_grad) {
-              double v6[6];
-              mv_lmin = lmin6_vec(a, v6);
+              mv_lmin = lmin6_core<true>(a, v6);
+#pragma unroll
               for (int ax = 0; ax < 3; ++ax) {  // d lambda = v^T dF v
                 double t = 0.0;
+#pragma unroll
                 for (int x = 0; x < 21; ++x) {
-                  const int r = kPackR[x], c = kPackC[x];
+                  const int r = pack_r(x), c = pack_c(x);
                   t = fma(r == c ? v6[r] * v6[r] : 2.0 * v6[r] * v6[c], cf[21 * (1 + ax) + x], t);
                 }
                 gl[ax] = t;
               }
             } else {
-              mv_lmin = lmin6(a);
+              mv_lmin = lmin6_core<false>(a, v6);
             }
           }
         }
