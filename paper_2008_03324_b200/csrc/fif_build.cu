@@ -467,10 +467,9 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
 // for packed FP32x2 math: float4 {ux, uy, uz, e20}, then e0..e19 as 5 float4.
 // Phase B: thread (v, g) evaluates vs_g once per landmark and accumulates
 // vs_g * entries with FFMA2 (sm_100 packed FP32) into FP32 partials, flushed
-// every GI_FLUSH landmarks into FP64 accumulators (F2F on the MUFU pipe + DADD
+// every GI_FLUSH_TILES tiles into FP64 accumulators (F2F on the MUFU pipe + DADD
 // on the otherwise idle FP64 pipe).
 constexpr int GI_TILE = 32;
-constexpr int GI_FLUSH = 32;
 constexpr int GI_THREADS_MAX = 320;
 
 typedef unsigned long long f32x2;
@@ -1239,11 +1238,7 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
   const double LOG2E = 1.4426950408889634;
   const double ax = -model->k_s * LOG2E;
   const double bx = model->k_s * model->cos_alpha * LOG2E;
-  int vb = GI_THREADS_MAX / ns;
-  if (vb < 1) vb = 1;
   FIF_CHECK_ARG(ns <= GI_THREADS_MAX, "fif_build: N_s=%d exceeds %d", ns, GI_THREADS_MAX);
-  int threads = ((vb * ns + 31) / 32) * 32;
-  unsigned blocks = (unsigned)((rows + vb - 1) / vb);
   if (trace) {
     const int tpv = (ns + GT_G - 1) / GT_G;
     int vbt = GT_THREADS / tpv;
