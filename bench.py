@@ -318,6 +318,8 @@ def run_ours(args, rank, world, local):
         thr = host_threads()
         cpu_v, sample = cpu_gp_info_rate(w2.points, grid.centers(), model, args.cpu_seconds, thr)
         line["cpu_baseline"] = {"value": cpu_v, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample}
+        v1, s1 = cpu_gp_info_rate(w2.points, grid.centers(), model, min(4.0, args.cpu_seconds / 3), 1)
+        line["cpu_baseline"]["single_thread"] = {"value": v1, "unit": UNIT, "sample": s1}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
