@@ -73,3 +73,119 @@ def build_sharded(points, config, model, factor_kind: str, sigma: float = 1.0, d
         rows64, rows32 = row_builder(pts, v0, v1)
     full = gather_slabs(rows64, config.voxel_count) if replicate else None
     return v0, v1, rows64, rows32, full
+
+
+# ── slab-routed queries (fields larger than one GPU's HBM) ─────────────────
+# each rank keeps the z-planes it owns plus a one-plane halo (the upper
+# trilinear corner), queries are routed to the owner of their base z-index with an
+# all-to-all of (pose, id) and the results come back the same way.  The owner queries
+# its slab through a slots map over the GLOBAL grid, so corner lookup, weights and
+# status use the full grid's geometry and every result is bit-identical to a query on
+# the unsharded field.
+
+QUERY_WIDTHS = {"trace": 1, "trace_grad": 6, "fim": 36, "fim_grad": 216, "det": 1, "det_grad": 6, "lmin": 1,
+                "lmin_grad": 6, "status": 1}
+
+
+def plane_range(nz: int, world: int, rank: int) -> tuple[int, int]:
+    """z-planes [z0, z1) owned by `rank` (plane-aligned split for routed queries)."""
+    return slab_range(nz, world, rank)
+
+
+def slab_rows_range(config, world: int, rank: int) -> tuple[int, int, int, int]:
+    """(z0, z1, v_begin, v_end): owned planes and the internal z-major row range of the
+    owned planes plus the one-plane halo above them."""
+    nx, ny, nz = (int(d) for d in config.dims)
+    z0, z1 = plane_range(nz, world, rank)
+    zh = min(z1 + 1, nz)
+    return z0, z1, z0 * nx * ny, zh * nx * ny
+
+
+def query_owners(positions: np.ndarray, config, world: int, trilinear: bool) -> np.ndarray:
+    """Owner rank of each query: the rank whose planes hold its base z-index (trilinear:
+    floor((z - o_z)/vs - 0.5), so both corner planes are on the owner; nearest:
+    floor((z - o_z)/vs)); out-of-field queries go to the nearest plane's owner, which
+    reports the out-of-field status."""
+    nz = int(config.dims[2])
+    g = (np.asarray(positions, dtype=np.float64)[:, 2] - config.origin[2]) / config.voxel_size
+    if trilinear:
+        g = g - 0.5
+    bz = np.clip(np.floor(g), 0, max(nz - (2 if trilinear else 1), 0)).astype(np.int64)
+    starts = np.array([plane_range(nz, world, r)[0] for r in range(world)])
+    return np.searchsorted(starts, bz, side="right") - 1
+
+
+def route_queries(positions, axes, config, trilinear: bool, query_fn, outputs) -> dict:
+    """Run this rank's queries on their owners.  `query_fn(pos (n,3), axes (n,3)) ->
+    {name: array (n, width)}` answers queries against this rank's slab; `outputs` names
+    the entries of QUERY_WIDTHS wanted.  Returns {name: (Q, width) float64 array} in the
+    caller's order.  Collectives: two all_to_all_single (requests, results) + sizes."""
+    world = dist.get_world_size()
+    pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+    ax = np.ascontiguousarray(axes, dtype=np.float64).reshape(-1, 3)
+    owner = query_owners(pos, config, world, trilinear)
+    order = np.argsort(owner, kind="stable")
+    send_counts = np.bincount(owner, minlength=world)
+    sc = torch.tensor(send_counts, dtype=torch.int64)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc)
+    recv_counts = rc.numpy()
+    req = torch.from_numpy(np.concatenate([pos[order], ax[order]], axis=1).reshape(-1))
+    got = torch.empty(int(recv_counts.sum()) * 6, dtype=torch.float64)
+    dist.all_to_all_single(got, req, output_split_sizes=[int(c) * 6 for c in recv_counts],
+                           input_split_sizes=[int(c) * 6 for c in send_counts])
+    got = got.numpy().reshape(-1, 6)
+    names = [n for n in QUERY_WIDTHS if n in outputs or n == "status"]
+    width = sum(QUERY_WIDTHS[n] for n in names)
+    res = query_fn(got[:, :3], got[:, 3:]) if got.shape[0] else {n: np.zeros((0, QUERY_WIDTHS[n])) for n in names}
+    packed = np.concatenate([np.asarray(res[n], dtype=np.float64).reshape(got.shape[0], -1) for n in names], axis=1) \
+        if got.shape[0] else np.zeros((0, width))
+    back = torch.empty(pos.shape[0] * width, dtype=torch.float64)
+    dist.all_to_all_single(back, torch.from_numpy(np.ascontiguousarray(packed).reshape(-1)),
+                           output_split_sizes=[int(c) * width for c in send_counts],
+                           input_split_sizes=[int(c) * width for c in recv_counts])
+    back = back.numpy().reshape(-1, width)
+    out = np.empty_like(back)
+    out[order] = back
+    result, col = {}, 0
+    for n in names:
+        result[n] = out[:, col:col + QUERY_WIDTHS[n]]
+        col += QUERY_WIDTHS[n]
+    return result
+
+
+def build_slab_field(points, config, model, factor_kind: str, sigma: float = 1.0, device=None):
+    """This rank's slab of a z-sharded field (owned planes + one-plane halo) as a device
+    Field whose slots map the GLOBAL grid (voxels of other ranks read as absent)."""
+    from .field import Field, _grid_of, build_rows
+    from .visibility import model_from_reference
+
+    config = _grid_of(config)
+    model = model_from_reference(model)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    pts = broadcast_points(points if rank == 0 else None, device)
+    _, _, v0, v1 = slab_rows_range(config, world, rank)
+    rows64, rows32 = build_rows(pts, model, factor_kind == "trace", sigma, device, grid=config, v_begin=v0, v_end=v1)
+    occ3 = config.index3_of_internal(np.arange(v0, v1)).astype(np.int32)
+    return Field(config, model, factor_kind, sigma, rows64, rows32, occ3, dense=False)
+
+
+def query_slab_field(slab_field, positions, axes, mode: str = "trilinear", outputs=("trace", "full"),
+                     grad: bool = False) -> dict:
+    """Slab-routed query (see route_queries) answered on each owner's device Field."""
+    outs = set(outputs)
+    names = {"trace"} if "trace" in outs else set()
+    if "full" in outs:
+        names.add("fim")
+    names |= outs & {"det", "lmin"}
+    if grad:
+        names |= {n + "_grad" for n in list(names)}
+    dev = slab_field.device
+
+    def fn(p, a):
+        r = slab_field.query_device(torch.from_numpy(np.ascontiguousarray(p)).to(dev),
+                                    torch.from_numpy(np.ascontiguousarray(a)).to(dev), mode, trace="trace" in outs,
+                                    full="full" in outs, det="det" in outs, lmin="lmin" in outs, grad=grad)
+        return {k: v.reshape(v.shape[0], -1).double().cpu().numpy() for k, v in r.items()}
+
+    return route_queries(positions, axes, slab_field.config, mode == "trilinear", fn, names)

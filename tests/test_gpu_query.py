@@ -320,3 +320,37 @@ def test_very_large_batch_is_sliced(g_small, models, small_grid):
         small = f.query_device(pos[sl].contiguous(), ax[sl].contiguous(), "trilinear", trace=True, full=True, grad=True)
         for k in ("trace", "trace_grad", "fim", "fim_grad", "status"):
             assert torch.equal(big[k][sl], small[k]), k
+
+
+def test_slab_fields_answer_their_queries_bit_exactly(models):
+    """The device side of slab-routed queries (parallel.py): a rank's slab Field (owned
+    z-planes + one halo plane, slots over the global grid) answers the queries routed to
+    it exactly like the full field."""
+    from paper_2008_03324_b200 import field as FDm
+    from paper_2008_03324_b200.parallel import query_owners, slab_rows_range
+
+    rng = np.random.default_rng(21)
+    pts = rng.uniform([-3, -3, 0], [3, 3, 3], size=(400, 3))
+    grid = F.GridConfig(np.array([-1.0, -1.0, 0.0]), 0.5, np.array([5, 4, 9]))
+    m = models["gp30"]
+    full = F.Field.build(pts, grid, m, "info")
+    dev = torch.device("cuda")
+    pts_dev = torch.tensor(pts, device=dev)
+    c = grid.centers()
+    pos = rng.uniform(c[0] - 0.3, c[-1] + 0.3, size=(300, 3))
+    ax = np.ascontiguousarray(np.stack([F.random_rotation(rng) for _ in range(300)])[:, :, 2])
+    for world in (2, 3):
+        for mode in ("trilinear", "nearest"):
+            owner = query_owners(pos, grid, world, mode == "trilinear")
+            for rank in range(world):
+                _, _, v0, v1 = slab_rows_range(grid, world, rank)
+                s64, s32 = FDm.build_rows(pts_dev, m, False, 1.0, dev, grid=grid, v_begin=v0, v_end=v1)
+                occ3 = grid.index3_of_internal(np.arange(v0, v1)).astype(np.int32)
+                slab = FDm.Field(grid, m, "info", 1.0, s64, s32, occ3, dense=False)
+                sel = owner == rank
+                p = torch.tensor(pos[sel], device=dev)
+                a = torch.tensor(ax[sel], device=dev)
+                got = slab.query_device(p, a, mode, trace=True, full=True, grad=True)
+                ref = full.query_device(p, a, mode, trace=True, full=True, grad=True)
+                for k in ("trace", "trace_grad", "fim", "fim_grad", "status"):
+                    assert torch.equal(got[k], ref[k]), (world, mode, rank, k)
