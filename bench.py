@@ -290,7 +290,7 @@ def run_ours(args, rank, world, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32+f64acc",
+        "vs_baseline": None, "dtype": "f32 (FP16 hi+lo tensor products, FP32 accumulate) + f64 accumulation",
         "data": "synthetic: seeded config-2 room landmarks (BASELINE configs[1]); no dataset",
         "config": {"workload": f"config2: GP-{model.n_v} info PIF build, {N} room landmarks x 81x81x21 grid @0.25 m",
                    "global_batch": int(pairs_total), "parallelism": f"z-slab x{world}",
