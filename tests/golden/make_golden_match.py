@@ -48,3 +48,15 @@ for mname, model in (("quad", quad), ("gp30", gp30)):
         arrays[f"factors_{mname}_{kind}"] = f.factors
 np.savez_compressed(os.path.join(OUT, "match.npz"), **arrays)
 print("wrote match.npz", {k: np.asarray(v).shape for k, v in arrays.items()})
+
+# ── FIF1 files written by the reference (field.py:525-560) for interop tests ──
+fif_dir = os.path.join(OUT, "fif1")
+os.makedirs(fif_dir, exist_ok=True)
+cfg2 = GridConfig(np.array([-1.0, -1.0, 0.0]), 0.5, np.array([4, 3, 3]))
+pts2 = rng.uniform([-2, -2, 0], [2, 2, 2], size=(60, 3))
+fifield.build(pts2, cfg2, quad, "info").serialize(os.path.join(fif_dir, "quad_info.fif"))
+fifield.build(pts2, cfg2, gp30, "trace").serialize(os.path.join(fif_dir, "gp30_trace.fif"))
+fifield.build(F_scene := Scene(pts2, vd[:60]), cfg2, gp30, "info",
+              matchability=Matchability(d_near=0.2, d_far=1.2)).serialize(os.path.join(fif_dir, "gp30_info_masked.fif"))
+np.savez_compressed(os.path.join(fif_dir, "inputs.npz"), points=pts2, view_dirs=vd[:60])
+print("wrote fif1/*.fif")

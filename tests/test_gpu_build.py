@@ -229,3 +229,34 @@ def test_gp150_build(oracle, kind, gp_info_kernel):
     mine = reference_order(f)
     err = trace_rel_l2(mine, ref) if kind == "trace" else info_rel_fro(mine, ref)
     assert err.max() <= (TRACE_TOL if kind == "trace" else INFO_TOL)
+
+
+def test_fif1_interop_with_reference_files(tmp_path, g_models):
+    """FIF1 files written by the reference's Field.serialize (tests/golden/fif1) load here,
+    and an EXACT-mode quad build serialises byte-for-byte like the reference's."""
+    import os
+
+    from tests._helpers import models_from_golden
+
+    d = os.path.join(os.path.dirname(__file__), "golden", "fif1")
+    inp = np.load(os.path.join(d, "inputs.npz"))
+    cfg = F.GridConfig(np.array([-1.0, -1.0, 0.0]), 0.5, np.array([4, 3, 3]))
+    m = models_from_golden(g_models)
+    # quad info: bit-exact build -> identical bytes
+    ours = F.Field.build(inp["points"], cfg, m["quad"], "info", exact=True)
+    p = tmp_path / "q.fif"
+    ours.serialize(p)
+    assert p.read_bytes() == open(os.path.join(d, "quad_info.fif"), "rb").read()
+    # the reference's files deserialise to the same rows the build produces
+    for name, model, kind in (("quad_info", m["quad"], "info"), ("gp30_trace", m["gp30"], "trace")):
+        g = F.Field.deserialize(os.path.join(d, name + ".fif"))
+        assert g.factor_kind == kind and g.rows == cfg.voxel_count
+        ref = F.Field.build(inp["points"], cfg, model, kind, exact=isinstance(model, F.QuadraticVisibility))
+        order = np.argsort(cfg.linear_index(ref.occupied_index3))
+        a, b = g.factors, ref.factors[order]
+        assert np.abs(a - b).max() <= (0.0 if kind == "info" else 1e-5 * np.abs(b).max())
+    # masked GP info (sparse rows in the reference's order) loads and queries
+    g = F.Field.deserialize(os.path.join(d, "gp30_info_masked.fif"))
+    assert g.factor_kind == "info" and 0 < g.rows <= cfg.voxel_count
+    q = g.query_batch(cfg.centers()[:5], axes=np.tile([0.0, 0.0, 1.0], (5, 1)), outputs=("trace",), mode="nearest")
+    assert torch.isfinite(q["trace"]).all()
