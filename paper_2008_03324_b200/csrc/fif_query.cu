@@ -544,6 +544,146 @@ __host__ __device__ constexpr uint32_t qw_warp_bytes() {
   return 64 + STAGES * (NC * QWShape<T>::CAP + QWShape<T>::KC * 32) + 8 * 8 * qw_cf<METRIC, MGRAD>();
 }
 
+// Outputs of one query from its per-corner contractions G_c (lane = packed entry),
+// the blended rotation derivatives R (or per-corner H for metric gradients), the
+// corner weights (lane c holds corner c's {w, dw} in my_cw) and r_lane (row of corner
+// `lane`, -1 = absent).  Shared by the streaming and the small-batch kernels.
+template <int NC, bool GRAD, bool METRIC, bool MGRAD>
+__device__ __forceinline__ void emit_outputs(const QueryOut& out, int64_t qo, int st, int lane, bool on,
+                                             const double (&w)[NC], const double (&G)[NC], double R0, double R1,
+                                             double R2, const double (&H)[MGRAD ? NC : 1][3], double4 my_cw,
+                                             double* cfim, const double* __restrict__ axes, int32_t r_lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr uint32_t CF = qw_cf<METRIC, MGRAD>();
+  if (MGRAD) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      R0 = fma(w[c], H[c][0], R0);
+      R1 = fma(w[c], H[c][1], R1);
+      R2 = fma(w[c], H[c][2], R2);
+      if (on) {
+        cfim[c * CF + 21 + lane] = H[c][0];
+        cfim[c * CF + 42 + lane] = H[c][1];
+        cfim[c * CF + 63 + lane] = H[c][2];
+      }
+    }
+  }
+  double val = 0, pgx = 0, pgy = 0, pgz = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    val = fma(w[c], G[c], val);
+    if (GRAD) {
+      pgx = fma(__shfl_sync(FULL, my_cw.y, c), G[c], pgx);
+      pgy = fma(__shfl_sync(FULL, my_cw.z, c), G[c], pgy);
+      pgz = fma(__shfl_sync(FULL, my_cw.w, c), G[c], pgz);
+    }
+    if (METRIC && on) cfim[c * CF + lane] = G[c];
+  }
+  const double zx = axes[3 * qo], zy = axes[3 * qo + 1], zz = axes[3 * qo + 2];
+  const double tgx = zy * R2 - zz * R1, tgy = zz * R0 - zx * R2, tgz = zx * R1 - zy * R0;  // z x d/dz
+  if (out.fim && on) {
+    const int pr = kPackR[lane], pc = kPackC[lane];
+    out.fim[qo * 36 + pr * 6 + pc] = val;
+    out.fim[qo * 36 + pc * 6 + pr] = val;
+  }
+  if (GRAD && out.fim_grad && on) {
+    const int pr = kPackR[lane], pc = kPackC[lane];
+    const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+      out.fim_grad[qo * 216 + d * 36 + pr * 6 + pc] = g6[d];
+      out.fim_grad[qo * 216 + d * 36 + pc * 6 + pr] = g6[d];
+    }
+  }
+  if (out.trace || (GRAD && out.trace_grad)) {
+    const bool dg = on && kIsDiag[lane];
+    const double tv = warp_sum(dg ? val : 0.0);
+    if (out.trace && lane == 0) out.trace[qo] = tv;
+    if (GRAD && out.trace_grad) {
+      const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
+#pragma unroll
+      for (int d = 0; d < 6; ++d) {
+        const double sgl = warp_sum(dg ? g6[d] : 0.0);
+        if (lane == d) out.trace_grad[qo * 6 + d] = sgl;
+      }
+    }
+  }
+  if (METRIC) {
+    __syncwarp();
+    double mv_det = 0, mv_lmin = 0, gd[3] = {0, 0, 0}, gl[3] = {0, 0, 0};
+    if (lane < NC) {
+      const double* cf = cfim + lane * CF;
+      if (r_lane >= 0) {
+        if (out.det) {
+          double a[36], inv[36];
+          unpack21(cf, a);
+          bool ok;
+          if (MGRAD && out.det_grad) {
+            mv_det = det6_core<true>(a, inv, ok);
+            if (ok)
+#pragma unroll
+              for (int ax = 0; ax < 3; ++ax) {  // d det = det tr(F^-1 dF), dF packed symmetric
+                double t = 0.0;
+#pragma unroll
+                for (int x = 0; x < 21; ++x) {
+                  const int r = pack_r(x), c = pack_c(x);
+                  t = fma(r == c ? inv[7 * r] : inv[6 * r + c] + inv[6 * c + r], cf[21 * (1 + ax) + x], t);
+                }
+                gd[ax] = mv_det * t;
+              }
+          } else {
+            mv_det = det6_core<false>(a, inv, ok);
+          }
+        }
+        if (out.lmin) {
+          double a[36], v6[6];
+          unpack21(cf, a);
+          if (MGRAD && out.lmin_grad) {
+            mv_lmin = lmin6_core<true>(a, v6);
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {  // d lambda = v^T dF v
+              double t = 0.0;
+#pragma unroll
+              for (int x = 0; x < 21; ++x) {
+                const int r = pack_r(x), c = pack_c(x);
+                t = fma(r == c ? v6[r] * v6[r] : 2.0 * v6[r] * v6[c], cf[21 * (1 + ax) + x], t);
+              }
+              gl[ax] = t;
+            }
+          } else {
+            mv_lmin = lmin6_core<false>(a, v6);
+          }
+        }
+      }
+    }
+    double mdet = 0, mlmin = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double dd = __shfl_sync(0xffffffffu, mv_det, c), ll = __shfl_sync(0xffffffffu, mv_lmin, c);
+      if (w[c] != 0.0) {
+        mdet = fma(w[c], dd, mdet);
+        mlmin = fma(w[c], ll, mlmin);
+      }
+    }
+    if (lane == 0) {
+      if (out.det) out.det[qo] = mdet;
+      if (out.lmin) out.lmin[qo] = mlmin;
+    }
+    if (MGRAD) {
+      // lane c < NC holds its corner's (w, dw) in my_cw; other lanes hold zeros
+      auto blend_grad = [&](double val_c, const double (&gz)[3], double* dst) {
+        const double tx = warp_sum(my_cw.y * val_c), ty = warp_sum(my_cw.z * val_c), tz = warp_sum(my_cw.w * val_c);
+        const double zxg = warp_sum(my_cw.x * gz[0]), zyg = warp_sum(my_cw.x * gz[1]), zzg = warp_sum(my_cw.x * gz[2]);
+        const double g6[6] = {tx, ty, tz, zy * zzg - zz * zyg, zz * zxg - zx * zzg, zx * zyg - zy * zxg};
+        if (lane < 6) dst[qo * 6 + lane] = g6[lane];
+      };
+      if (out.det_grad) blend_grad(mv_det, gd, out.det_grad);
+      if (out.lmin_grad) blend_grad(mv_lmin, gl, out.lmin_grad);
+    }
+  }
+  if (out.status && lane == 0) out.status[qo] = (uint8_t)st;
+}
+
 template <typename T, int NC, int STAGES, bool GRAD, bool METRIC, bool MGRAD>
 __global__ void __launch_bounds__(qw_wpb(STAGES) * 32, STAGES == 2 ? 3 : (STAGES == 3 ? 2 : 3))
 k_query_info(int nv, const T* __restrict__ field,
@@ -642,6 +782,7 @@ k_query_info(int nv, const T* __restrict__ field,
       G[c] = 0.0;
     }
     const double4 my_cw = c_cw;
+    const int32_t my_r = c_r;  // row of corner `lane` (lanes < NC)
     // prefetch the next query's metadata
     c_r = row_of(i + 1);
     if (i + 1 < nmine) {
@@ -724,133 +865,7 @@ k_query_info(int nv, const T* __restrict__ field,
       if (out.status && lane == 0) out.status[qo] = (uint8_t)st;
       continue;
     }
-    if (MGRAD) {
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        R0 = fma(w[c], H[c][0], R0);
-        R1 = fma(w[c], H[c][1], R1);
-        R2 = fma(w[c], H[c][2], R2);
-        if (on) {
-          cfim[c * CF + 21 + lane] = H[c][0];
-          cfim[c * CF + 42 + lane] = H[c][1];
-          cfim[c * CF + 63 + lane] = H[c][2];
-        }
-      }
-    }
-    double val = 0, pgx = 0, pgy = 0, pgz = 0;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      val = fma(w[c], G[c], val);
-      if (GRAD) {
-        pgx = fma(__shfl_sync(FULL, my_cw.y, c), G[c], pgx);
-        pgy = fma(__shfl_sync(FULL, my_cw.z, c), G[c], pgy);
-        pgz = fma(__shfl_sync(FULL, my_cw.w, c), G[c], pgz);
-      }
-      if (METRIC && on) cfim[c * CF + lane] = G[c];
-    }
-    const double zx = axes[3 * qo], zy = axes[3 * qo + 1], zz = axes[3 * qo + 2];
-    const double tgx = zy * R2 - zz * R1, tgy = zz * R0 - zx * R2, tgz = zx * R1 - zy * R0;  // z x d/dz
-    if (out.fim && on) {
-      const int pr = kPackR[lane], pc = kPackC[lane];
-      out.fim[qo * 36 + pr * 6 + pc] = val;
-      out.fim[qo * 36 + pc * 6 + pr] = val;
-    }
-    if (GRAD && out.fim_grad && on) {
-      const int pr = kPackR[lane], pc = kPackC[lane];
-      const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
-#pragma unroll
-      for (int d = 0; d < 6; ++d) {
-        out.fim_grad[qo * 216 + d * 36 + pr * 6 + pc] = g6[d];
-        out.fim_grad[qo * 216 + d * 36 + pc * 6 + pr] = g6[d];
-      }
-    }
-    if (out.trace || (GRAD && out.trace_grad)) {
-      const bool dg = on && kIsDiag[lane];
-      const double tv = warp_sum(dg ? val : 0.0);
-      if (out.trace && lane == 0) out.trace[qo] = tv;
-      if (GRAD && out.trace_grad) {
-        const double g6[6] = {pgx, pgy, pgz, tgx, tgy, tgz};
-#pragma unroll
-        for (int d = 0; d < 6; ++d) {
-          const double sgl = warp_sum(dg ? g6[d] : 0.0);
-          if (lane == d) out.trace_grad[qo * 6 + d] = sgl;
-        }
-      }
-    }
-    if (METRIC) {
-      __syncwarp();
-      double mv_det = 0, mv_lmin = 0, gd[3] = {0, 0, 0}, gl[3] = {0, 0, 0};
-      if (lane < NC) {
-        const double* cf = cfim + lane * CF;
-        if (rows[q * 8 + lane] >= 0) {
-          if (out.det) {
-            double a[36], inv[36];
-            unpack21(cf, a);
-            bool ok;
-            if (MGRAD && out.det_grad) {
-              mv_det = det6_core<true>(a, inv, ok);
-              if (ok)
-#pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {  // d det = det tr(F^-1 dF), dF packed symmetric
-                  double t = 0.0;
-#pragma unroll
-                  for (int x = 0; x < 21; ++x) {
-                    const int r = pack_r(x), c = pack_c(x);
-                    t = fma(r == c ? inv[7 * r] : inv[6 * r + c] + inv[6 * c + r], cf[21 * (1 + ax) + x], t);
-                  }
-                  gd[ax] = mv_det * t;
-                }
-            } else {
-              mv_det = det6_core<false>(a, inv, ok);
-            }
-          }
-          if (out.lmin) {
-            double a[36], v6[6];
-            unpack21(cf, a);
-            if (MGRAD && out.lmin_grad) {
-              mv_lmin = lmin6_core<true>(a, v6);
-#pragma unroll
-              for (int ax = 0; ax < 3; ++ax) {  // d lambda = v^T dF v
-                double t = 0.0;
-#pragma unroll
-                for (int x = 0; x < 21; ++x) {
-                  const int r = pack_r(x), c = pack_c(x);
-                  t = fma(r == c ? v6[r] * v6[r] : 2.0 * v6[r] * v6[c], cf[21 * (1 + ax) + x], t);
-                }
-                gl[ax] = t;
-              }
-            } else {
-              mv_lmin = lmin6_core<false>(a, v6);
-            }
-          }
-        }
-      }
-      double mdet = 0, mlmin = 0;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const double dd = __shfl_sync(0xffffffffu, mv_det, c), ll = __shfl_sync(0xffffffffu, mv_lmin, c);
-        if (w[c] != 0.0) {
-          mdet = fma(w[c], dd, mdet);
-          mlmin = fma(w[c], ll, mlmin);
-        }
-      }
-      if (lane == 0) {
-        if (out.det) out.det[qo] = mdet;
-        if (out.lmin) out.lmin[qo] = mlmin;
-      }
-      if (MGRAD) {
-        // lane c < NC holds its corner's (w, dw) in my_cw; other lanes hold zeros
-        auto blend_grad = [&](double val_c, const double (&gz)[3], double* dst) {
-          const double tx = warp_sum(my_cw.y * val_c), ty = warp_sum(my_cw.z * val_c), tz = warp_sum(my_cw.w * val_c);
-          const double zxg = warp_sum(my_cw.x * gz[0]), zyg = warp_sum(my_cw.x * gz[1]), zzg = warp_sum(my_cw.x * gz[2]);
-          const double g6[6] = {tx, ty, tz, zy * zzg - zz * zyg, zz * zxg - zx * zzg, zx * zyg - zy * zxg};
-          if (lane < 6) dst[qo * 6 + lane] = g6[lane];
-        };
-        if (out.det_grad) blend_grad(mv_det, gd, out.det_grad);
-        if (out.lmin_grad) blend_grad(mv_lmin, gl, out.lmin_grad);
-      }
-    }
-    if (out.status && lane == 0) out.status[qo] = (uint8_t)st;
+    emit_outputs<NC, GRAD, METRIC, MGRAD>(out, qo, st, lane, on, w, G, R0, R1, R2, H, my_cw, cfim, axes, my_r);
   }
 }
 
