@@ -132,6 +132,9 @@ __device__ __forceinline__ double det6_core(double (&a)[36], double (&inv)[36], 
     }
   }
   if (INV) {
+    double rd[6];  // one division per pivot, then multiplies in the 6 back substitutions
+#pragma unroll
+    for (int i = 0; i < 6; ++i) rd[i] = 1.0 / a[6 * i + i];
 #pragma unroll
     for (int j = 0; j < 6; ++j) {  // column j of A^-1: solve L U x = P e_j
       double x[6];
@@ -147,7 +150,7 @@ __device__ __forceinline__ double det6_core(double (&a)[36], double (&inv)[36], 
         double y = x[i];
 #pragma unroll
         for (int k = i + 1; k < 6; ++k) y -= a[6 * i + k] * x[k];
-        x[i] = y / a[6 * i + i];
+        x[i] = y * rd[i];
       }
 #pragma unroll
       for (int i = 0; i < 6; ++i) inv[6 * i + j] = x[i];
@@ -185,7 +188,7 @@ __device__ __forceinline__ double lmin6_core(double (&a)[36], double (&vec)[6]) 
         if (apq != 0.0) {
           const double theta = (a[6 * q + q] - a[6 * p + p]) / (2.0 * apq);
           const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+          const double cs = rsqrt(fma(t, t, 1.0)), sn = t * cs;
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
             const double akp = a[6 * k + p], akq = a[6 * k + q];
@@ -869,6 +872,245 @@ k_query_info(int nv, const T* __restrict__ field,
   }
 }
 
+// ───────────────────────── small batches: fused prep + k-split contraction ──
+// Latency-bound regime (a few hundred queries or fewer, e.g. planner state checks):
+// one CTA of QS_WARPS warps per query.  Thread 0 locates the corners and issues TMA
+// bulk copies of the (whole) corner rows at once; while they land, the CTA evaluates
+// v^r and omega = kinv v^r (+ derivatives) in FP64 into shared memory; then the warps
+// split the sample range, lanes over packed entries, and warp 0 reduces the partials
+// and emits the outputs (emit_outputs, as the streaming kernel).  GP fields, FP32 rows.
+constexpr int QS_WARPS = 8;
+
+template <int NC, bool GRAD, bool METRIC, bool MGRAD>
+__host__ __device__ constexpr int qs_np() {
+  return NC + (MGRAD ? 3 * NC : (GRAD ? 3 : 0));
+}
+
+template <int NC, bool GRAD, bool METRIC, bool MGRAD>
+__global__ void __launch_bounds__(QS_WARPS * 32) k_query_small(fif_model m, QueryGeom gm,
+                                                               const int32_t* __restrict__ slots,
+                                                               const double* __restrict__ pos,
+                                                               const double* __restrict__ axes, int64_t nq,
+                                                               int trilinear, const float* __restrict__ field,
+                                                               QueryOut out) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NP = qs_np<NC, GRAD, METRIC, MGRAD>();
+  constexpr uint32_t CF = qw_cf<METRIC, MGRAD>();
+  const int nv = m.n_v;
+  const int64_t rw = (int64_t)nv * 21;
+  const uint32_t rowcap = (uint32_t)((rw * 4 + 16 + 15) & ~15ll);
+  extern __shared__ __align__(128) unsigned char qsm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(qsm);
+  int* meta_i = reinterpret_cast<int*>(qsm + 16);               // [0] status, [1..8] rows, [9..16] offsets
+  double4* meta_cw = reinterpret_cast<double4*>(qsm + 128);      // [8]
+  unsigned char* rowbuf = qsm + 128 + 8 * sizeof(double4);       // [NC][rowcap]
+  double4* om = reinterpret_cast<double4*>(rowbuf + (size_t)NC * rowcap);  // [nv]
+  double* vr = reinterpret_cast<double*>(om + nv);                // [nv]
+  double* part = vr + ((nv + 1) & ~1);                            // [QS_WARPS][NP][32]
+  double* cfim = part + QS_WARPS * NP * 32;                       // METRIC: [8][CF]
+  double* kin = cfim + (METRIC ? 8 * CF : 0);                     // [nv][nv] kinv, landed once per CTA
+  uint64_t* kbar = bar + 1;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const uint32_t kbytes = (uint32_t)(nv * nv * sizeof(double));
+  const bool k_tma = (kbytes % 16u) == 0 && (reinterpret_cast<uintptr_t>(m.kinv) & 15) == 0;
+  if (t == 0) {
+    mbar_init(bar, 1);
+    mbar_init(kbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (k_tma) {
+      mbar_expect_tx(kbar, kbytes);
+      tma_bulk_g2s(kin, m.kinv, kbytes, kbar);
+    }
+  }
+  if (!k_tma)
+    for (int i = t; i < nv * nv; i += blockDim.x) kin[i] = m.kinv[i];
+  __syncthreads();
+  bool k_ready = !k_tma;
+  const double inv_l2 = 1.0 / (m.ell * m.ell);
+  uint32_t phase = 0;
+  for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    if (t == 0) {  // corners, weights, status (FP64, reference order) and the row copies
+      int nc = 0;
+      int64_t r[8];
+      double w[8], dw[8][3];
+      const int st = locate(gm, slots, pos[3 * q], pos[3 * q + 1], pos[3 * q + 2], trilinear != 0, nc, r, w, dw);
+      meta_i[0] = st;
+      uint32_t total = 0;
+      for (int c = 0; c < 8; ++c) {
+        const bool ok = st == FIF_STATUS_OK && c < nc;
+        const int32_t rr = ok ? (int32_t)r[c] : -1;
+        meta_i[1 + c] = rr;
+        meta_cw[c] = ok ? make_double4(w[c], dw[c][0], dw[c][1], dw[c][2]) : make_double4(0, 0, 0, 0);
+        if (c < NC && rr >= 0) {
+          const uintptr_t src = reinterpret_cast<uintptr_t>(field + (int64_t)rr * rw);
+          meta_i[9 + c] = (int)(src & 15);
+          total += (uint32_t)(((src + rw * 4 + 15) & ~(uintptr_t)15) - (src & ~(uintptr_t)15));
+        }
+      }
+      if (st == FIF_STATUS_OK && total > 0) {
+        mbar_expect_tx(bar, total);
+        for (int c = 0; c < NC; ++c) {
+          if (meta_i[1 + c] < 0) continue;
+          const uintptr_t src = reinterpret_cast<uintptr_t>(field + (int64_t)meta_i[1 + c] * rw);
+          const uintptr_t a0 = src & ~(uintptr_t)15;
+          tma_bulk_g2s(rowbuf + (size_t)c * rowcap, reinterpret_cast<const void*>(a0),
+                       (uint32_t)(((src + rw * 4 + 15) & ~(uintptr_t)15) - a0), bar);
+        }
+      }
+    }
+    __syncthreads();
+    const int st = meta_i[0];
+    if (st == FIF_STATUS_OK) {
+      bool any_copy = false;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) any_copy |= meta_i[1 + c] >= 0;
+      // absent corners (sparse fields) read as zero rows
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (meta_i[1 + c] < 0)
+          for (int i = t; i < (int)(rowcap / 4); i += blockDim.x) reinterpret_cast<float*>(rowbuf + (size_t)c * rowcap)[i] = 0.f;
+      // v^r (kernels.py:652-657), then omega = kinv v^r and its z-derivatives (FP64)
+      const double zx = axes[3 * q], zy = axes[3 * q + 1], zz = axes[3 * q + 2];
+      for (int g = t; g < nv; g += blockDim.x) {
+        const double c = __dadd_rn(__dadd_rn(__dmul_rn(zx, m.zs[3 * g]), __dmul_rn(zy, m.zs[3 * g + 1])),
+                                   __dmul_rn(zz, m.zs[3 * g + 2]));
+        vr[g] = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
+      }
+      if (!k_ready) {
+        mbar_wait(kbar, 0);
+        k_ready = true;
+      }
+      __syncthreads();
+      for (int k = t; k < nv; k += blockDim.x) {
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll 4
+        for (int g = 0; g < nv; ++g) {
+          const double tg = kin[g * nv + k] * vr[g];
+          a0 += tg;
+          a1 = fma(tg, m.zs[3 * g], a1);
+          a2 = fma(tg, m.zs[3 * g + 1], a2);
+          a3 = fma(tg, m.zs[3 * g + 2], a3);
+        }
+        om[k] = make_double4(a0, a1 * inv_l2, a2 * inv_l2, a3 * inv_l2);
+      }
+      __syncthreads();
+      if (any_copy) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+      }
+      // k-split contraction: warp w covers samples [k0, k1), lane = packed entry
+      const bool on = lane < 21;
+      const int e = on ? lane : 0;
+      const int kper = (nv + QS_WARPS - 1) / QS_WARPS;
+      const int k0 = warp * kper, k1 = min(nv, k0 + kper);
+      double w[NC], G[NC], H[MGRAD ? NC : 1][3];
+      const float* src[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        w[c] = meta_cw[c].x;
+        G[c] = 0.0;
+        H[MGRAD ? c : 0][0] = H[MGRAD ? c : 0][1] = H[MGRAD ? c : 0][2] = 0.0;
+        src[c] = reinterpret_cast<const float*>(rowbuf + (size_t)c * rowcap + (meta_i[1 + c] >= 0 ? meta_i[9 + c] : 0)) + e;
+      }
+      double R0 = 0, R1 = 0, R2 = 0;
+      if (on) {
+        for (int k = k0; k < k1; ++k) {
+          const double4 o = om[k];
+          double sv[NC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) sv[c] = (double)src[c][k * 21];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) G[c] = fma(o.x, sv[c], G[c]);
+          if (MGRAD) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              H[MGRAD ? c : 0][0] = fma(o.y, sv[c], H[MGRAD ? c : 0][0]);
+              H[MGRAD ? c : 0][1] = fma(o.z, sv[c], H[MGRAD ? c : 0][1]);
+              H[MGRAD ? c : 0][2] = fma(o.w, sv[c], H[MGRAD ? c : 0][2]);
+            }
+          } else if (GRAD) {
+            double bl = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) bl = fma(w[c], sv[c], bl);
+            R0 = fma(o.y, bl, R0);
+            R1 = fma(o.z, bl, R1);
+            R2 = fma(o.w, bl, R2);
+          }
+        }
+      }
+      double* pw = part + (size_t)warp * NP * 32;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) pw[c * 32 + lane] = G[c];
+      if (MGRAD) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) pw[(NC + 3 * c + a) * 32 + lane] = H[MGRAD ? c : 0][a];
+      } else if (GRAD) {
+        pw[NC * 32 + lane] = R0;
+        pw[(NC + 1) * 32 + lane] = R1;
+        pw[(NC + 2) * 32 + lane] = R2;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // reduce the warps' partials (fixed order), then the shared output emission
+#pragma unroll
+        for (int c = 0; c < NC; ++c) G[c] = 0.0;
+        R0 = R1 = R2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < (MGRAD ? NC : 1); ++c) H[c][0] = H[c][1] = H[c][2] = 0.0;
+        for (int ww = 0; ww < QS_WARPS; ++ww) {
+          const double* pp = part + (size_t)ww * NP * 32;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) G[c] += pp[c * 32 + lane];
+          if (MGRAD) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+              for (int a = 0; a < 3; ++a) H[MGRAD ? c : 0][a] += pp[(NC + 3 * c + a) * 32 + lane];
+          } else if (GRAD) {
+            R0 += pp[NC * 32 + lane];
+            R1 += pp[(NC + 1) * 32 + lane];
+            R2 += pp[(NC + 2) * 32 + lane];
+          }
+        }
+        const double4 my_cw = lane < NC ? meta_cw[lane] : make_double4(0, 0, 0, 0);
+        const int32_t r_lane = lane < NC ? meta_i[1 + lane] : -1;
+        emit_outputs<NC, GRAD, METRIC, MGRAD>(out, q, st, lane, on, w, G, R0, R1, R2, H, my_cw, cfim, axes,
+                                              r_lane);
+      }
+    } else if (warp == 0) {
+      if (out.fim) for (int i2 = lane; i2 < 36; i2 += 32) out.fim[q * 36 + i2] = 0.0;
+      if (out.fim_grad) for (int i2 = lane; i2 < 216; i2 += 32) out.fim_grad[q * 216 + i2] = 0.0;
+      if (lane == 0) {
+        if (out.trace) out.trace[q] = 0.0;
+        if (out.det) out.det[q] = 0.0;
+        if (out.lmin) out.lmin[q] = 0.0;
+      }
+      if (out.trace_grad && lane < 6) out.trace_grad[q * 6 + lane] = 0.0;
+      if (out.det_grad && lane < 6) out.det_grad[q * 6 + lane] = 0.0;
+      if (out.lmin_grad && lane < 6) out.lmin_grad[q * 6 + lane] = 0.0;
+      if (out.status && lane == 0) out.status[q] = (uint8_t)st;
+    }
+    __syncthreads();  // shared buffers are reused by the next query
+  }
+}
+
+template <int NC, bool GRAD, bool METRIC, bool MGRAD>
+static void launch_small(const fif_model& m, const QueryGeom& gm, const int32_t* slots, const double* pos,
+                         const double* axes, int64_t q, int trilinear, const float* field, const QueryOut& out,
+                         cudaStream_t st) {
+  auto kern = k_query_small<NC, GRAD, METRIC, MGRAD>;
+  const int nv = m.n_v;
+  const size_t rowcap = ((size_t)nv * 21 * 4 + 16 + 15) & ~(size_t)15;
+  const size_t smem = 128 + 8 * sizeof(double4) + NC * rowcap + sizeof(double4) * nv +
+                      sizeof(double) * (((nv + 1) & ~1) + QS_WARPS * qs_np<NC, GRAD, METRIC, MGRAD>() * 32 +
+                                        8 * qw_cf<METRIC, MGRAD>() + (size_t)nv * nv);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t cap = (int64_t)kSMs * 4;
+  kern<<<(unsigned)(q < cap ? q : cap), QS_WARPS * 32, smem, st>>>(m, gm, slots, pos, axes, q, trilinear, field, out);
+}
+
 // ───────────────────────── contraction: trace fields ────────────────────
 constexpr int QC_WARPS = 8;
 // Rows of n_v scalars: lanes stride over k, per-lane partial sums, warp reduction.
@@ -1106,6 +1348,26 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
   const bool metric = info && (out.det || out.lmin);
   const bool trilinear = mode == FIF_MODE_TRILINEAR;
   cudaStream_t st = (cudaStream_t)stream;
+  // small GP info batches (latency-bound): one fused kernel, one CTA per query
+  static const bool no_small = getenv("FIF_QUERY_NO_FUSED_SMALL") != nullptr;
+  if (info && model->kind == FIF_MODEL_GP && !(flags & FIF_Q_FIELD_F64) && q <= (int64_t)kSMs * 3 && !no_small &&
+      (size_t)nv * 21 * 4 * (trilinear ? 8 : 1) + (size_t)nv * nv * 8 <= 150 * 1024) {
+    const float* ff = reinterpret_cast<const float*>(d_field);
+    const int tri = trilinear ? 1 : 0;
+#define QSM(NC)                                                                                              \
+  do {                                                                                                       \
+    if (mgrad) launch_small<NC, true, true, true>(*model, gm, d_slots, d_positions, d_axes, q, tri, ff, out, st); \
+    else if (metric && grad) launch_small<NC, true, true, false>(*model, gm, d_slots, d_positions, d_axes, q, tri, ff, out, st); \
+    else if (metric) launch_small<NC, false, true, false>(*model, gm, d_slots, d_positions, d_axes, q, tri, ff, out, st); \
+    else if (grad) launch_small<NC, true, false, false>(*model, gm, d_slots, d_positions, d_axes, q, tri, ff, out, st); \
+    else launch_small<NC, false, false, false>(*model, gm, d_slots, d_positions, d_axes, q, tri, ff, out, st); \
+  } while (0)
+    if (trilinear) QSM(8);
+    else QSM(1);
+#undef QSM
+    FIF_CHECK_LAUNCH("k_query_small");
+    return FIF_OK;
+  }
   // stream-ordered scratch: status, rows, corner weights, rotation weights
   const size_t b_status = ((size_t)q + 255) & ~(size_t)255;
   const size_t b_rows = (size_t)q * 8 * sizeof(int32_t);
