@@ -354,3 +354,30 @@ def test_slab_fields_answer_their_queries_bit_exactly(models):
                 ref = full.query_device(p, a, mode, trace=True, full=True, grad=True)
                 for k in ("trace", "trace_grad", "fim", "fim_grad", "status"):
                     assert torch.equal(got[k], ref[k]), (world, mode, rank, k)
+
+
+@pytest.mark.parametrize("mode", ["trilinear", "nearest"])
+def test_streaming_and_fused_small_paths_agree(g_small, models, small_grid, mode):
+    """Batches above 444 queries take the streaming kernels (prep + TMA ring), smaller
+    GP batches the fused per-query kernel: the two agree (summation order only) for every
+    output, metrics and metric gradients included (this also covers the streaming metric
+    kernel variants, which the small-batch tests do not reach)."""
+    m = models["gp70"]
+    f = field_from_reference(small_grid, m, "info", g_small["factors_gp70_info"])
+    rng = np.random.default_rng(41)
+    c = small_grid.centers()
+    n = 900
+    pos = torch.tensor(rng.uniform(c[0] - 0.2, c[-1] + 0.2, size=(n, 3)), device="cuda")
+    ax = torch.nn.functional.normalize(torch.tensor(rng.standard_normal((n, 3)), device="cuda"), dim=1)
+    kw = dict(trace=True, full=True, det=True, lmin=True, grad=True)
+    big = f.query_device(pos, ax, mode, **kw)
+    for s in (0, 300, 600):
+        small = f.query_device(pos[s:s + 300].contiguous(), ax[s:s + 300].contiguous(), mode, **kw)
+        assert torch.equal(small["status"], big["status"][s:s + 300])
+        for k in ("trace", "trace_grad", "fim", "fim_grad", "det", "det_grad", "lmin", "lmin_grad"):
+            a, b = small[k].cpu().numpy(), big[k][s:s + 300].cpu().numpy()
+            scale = np.abs(b).reshape(b.shape[0], -1).max(axis=1) + 1e-300
+            err = np.abs(a - b).reshape(a.shape[0], -1).max(axis=1) / scale
+            # det / lambda_min amplify the entries' last-bit differences by the 6x6's condition
+            tol = 1e-6 if k.startswith(("det", "lmin")) else 1e-9
+            assert err.max() <= tol, (k, err.max())
