@@ -382,13 +382,17 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
 
 // QQ queries per CTA: 32 for streaming batches, 8 for small batches (more CTAs, so the
 // latency-bound prep spreads over more SMs)
-template <int QQ>
+// RPQ weight rows per query in an m8 tile: 4 (omega and its 3 z-derivatives) when
+// gradients are wanted, else 1 (8 queries per tile, a quarter of the DMMAs)
+template <int QQ, int RPQ>
 struct QDShape {
-  static constexpr int THREADS = QQ == 32 ? QD_THREADS : 128;
-  static constexpr int MT_PER_WARP = QQ / 2 / (THREADS / 32);
+  static constexpr int MTILES = QQ * RPQ / 8;
+  static constexpr int NWARPS = MTILES < 8 ? MTILES : 8;
+  static constexpr int THREADS = 32 * NWARPS;
+  static constexpr int MT_PER_WARP = MTILES / NWARPS;
 };
-template <int NT, int QQ>
-__global__ void __launch_bounds__(QDShape<QQ>::THREADS, 3) k_query_prep_gp(fif_model m, QueryGeom gm,
+template <int NT, int QQ, int RPQ>
+__global__ void __launch_bounds__(QDShape<QQ, RPQ>::THREADS, 3) k_query_prep_gp(fif_model m, QueryGeom gm,
                                                               const int32_t* __restrict__ slots,
                                                               const double* __restrict__ pos,
                                                               const double* __restrict__ axes, int64_t nq,
@@ -398,8 +402,9 @@ __global__ void __launch_bounds__(QDShape<QQ>::THREADS, 3) k_query_prep_gp(fif_m
                                                               const int32_t* __restrict__ perm) {
   extern __shared__ double smd[];
   constexpr int NP8 = 8 * NT, KS = NP8 / 4;
-  constexpr int MT_PER_WARP = QDShape<QQ>::MT_PER_WARP;
-  constexpr int NWARPS = QDShape<QQ>::THREADS / 32;
+  constexpr int MT_PER_WARP = QDShape<QQ, RPQ>::MT_PER_WARP;
+  constexpr int NWARPS = QDShape<QQ, RPQ>::NWARPS;
+  constexpr int QPM = 8 / RPQ;  // queries per m8 tile
   const int nv = m.n_v;
   // kinv row-major (stride nv) landed by one TMA bulk copy; rows nv..NP8-1 read by the
   // padded k-steps are zeroed (their A entries are zero too, and 0 x NaN would not be)
@@ -460,7 +465,7 @@ __global__ void __launch_bounds__(QDShape<QQ>::THREADS, 3) k_query_prep_gp(fif_m
   __syncthreads();
   const int warp = t >> 5, lane = t & 31;
   const int row = lane >> 2, tq = lane & 3;  // A/C row; A col = B row = tq
-  const int qq = row >> 2, a = row & 3;     // m8 row -> (query of the pair, weight row)
+  const int qq = row / RPQ, a = row % RPQ;  // m8 row -> (query of the tile, weight row)
   // each warp owns MT_PER_WARP m-tiles (2 queries each) and all NT n-tiles: every B
   // fragment load feeds MT_PER_WARP DMMAs, every A fragment NT DMMAs
   double c[MT_PER_WARP][NT][2];
@@ -474,12 +479,12 @@ __global__ void __launch_bounds__(QDShape<QQ>::THREADS, 3) k_query_prep_gp(fif_m
 #pragma unroll 1
   for (int ks = 0; ks < KS; ++ks) {
     const int g = 4 * ks + tq;
-    const double sg = sa[4 * g + a];
+    const double sg = RPQ == 1 ? 1.0 : sa[4 * g + a];
     double av[MT_PER_WARP];
 #pragma unroll
     for (int i = 0; i < MT_PER_WARP; ++i) {
-      const int qi = (warp + i * NWARPS) * 2 + qq;
-      av[i] = sv[qi * NP8 + g] * sg;
+      const int qi = (warp + i * NWARPS) * QPM + qq;
+      av[i] = RPQ == 1 ? sv[qi * NP8 + g] : sv[qi * NP8 + g] * sg;
     }
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -490,7 +495,7 @@ __global__ void __launch_bounds__(QDShape<QQ>::THREADS, 3) k_query_prep_gp(fif_m
   }
 #pragma unroll
   for (int i = 0; i < MT_PER_WARP; ++i) {
-    const int64_t q = q0 + (warp + i * NWARPS) * 2 + qq;
+    const int64_t q = q0 + (warp + i * NWARPS) * QPM + qq;
     if (q >= nq) continue;
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -501,13 +506,13 @@ __global__ void __launch_bounds__(QDShape<QQ>::THREADS, 3) k_query_prep_gp(fif_m
   }
 }
 
-template <int NT, int QQ>
+template <int NT, int QQ, int RPQ>
 static void launch_prep_gp(size_t smem, int64_t q, cudaStream_t st, const fif_model& m, const QueryGeom& gm,
                            const int32_t* slots, const double* pos, const double* axes, int trilinear,
                            uint8_t* status, int32_t* rows, double4* cw, double* wt, const int32_t* perm) {
-  auto kern = k_query_prep_gp<NT, QQ>;
+  auto kern = k_query_prep_gp<NT, QQ, RPQ>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<(unsigned)((q + QQ - 1) / QQ), QDShape<QQ>::THREADS, smem, st>>>(m, gm, slots, pos, axes, q, trilinear, status,
+  kern<<<(unsigned)((q + QQ - 1) / QQ), QDShape<QQ, RPQ>::THREADS, smem, st>>>(m, gm, slots, pos, axes, q, trilinear, status,
                                                                      rows, cw, wt, perm);
 }
 
@@ -1427,10 +1432,14 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
     switch (ntiles) {
 #define PG(NT)                                                                                                   \
   case NT:                                                                                                       \
-    if (small) launch_prep_gp<NT, 8>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows,  \
-                                     s_cw, wtd, perm);                                                           \
-    else launch_prep_gp<NT, 32>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows, s_cw, \
-                                wtd, perm);                                                                      \
+    if (small && grad) launch_prep_gp<NT, 8, 4>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, \
+                                                s_rows, s_cw, wtd, perm);                                        \
+    else if (small) launch_prep_gp<NT, 8, 1>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status,   \
+                                             s_rows, s_cw, wtd, perm);                                           \
+    else if (grad) launch_prep_gp<NT, 32, 4>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status,   \
+                                             s_rows, s_cw, wtd, perm);                                           \
+    else launch_prep_gp<NT, 32, 1>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows,     \
+                                   s_cw, wtd, perm);                                                             \
     break;
       PG(1) PG(2) PG(3) PG(4) PG(5) PG(6) PG(7) PG(8) PG(9) PG(10) PG(11) PG(12)
 #undef PG
