@@ -344,6 +344,13 @@ constexpr int GT_THREADS = 256;
 #ifndef GT_MINB
 #define GT_MINB 3
 #endif
+// sigmoid reciprocal: 0 MUFU rcp (default), 1 scalar FMA-pipe Newton, 2 packed (FFMA2)
+// Newton.  Measured on config 2 (tools/sweep_build.sh): 113.7 / 133.5 / 140.3 ms -- moving
+// the reciprocal off MUFU costs more issue slots and latency than the MUFU time it frees.
+#ifndef GT_RCP
+#define GT_RCP 0
+#endif
+static_assert(GT_RCP != 2 || GT_G % 2 == 0, "packed sigmoids need an even GT_G");
 struct __align__(16) PairT {
   double ux, uy, uz;
   float tr, pad;
@@ -435,14 +442,37 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
 #pragma unroll 2
         for (int j = j0; j < j0 + GT_FLUSH; ++j) {
           const PairT pr = pv[j];
+#if GT_RCP == 2
+          const f32x2 tr2 = splat2(pr.tr);
+#pragma unroll
+          for (int s = 0; s < GT_G; s += 2) {
+            // -k_s (u.z - cos a) log2(e) in FP64 (zx..bxs carry the exact 2^-896
+            // pre-scale of f64s_to_f32_alu), converted to FP32 with two ALU ops;
+            // clamped so 1 + 2^x stays finite for the FMA-pipe reciprocal
+            const float x0 = fminf(f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs)))), 126.f);
+            const float x1 =
+                fminf(f64s_to_f32_alu(fma(pr.ux, zx[s + 1], fma(pr.uy, zy[s + 1], fma(pr.uz, zz[s + 1], bxs)))), 126.f);
+            const f32x2 ny = ffma2(pack2(ex2_approx(x0), ex2_approx(x1)), splat2(-1.0f), splat2(-1.0f));
+            const f32x2 vs = rcp_nr2_neg(ny);
+            float p0, p1;
+            unpack2(ffma2(tr2, vs, pack2(part[s], part[s + 1])), p0, p1);
+            part[s] = p0;
+            part[s + 1] = p1;
+          }
+#else
 #pragma unroll
           for (int s = 0; s < GT_G; ++s) {
             // -k_s (u.z - cos a) log2(e) in FP64 (zx..bxs carry the exact 2^-896
             // pre-scale of f64s_to_f32_alu), converted to FP32 with two ALU ops
             const float x = f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs))));
+#if GT_RCP == 1
+            const float vs = rcp_nr_neg(-1.0f - ex2_approx(fminf(x, 126.f)));
+#else
             const float vs = rcp_approx(1.0f + ex2_approx(x));
+#endif
             part[s] = fmaf(pr.tr, vs, part[s]);
           }
+#endif
         }
 #pragma unroll
         for (int s = 0; s < GT_G; ++s) acc[s].add(part[s]);
@@ -471,21 +501,6 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
 // on the otherwise idle FP64 pipe).
 constexpr int GI_TILE = 32;
 constexpr int GI_THREADS_MAX = 320;
-
-typedef unsigned long long f32x2;
-__device__ __forceinline__ f32x2 pack2(float a, float b) {
-  f32x2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void unpack2(f32x2 v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
 
 // All 21 packed entries (FP32) for one pair.
 __device__ __forceinline__ void entries21(const PairF& q, float4 a, float* e) {
@@ -909,6 +924,12 @@ constexpr int H16_BEXP = 13;  // |B'| < 2^14
 #ifndef GH_MINB
 #define GH_MINB 3  // 12 warps per SM when the shared memory allows it (N_s <= 70)
 #endif
+// sample m16 tiles whose sigmoid reciprocals run as packed FMA-pipe Newton (the rest on
+// MUFU).  Measured on config 2: 0 tiles 166.1 ms, 2: 168.9, 3: 173.5, 5: 187.9 -- MUFU
+// stays (the kernel is issue/latency-limited, not MUFU-throughput-limited).
+#ifndef GH_NR_MT
+#define GH_NR_MT 0
+#endif
 
 template <bool HAS_MASK, bool DEAD_TOP>
 __global__ void __launch_bounds__(GC_WARPS * 32, GH_MINB)
@@ -1025,11 +1046,23 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
             continue;
           }
           float sg[2];
+          if (m < GH_NR_MT) {  // reciprocal on the FMA pipe (packed Newton), x clamped so y stays finite
+            float ex[2];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const float4 uj = u[kb + j];
-            const float x = fmaf(uj.x, zr[m][h][0], fmaf(uj.y, zr[m][h][1], fmaf(uj.z, zr[m][h][2], bx)));
-            sg[j] = rcp_approx(fmaf(ex2_approx(x), 0x1p-12f, 0x1p-12f));  // 2^12 / (1 + 2^x)
+            for (int j = 0; j < 2; ++j) {
+              const float4 uj = u[kb + j];
+              const float x = fmaf(uj.x, zr[m][h][0], fmaf(uj.y, zr[m][h][1], fmaf(uj.z, zr[m][h][2], bx)));
+              ex[j] = ex2_approx(fminf(x, 126.f));
+            }
+            const f32x2 ny = ffma2(pack2(ex[0], ex[1]), splat2(-0x1p-12f), splat2(-0x1p-12f));
+            unpack2(rcp_nr2_neg(ny), sg[0], sg[1]);  // 2^12 / (1 + 2^x)
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const float4 uj = u[kb + j];
+              const float x = fmaf(uj.x, zr[m][h][0], fmaf(uj.y, zr[m][h][1], fmaf(uj.z, zr[m][h][2], bx)));
+              sg[j] = rcp_approx(fmaf(ex2_approx(x), 0x1p-12f, 0x1p-12f));  // 2^12 / (1 + 2^x)
+            }
           }
           h16_split2(sg[0], sg[1], ah[r], al[r]);
         }

@@ -21,8 +21,9 @@ def timeit(fn, reps=3):
         a.record(); fn(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
     return min(ts)
 
+ONLY_Q = '--only-query' in sys.argv
 pairs = V * N
-for name, model, tr, ex in [('quad trace', quad, True, False), ('quad trace exact', quad, True, True), ('quad info', quad, False, False),
+for name, model, tr, ex in [] if ONLY_Q else [('quad trace', quad, True, False), ('quad trace exact', quad, True, True), ('quad info', quad, False, False),
                             ('gp70 trace', gp70, True, False), ('gp70 info', gp70, False, False)]:
     dm = FD._DeviceModel(model, dev)
     ms = timeit(lambda: FD.build_rows(pts, model, tr, 1.0, dev, grid=grid, dmodel=dm, exact=ex))
@@ -33,7 +34,7 @@ rng = np.random.default_rng(5)
 cen = grid.centers()
 sel = np.sort(rng.choice(V, 48, replace=False))
 csel = torch.tensor(cen[sel], device=dev)
-for name, model, tr in [('gp70 trace', gp70, True), ('gp70 info', gp70, False), ('quad info', quad, False)]:
+for name, model, tr in [] if ONLY_Q else [('gp70 trace', gp70, True), ('gp70 info', gp70, False), ('quad info', quad, False)]:
     s64, _ = FD.build_rows(pts, model, tr, 1.0, dev, centers=csel)
     fld = FD.Field(grid, model, 'trace' if tr else 'info', 1.0, s64, None, grid.index3_of(sel).astype(np.int32), dense=False)
     mine = fld.factors
@@ -55,8 +56,11 @@ for name, model in [('gp70', gp70), ('quad', quad)]:
     pos = torch.tensor(w2.positions, device=dev); ax = torch.tensor(w2.rotations[:, :, 2].copy(), device=dev)
     out = {}
     for label, kw in [('full+grad', dict(trace=True, full=True, grad=True)), ('full', dict(trace=False, full=True)),
-                      ('trace', dict(trace=True)), ('trace+grad', dict(trace=True, grad=True))]:
-        ms = timeit(lambda: f.query_device(pos, ax, 'trilinear', out={}, **kw))
+                      ('trace', dict(trace=True)), ('trace+grad', dict(trace=True, grad=True)),
+                      ('det', dict(trace=False, det=True)), ('det+grad', dict(trace=False, det=True, grad=True)),
+                      ('lmin', dict(trace=False, lmin=True)), ('nearest full+grad', dict(trace=True, full=True, grad=True, mode='nearest'))]:
+        kw = dict(kw); md = kw.pop('mode', 'trilinear')
+        ms = timeit(lambda: f.query_device(pos, ax, md, out={}, **kw))
         print(f'query {name} info {label:10s} {ms:8.3f} ms  {1e5/ms*1e3:.3e} q/s', flush=True)
     # precision vs oracle on a cropped reference field for 40 queries
     qsel = np.arange(40)
@@ -82,6 +86,8 @@ for name, model in [('gp70', gp70), ('quad', quad)]:
     ef = np.linalg.norm((res['fim'] - rf).reshape(40, -1), axis=1) / np.linalg.norm(rf.reshape(40, -1), axis=1)
     print(f'query {name} config2 parity: trace rel max {et.max():.2e}  fim relF max {ef.max():.2e} (oracle {time.time()-t0:.1f}s)', flush=True)
 
+if ONLY_Q:
+    sys.exit(0)
 # PC: 100k poses of config 3
 w3 = SC.config3(100000)
 r = torch.tensor(w3.rotations.reshape(-1, 9), device=dev); t = torch.tensor(w3.positions, device=dev)
