@@ -907,10 +907,23 @@ k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSr
 //   larger entry, reset after every FP64 flush; the flush divides by 2^12 s exactly.
 // Entries below max|E| 2^-17 keep an absolute error <= 2^-37 max|E| (FP16 subnormal
 // spacing), far under the FP32 accumulation error of the voxel's sums.
+// packed FP32x2 arithmetic where pairs of sigmoids or entries meet (bit mask):
+// 1 split residuals (FADD2), 2 sigmoid denominators (FFMA2), 4 B-operand scaling (FMUL2)
+#ifndef GH_PACKED
+#define GH_PACKED 3
+#endif
 __device__ __forceinline__ void h16_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
   const float2 b = __half22float2(h);
+#if GH_PACKED & 1
+  f32x2 d;  // both residuals in one packed FP32x2 subtraction
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pack2(x0, x1)), "l"(pack2(b.x, b.y)));
+  float d0, d1;
+  unpack2(d, d0, d1);
+  const __half2 l = __floats2half2_rn(d0, d1);
+#else
   const __half2 l = __floats2half2_rn(x0 - b.x, x1 - b.y);
+#endif
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
@@ -1057,12 +1070,25 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
             const f32x2 ny = ffma2(pack2(ex[0], ex[1]), splat2(-0x1p-12f), splat2(-0x1p-12f));
             unpack2(rcp_nr2_neg(ny), sg[0], sg[1]);  // 2^12 / (1 + 2^x)
           } else {
+#if GH_PACKED & 2
+            float ex[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const float4 uj = u[kb + j];
+              ex[j] = ex2_approx(fmaf(uj.x, zr[m][h][0], fmaf(uj.y, zr[m][h][1], fmaf(uj.z, zr[m][h][2], bx))));
+            }
+            float y0, y1;  // 2^-12 (1 + 2^x) for both, one FFMA2
+            unpack2(ffma2(pack2(ex[0], ex[1]), splat2(0x1p-12f), splat2(0x1p-12f)), y0, y1);
+            sg[0] = rcp_approx(y0);  // 2^12 / (1 + 2^x)
+            sg[1] = rcp_approx(y1);
+#else
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               const float4 uj = u[kb + j];
               const float x = fmaf(uj.x, zr[m][h][0], fmaf(uj.y, zr[m][h][1], fmaf(uj.z, zr[m][h][2], bx)));
               sg[j] = rcp_approx(fmaf(ex2_approx(x), 0x1p-12f, 0x1p-12f));  // 2^12 / (1 + 2^x)
             }
+#endif
           }
           h16_split2(sg[0], sg[1], ah[r], al[r]);
         }
@@ -1080,8 +1106,16 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
 #pragma unroll
         for (int n = 0; n < GC_NT; ++n) {
           const float* eb = ehv + 8 * n + gid;
+#if GH_PACKED & 4
+          float b0, b1, b2, b3;  // scaled by s_cur, two FMUL2
+          unpack2(fmul2(pack2(eb[(k0 + 2 * tig) * 21], eb[(k0 + 2 * tig + 1) * 21]), splat2(s_cur)), b0, b1);
+          unpack2(fmul2(pack2(eb[(k0 + 2 * tig + 8) * 21], eb[(k0 + 2 * tig + 9) * 21]), splat2(s_cur)), b2, b3);
+          h16_split2(b0, b1, bh[n][0], bl[n][0]);
+          h16_split2(b2, b3, bh[n][1], bl[n][1]);
+#else
           h16_split2(eb[(k0 + 2 * tig) * 21] * s_cur, eb[(k0 + 2 * tig + 1) * 21] * s_cur, bh[n][0], bl[n][0]);
           h16_split2(eb[(k0 + 2 * tig + 8) * 21] * s_cur, eb[(k0 + 2 * tig + 9) * 21] * s_cur, bh[n][1], bl[n][1]);
+#endif
         }
         const int kn = k0 + 16;
         uint32_t nh[GC_MT][4], nl[GC_MT][4];
