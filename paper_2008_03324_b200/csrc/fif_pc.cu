@@ -98,50 +98,66 @@ __device__ __forceinline__ void fim21(float dx, float dy, float dz, float px, fl
 __constant__ int kPR[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
 __constant__ int kPC[21] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5};
 
-// Landmark tables: hi[i] = {p_hi.xyz, |p_hi|_1}, lo[i] = {p_lo.xyz, 0}, p = p_hi + p_lo.
-__global__ void k_pc_prep(const double* __restrict__ pts, int64_t n, float4* __restrict__ tab) {
+// Landmark tables: hi[i] = {p_hi.xyz, |p_hi|_1}, lo[i] = {p_lo.xyz, 0}, p = p_hi + p_lo;
+// *p1max = max_i |p_hi|_1 (float bits, for the pre-test margins).
+__global__ void k_pc_prep(const double* __restrict__ pts, int64_t n, float4* __restrict__ tab,
+                          unsigned* __restrict__ p1max) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  float hx, lx, hy, ly, hz, lz;
-  split_f32(pts[3 * i], hx, lx);
-  split_f32(pts[3 * i + 1], hy, ly);
-  split_f32(pts[3 * i + 2], hz, lz);
-  tab[i] = make_float4(hx, hy, hz, fabsf(hx) + fabsf(hy) + fabsf(hz));
-  tab[n + i] = make_float4(lx, ly, lz, 0.f);
+  float l1 = 0.f;
+  if (i < n) {
+    float hx, lx, hy, ly, hz, lz;
+    split_f32(pts[3 * i], hx, lx);
+    split_f32(pts[3 * i + 1], hy, ly);
+    split_f32(pts[3 * i + 2], hz, lz);
+    l1 = fabsf(hx) + fabsf(hy) + fabsf(hz);
+    tab[i] = make_float4(hx, hy, hz, l1);
+    tab[n + i] = make_float4(lx, ly, lz, 0.f);
+  }
+  const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(l1));  // non-negative floats order as ints
+  if ((threadIdx.x & 31) == 0) atomicMax(p1max, m);
 }
 
 // FP32 pre-test with rigorous margins, branch-free.  Every quantity the reference
 // compares is an affine function of the landmark position p for a fixed pose:
 //   zc = R2 . (p - t),  b0 = zc (u - 0) = (fx R0 + cx R2) . (p - t),  b1 = zc (u - W),
 //   c0 = zc (v - 0),    c1 = zc (v - H)                 (u, v the pixel coordinates)
-// so each is one 3-FMA dot product w_k . p_hi + C_k with per-pose FP32 coefficients
-// (formed in FP64).  The FP32 evaluation differs from the exact value by at most
-// ~6 u W_k (|p|_1 + |t|_1) (u = 2^-24, W_k = max |w_k|: coefficient and constant
-// rounding, p_lo dropped, three FMA roundings), and the reference's FP64 decision by
-// far less, so outside the margin 16 u W_k (|p|_1 + |t|_1) the sign — hence the
-// reference's decision — is certain.  Returns +1 certainly visible, -1 certainly not,
-// 0 within a margin: run the reference's exact FP64 test.
+// and the reference sees the landmark iff zc > 0, b0 >= 0, b1 < 0, c0 >= 0, c1 < 0.
+// The FP32 evaluation of w_k . p_hi + C_k (per-pose coefficients formed in FP64)
+// differs from the exact value by at most ~6 u W_k (|p|_1 + |t|_1) (u = 2^-24, W_k =
+// max |w_k|: coefficient and constant rounding, p_lo dropped, three FMA roundings), and
+// the reference's FP64 decision by far less.  With the pose-uniform margin
+// m_k = 16 u (W_k (max_i |p_i|_1 + |t|_1) + |C_k|), each row is stored normalised as
+//   h_k = s_k (w_k . p + C_k) / m_k + 1      (s_k = +1, +1, -1, +1, -1: "inside" > 0)
+// whose FP32 evaluation is within ~0.4 of its exact value (the normalisation's own
+// roundings included), so h_k > 2 proves the row's condition and h_k < 0 refutes it.
+// Returns +1 certainly visible, -1 certainly not, 0 otherwise: run the reference's
+// exact FP64 test.
 struct PoseAff {
-  float w[5][3], c[5], mg[5], m0[5];  // rows: zc, b0, b1, c0, c1; margin = mg |p|_1 + m0
+  float w[5][3], c[5];
 };
 __device__ __forceinline__ int pc_pretest(const PoseAff& A, float4 ph) {
-  float v[5], m[5];
+  float h[5];
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    v[k] = fmaf(A.w[k][0], ph.x, fmaf(A.w[k][1], ph.y, fmaf(A.w[k][2], ph.z, A.c[k])));
-    m[k] = fmaf(A.mg[k], ph.w, A.m0[k]);
-  }
-  const bool zpos = v[0] > m[0], zneg = v[0] < -m[0];
-  const bool out = (v[1] < -m[1]) | (v[2] > m[2]) | (v[3] < -m[3]) | (v[4] > m[4]);
-  const bool in = (v[1] > m[1]) & (v[2] < -m[2]) & (v[3] > m[3]) & (v[4] < -m[4]);
-  return (zpos & in) ? 1 : ((zneg | (zpos & out)) ? -1 : 0);
+  for (int k = 0; k < 5; ++k) h[k] = fmaf(A.w[k][0], ph.x, fmaf(A.w[k][1], ph.y, fmaf(A.w[k][2], ph.z, A.c[k])));
+  const float img = fminf(fminf(h[1], h[2]), fminf(h[3], h[4]));  // the four image-border rows
+  const bool vis = fminf(h[0], img) > 2.f;
+  const bool invis = (h[0] < 0.f) | ((h[0] > 2.f) & (img < 0.f));
+  return vis ? 1 : (invis ? -1 : 0);
+}
+
+// 16-byte shared-memory load at a shared-window address (keeps the tile address
+// arithmetic in 32-bit shared offsets)
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
 }
 
 template <bool MASK>
 __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double* __restrict__ rot, const double* __restrict__ tr,
                                                           int64_t nq, const double* __restrict__ pts,
                                                           const float4* __restrict__ ptab, int64_t n, fif_camera cam,
-                                                          float inv_s2, double* __restrict__ out,
+                                                          const unsigned* __restrict__ p1max, float inv_s2, double* __restrict__ out,
                                                           uint8_t* __restrict__ mask, const int32_t* __restrict__ perm) {
   extern __shared__ float4 pcsm[];
   float4* ring_hi = pcsm;                                  // [PC_NBUF][PC_TILE]
@@ -197,7 +213,7 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
       split_f32(tz, thz, tlz);
       // affine rows in FP64: world-frame coefficients of zc, b0, b1, c0, c1
       const double R0[3] = {R[0], R[3], R[6]}, R1[3] = {R[1], R[4], R[7]}, R2[3] = {R[2], R[5], R[8]};
-      const double lt = fabs(tx) + fabs(ty) + fabs(tz);
+      const double lt = fabs(tx) + fabs(ty) + fabs(tz) + (double)__uint_as_float(*p1max);
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
         double w[3];
@@ -209,11 +225,11 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
                                           : k == 3 ? cam.fy * R1[i] + cam.cy * R2[i] : cam.fy * R1[i] + cyh * R2[i];
         const double c = -(w[0] * tx + w[1] * ty + w[2] * tz);
         const double wm = fmax(fabs(w[0]), fmax(fabs(w[1]), fabs(w[2])));
+        const double mk = 16.0 * 0x1p-24 * (wm * lt + fabs(c)) * 1.000001;
+        const double sc = (k == 2 || k == 4 ? -1.0 : 1.0) / mk;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) A.w[k][i] = (float)w[i];
-        A.c[k] = (float)c;
-        A.mg[k] = (float)(16.0 * 0x1p-24 * wm * 1.0000001);
-        A.m0[k] = (float)(16.0 * 0x1p-24 * (wm * lt + fabs(c)) * 1.0000001);
+        for (int i = 0; i < 3; ++i) A.w[k][i] = (float)(w[i] * sc);
+        A.c[k] = (float)(c * sc + 1.0);
       }
     }
     float acc[21];
@@ -224,8 +240,8 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
       const int64_t base = t * PC_TILE;
       const int cnt = (int)min((int64_t)PC_TILE, n - base);
       const int bsel = (int)(seq % PC_NBUF);
-      const float4* tile_hi = ring_hi + bsel * PC_TILE;
-      const float4* tile_lo = ring_lo + bsel * PC_TILE;
+      const uint32_t tile_hi = smem_u32(ring_hi + bsel * PC_TILE) + 16u * lane;  // this lane's first landmark
+      const uint32_t tile_lo = smem_u32(ring_lo + bsel * PC_TILE) + 16u * lane;
       mbar_wait(&full[bsel], (uint32_t)((seq / PC_NBUF) & 1));
       if (!has_pose) {
         __syncwarp();
@@ -237,7 +253,7 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
         bool vis = false;
         float4 ph = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < cnt) {
-          ph = tile_hi[j];
+          ph = lds128(tile_hi + 16u * j0);
           const int pre = pc_pretest(A, ph);
           if (pre == 0) {  // within a margin: the reference's FP64 test (pose re-read: rare path)
             const int64_t i = base + j;
@@ -252,7 +268,7 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
         const unsigned bal = __ballot_sync(0xffffffffu, vis);
         if (vis) {
           // d = p - t, exact to ~1 ulp of |d| from the hi / lo parts
-          const float4 pl = tile_lo[j];
+          const float4 pl = lds128(tile_lo + 16u * j0);
           const float dx = (ph.x - thx) + (pl.x - tlx), dy = (ph.y - thy) + (pl.y - tly),
                       dz = (ph.z - thz) + (pl.z - tlz);
           const int slot = qn + __popc(bal & lt_mask);
@@ -392,11 +408,13 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
   unsigned blocks = (unsigned)(need < cap ? need : cap);
   const float inv_s2 = (float)(1.0 / (sigma * sigma));
   float4* ptab = nullptr;
-  if (cudaMallocAsync(&ptab, sizeof(float4) * 2 * n_points, st) != cudaSuccess) {  // hi[n], lo[n]
+  if (cudaMallocAsync(&ptab, sizeof(float4) * (2 * n_points + 1), st) != cudaSuccess) {  // hi[n], lo[n], max |p|_1
     set_error("fif_pc_fim: cudaMallocAsync failed");
     return FIF_ERR_CUDA;
   }
-  k_pc_prep<<<(unsigned)((n_points + 255) / 256), 256, 0, st>>>(d_points, n_points, ptab);
+  unsigned* p1max = reinterpret_cast<unsigned*>(ptab + 2 * n_points);
+  cudaMemsetAsync(p1max, 0, sizeof(unsigned), st);
+  k_pc_prep<<<(unsigned)((n_points + 255) / 256), 256, 0, st>>>(d_points, n_points, ptab, p1max);
   FIF_CHECK_LAUNCH("k_pc_prep");
   const size_t smem = sizeof(float4) * (2 * PC_NBUF * PC_TILE + PC_WARPS * PC_QCAP * 2) + 2 * PC_NBUF * sizeof(uint64_t);
   static bool attr = false;
@@ -431,10 +449,10 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
     cub::DeviceRadixSort::SortPairs(sbuf + 4 * b4 + bp, temp, keys, keys2, idx, perm, (int)q, 0, 19, st);
   }
   if (d_mask)
-    k_pc_fim<true><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2, d_out,
-                                                        d_mask, perm);
+    k_pc_fim<true><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, p1max, inv_s2,
+                                                        d_out, d_mask, perm);
   else
-    k_pc_fim<false><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, inv_s2,
+    k_pc_fim<false><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, p1max, inv_s2,
                                                          d_out, d_mask, perm);
   if (sbuf) cudaFreeAsync(sbuf, st);
   cudaFreeAsync(ptab, st);
