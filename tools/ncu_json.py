@@ -31,6 +31,6 @@ res["k_query_info"], res["k_query_prep_gp"] = q, p
 nq = 100000
 res["query_per_query"] = {"dram_bytes": (q["dram_read"] + q["dram_write"] + p["dram_read"] + p["dram_write"]) / nq,
                           "source": "k_query_prep_gp + k_query_info dram bytes / 1e5 queries (bench.py config-2)"}
-path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+path = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "ncu_summary.json")
 json.dump(res, open(path, "w"), indent=1)
 print(json.dumps(res, indent=1))
