@@ -128,7 +128,10 @@ int fif_export_reference(int factor_kind, const fif_model* model, const double* 
  * Outputs (each optional, NULL = not written):
  *   d_trace (Q) | d_trace_grad (Q,6) | d_fim (Q,36) | d_fim_grad (Q,6,36) |
  *   d_det (Q) | d_lmin (Q) | d_status (Q) uint8.
- * Gradient convention: d/d[t(3); theta(3)] with t' = t + dt, R' = exp(dtheta^) R.*/
+ * Gradient convention: d/d[t(3); theta(3)] with t' = t + dt, R' = exp(dtheta^) R.
+ * lambda_min gradients (fif_query_ex) go through the eigenvector, whose sensitivity
+ * to the FP32 copy grows like 1/gap: pass the f64 rows with FIF_Q_FIELD_F64 for
+ * them (the Python Field does so automatically).                                */
 int fif_query(int factor_kind, const fif_model* model, const fif_grid* grid, const void* d_field,
               const int32_t* d_slots, const double* d_positions, const double* d_axes, int64_t q, int mode,
               uint32_t flags, double* d_trace, double* d_trace_grad, double* d_fim, double* d_fim_grad,

@@ -481,7 +481,10 @@ class Field:
             if grad:
                 lming_t = buf("lmin_grad", (6,))
         st_t = buf("status", (), torch.uint8)
-        field_t, is64 = self._field_ptr(field_f64)
+        # lambda_min gradients read the FP64 master: d lambda = v^T dF v through the
+        # eigenvector v, whose sensitivity to the FP32 copy's rounding grows like
+        # 1 / (eigenvalue gap) (measured 6e-4 on near-degenerate golden voxels vs 9e-6)
+        field_t, is64 = self._field_ptr(field_f64 or (lmin and grad))
         if is64 and isinstance(self.model, GpVisibility):
             flags |= _lib.Q_FIELD_F64
         kind = _lib.KIND_INFO if self._is_info else _lib.KIND_TRACE

@@ -60,10 +60,11 @@ def test_metric_yaw_gradient(oracle, g_small, setup, metric, mode):
     for f64 in (True, False):
         r = P.metric_yaw_batch(f, pos, yaws, metric, mode, grad=True, field_f64=f64)
         assert np.array_equal(r["in_field"], st == 0)
-        assert np.allclose(r["values"], v, rtol=1e-4 if f64 else 5e-4, atol=0)
+        assert np.allclose(r["values"], v, rtol=1e-4, atol=0)
         err = np.linalg.norm(r["grad"] - fd, axis=1) / np.maximum(np.linalg.norm(fd, axis=1), 1e-300)
-        # FP32 S copy: lambda_min's eigenvector (and so d lambda) is sensitive to 1/gap
-        tol = 1e-4 if f64 else (2e-3 if metric == "lmin" else 5e-4)
+        # lambda_min gradients always read the FP64 master (eigenvector sensitivity ~ 1/gap)
+        tol = 1e-4
+        print(f"[yaw {metric} {mode} f64={f64}] value {(np.abs(r['values'] - v) / np.abs(v)).max():.2e} grad {err.max():.2e}")
         assert err.max() <= tol, (f64, err.max())
 
 

@@ -148,13 +148,16 @@ def test_gradients_vs_finite_difference(oracle, g_small, models, small_grid, mna
                                         rots)
         g_tr = res["trace_grad"].cpu().numpy()
         err = np.linalg.norm(g_tr - g_tr_fd, axis=1) / np.linalg.norm(g_tr_fd, axis=1)
-        tol = TOL if (f64 or isinstance(m, F.QuadraticVisibility)) else 5 * TOL
+        print(f"[grad {mname} {kind} f64={f64}] trace grad {err.max():.2e}", end="")
+        tol = TOL  # the north_star's 1e-4, FP32 and FP64 query copies alike
         assert err.max() <= tol, (f64, err.max())
         if kind == "info":
             g_f = res["fim_grad"].cpu().numpy().reshape(-1, 6, 6, 6)
             e2 = np.linalg.norm((g_f - g_fim_fd).reshape(len(pos), -1), axis=1) / np.linalg.norm(
                 g_fim_fd.reshape(len(pos), -1), axis=1)
+            print(f" 6x6 grad {e2.max():.2e}", end="")
             assert e2.max() <= tol, (f64, e2.max())
+        print()
 
 
 def test_config2_queries_end_to_end(oracle, models):
@@ -251,10 +254,11 @@ def test_metric_gradients_vs_finite_difference(oracle, g_small, models, small_gr
                              field_f64=f64)
         mine_v = res[metric].cpu().numpy()
         mine_g = res[f"{metric}_grad"].cpu().numpy()
-        tol = TOL if (f64 or isinstance(m, F.QuadraticVisibility)) else 5 * TOL
+        tol = TOL  # the north_star's 1e-4, FP32 and FP64 query copies alike
         ev_err = np.abs(mine_v - val) / np.abs(val)
         assert ev_err.max() <= tol, (f64, ev_err.max())
         err = np.linalg.norm(mine_g - fd, axis=1) / np.linalg.norm(fd, axis=1)
+        print(f"[metric grad {mname} {metric} f64={f64}] value {ev_err.max():.2e} grad {err.max():.2e}")
         assert err.max() <= tol, (f64, err.max())
 
 
