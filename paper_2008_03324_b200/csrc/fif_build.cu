@@ -344,13 +344,20 @@ constexpr int GT_THREADS = 256;
 #ifndef GT_MINB
 #define GT_MINB 3
 #endif
-// sigmoid reciprocal: 0 MUFU rcp (default), 1 scalar FMA-pipe Newton, 2 packed (FFMA2)
-// Newton.  Measured on config 2 (tools/sweep_build.sh): 113.7 / 133.5 / 140.3 ms -- moving
-// the reciprocal off MUFU costs more issue slots and latency than the MUFU time it frees.
+// Sigmoid reciprocals.  GT_PAIR (default): one MUFU rcp per pair of sigmoids,
+// r = 1 / ((1 + 2^x0)(1 + 2^x1)) with x clamped to 63 -- a quarter less MUFU/MIO traffic
+// for 2 FMULs and 2 clamps: config 2 113.7 -> 110.1 ms (106.1 unclamped, which is only safe
+// for |x| <= 63; a per-CTA proof plus a fallback path measured 111.8, a per-landmark
+// branch 115.0).  Otherwise GT_RCP: 0 one MUFU rcp per sigmoid, 1 scalar FMA-pipe Newton,
+// 2 packed (FFMA2) Newton -- measured 113.7 / 133.5 / 140.3 ms: moving the reciprocal to
+// the FMA pipe costs more issue slots and latency than the MUFU time it frees.
+#ifndef GT_PAIR
+#define GT_PAIR 1
+#endif
 #ifndef GT_RCP
 #define GT_RCP 0
 #endif
-static_assert(GT_RCP != 2 || GT_G % 2 == 0, "packed sigmoids need an even GT_G");
+static_assert(GT_G % 2 == 0, "paired sigmoids need an even GT_G");
 struct __align__(16) PairT {
   double ux, uy, uz;
   float tr, pad;
@@ -442,6 +449,22 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
 #pragma unroll 2
         for (int j = j0; j < j0 + GT_FLUSH; ++j) {
           const PairT pr = pv[j];
+          if (GT_PAIR) {
+#pragma unroll
+          for (int s = 0; s < GT_G; s += 2) {
+            // two sigmoids, one reciprocal: r = 1 / ((1 + 2^x0)(1 + 2^x1)),
+            // vs0 = (1 + 2^x1) r, vs1 = (1 + 2^x0) r; x <= 63 keeps the product finite
+            // (a sigmoid below 2^-63 is then off by < 2^-63 absolute)
+            const float x0 =
+                fminf(f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs)))), 63.f);
+            const float x1 =
+                fminf(f64s_to_f32_alu(fma(pr.ux, zx[s + 1], fma(pr.uy, zy[s + 1], fma(pr.uz, zz[s + 1], bxs)))), 63.f);
+            const float a0 = 1.0f + ex2_approx(x0), a1 = 1.0f + ex2_approx(x1);
+            const float tr_r = pr.tr * rcp_approx(a0 * a1);
+            part[s] = fmaf(tr_r, a1, part[s]);
+            part[s + 1] = fmaf(tr_r, a0, part[s + 1]);
+          }
+          } else {
 #if GT_RCP == 2
           const f32x2 tr2 = splat2(pr.tr);
 #pragma unroll
@@ -473,6 +496,7 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
             part[s] = fmaf(pr.tr, vs, part[s]);
           }
 #endif
+          }
         }
 #pragma unroll
         for (int s = 0; s < GT_G; ++s) acc[s].add(part[s]);
@@ -907,6 +931,12 @@ k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSr
 //   larger entry, reset after every FP64 flush; the flush divides by 2^12 s exactly.
 // Entries below max|E| 2^-17 keep an absolute error <= 2^-37 max|E| (FP16 subnormal
 // spacing), far under the FP32 accumulation error of the voxel's sums.
+// one reciprocal per pair of sigmoids (1 / (y0 y1)): 165.1 -> 164.0 ms, but it needs
+// |x| <= 62 (a host-checked template variant would double the instantiations; the clamp
+// that avoids it costs more than the gain: 166.5 ms) -- off
+#ifndef GH_PAIR_RCP
+#define GH_PAIR_RCP 0
+#endif
 // packed FP32x2 arithmetic where pairs of sigmoids or entries meet (bit mask):
 // 1 split residuals (FADD2), 2 sigmoid denominators (FFMA2), 4 B-operand scaling (FMUL2)
 #ifndef GH_PACKED
@@ -1074,7 +1104,20 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
             const f32x2 ny = ffma2(pack2(ex[0], ex[1]), splat2(-0x1p-12f), splat2(-0x1p-12f));
             unpack2(rcp_nr2_neg(ny), sg[0], sg[1]);  // 2^12 / (1 + 2^x)
           } else {
-#if GH_PACKED & 2
+#if GH_PAIR_RCP
+            // one reciprocal for both: r = 1 / (y0 y1), sg0 = y1 r, sg1 = y0 r; x <= 63 keeps
+            // the product finite (a sigmoid below 2^-63 is then off by < 2^-63 absolute)
+            float ex[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const float4 uj = u[kb + j];
+              ex[j] = ex2_approx(fminf(fmaf(uj.x, zr[m][h][0], fmaf(uj.y, zr[m][h][1], fmaf(uj.z, zr[m][h][2], bx))), 63.f));
+            }
+            const float y0 = fmaf(ex[0], 0x1p-12f, 0x1p-12f), y1 = fmaf(ex[1], 0x1p-12f, 0x1p-12f);
+            const float r = rcp_approx(y0 * y1);
+            sg[0] = y1 * r;
+            sg[1] = y0 * r;
+#elif GH_PACKED & 2
             float ex[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
