@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(QDShape<QQ, RPQ>::THREADS, 3) k_query_prep_gp(
   double* kf = smd;                                  // [NP8][nv] (+ tail)
   double* sv = kf + ((NP8 * nv + 8 + 15) & ~15);     // [QQ][NP8] v^r
   double* sa = sv + QQ * NP8;                        // [NP8][4] {1, zs/l^2}
+  double* sz = sa + 4 * NP8;                         // [QQ][4] optical axes of the CTA's queries
   __shared__ __align__(8) uint64_t kbar;
   const int64_t q0 = blockIdx.x * (int64_t)QQ;
   const int t = threadIdx.x;
@@ -433,6 +434,9 @@ __global__ void __launch_bounds__(QDShape<QQ, RPQ>::THREADS, 3) k_query_prep_gp(
     int64_t r[8];
     double w[8], dw[8][3];
     const int64_t qo = perm ? (int64_t)perm[q] : q;  // slot q holds query qo (locality order)
+    sz[4 * t] = axes[3 * qo];
+    sz[4 * t + 1] = axes[3 * qo + 1];
+    sz[4 * t + 2] = axes[3 * qo + 2];
     const int st = locate(gm, slots, pos[3 * qo], pos[3 * qo + 1], pos[3 * qo + 2], trilinear != 0, nc, r, w, dw);
     status[q] = (uint8_t)st;
     for (int c = 0; c < 8; ++c) {
@@ -449,17 +453,24 @@ __global__ void __launch_bounds__(QDShape<QQ, RPQ>::THREADS, 3) k_query_prep_gp(
     sa[4 * g + 2] = ok ? m.zs[3 * g + 1] * inv_l2 : 0.0;
     sa[4 * g + 3] = ok ? m.zs[3 * g + 2] * inv_l2 : 0.0;
   }
-  for (int idx = t; idx < QQ * NP8; idx += blockDim.x) {  // v^r (kernels.py:652-657)
-    const int qi = idx / NP8, g = idx - qi * NP8;
-    const int64_t q = q0 + qi;
-    double v = 0.0;
-    if (q < nq && g < nv) {
-      const int64_t qo = perm ? (int64_t)perm[q] : q;
-      const double c = __dadd_rn(__dadd_rn(__dmul_rn(axes[3 * qo], m.zs[3 * g]), __dmul_rn(axes[3 * qo + 1], m.zs[3 * g + 1])),
-                                 __dmul_rn(axes[3 * qo + 2], m.zs[3 * g + 2]));
-      v = m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
+  __syncthreads();  // sz (the queries' optical axes) staged by the locating threads
+  auto vr_of = [&](int qi, double z0, double z1, double z2) {  // kernels.py:652-657
+    const double c = __dadd_rn(__dadd_rn(__dmul_rn(sz[4 * qi], z0), __dmul_rn(sz[4 * qi + 1], z1)),
+                               __dmul_rn(sz[4 * qi + 2], z2));
+    return m.sig2 * exp(__dmul_rn(__dsub_rn(c, 1.0), inv_l2));
+  };
+  if ((int)blockDim.x >= NP8) {  // thread owns sample g (its zs in registers), strides over queries
+    const int gq = blockDim.x / NP8, g = t % NP8, qs = t / NP8;
+    if (qs < gq) {
+      const bool gok = g < nv;
+      const double z0 = gok ? m.zs[3 * g] : 0.0, z1 = gok ? m.zs[3 * g + 1] : 0.0, z2 = gok ? m.zs[3 * g + 2] : 0.0;
+      for (int qi = qs; qi < QQ; qi += gq) sv[qi * NP8 + g] = (q0 + qi < nq && gok) ? vr_of(qi, z0, z1, z2) : 0.0;
     }
-    sv[idx] = v;
+  } else {
+    for (int idx = t; idx < QQ * NP8; idx += blockDim.x) {
+      const int qi = idx / NP8, g = idx - qi * NP8;
+      sv[idx] = (q0 + qi < nq && g < nv) ? vr_of(qi, m.zs[3 * g], m.zs[3 * g + 1], m.zs[3 * g + 2]) : 0.0;
+    }
   }
   if (use_tma) mbar_wait(&kbar, 0);
   __syncthreads();
@@ -1422,7 +1433,8 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
     FIF_CHECK_LAUNCH("fif_query(locality sort)");
   }
   const int np8 = (nv + 7) & ~7, ntiles = np8 / 8;
-  const size_t dmma_smem = sizeof(double) * ((size_t)((np8 * nv + 8 + 15) & ~15) + (size_t)QD_Q * np8 + 4 * (size_t)np8);
+  const size_t dmma_smem =
+      sizeof(double) * ((size_t)((np8 * nv + 8 + 15) & ~15) + (size_t)QD_Q * np8 + 4 * (size_t)np8 + 4 * (size_t)QD_Q);
   static const bool simt_prep = getenv("FIF_QUERY_PREP_SIMT") != nullptr;
   if (model->kind == FIF_MODEL_GP && ntiles <= 12 && !simt_prep) {
     double* wtd = reinterpret_cast<double*>(s_wt);
