@@ -260,3 +260,20 @@ def test_fif1_interop_with_reference_files(tmp_path, g_models):
     assert g.factor_kind == "info" and 0 < g.rows <= cfg.voxel_count
     q = g.query_batch(cfg.centers()[:5], axes=np.tile([0.0, 0.0, 1.0], (5, 1)), outputs=("trace",), mode="nearest")
     assert torch.isfinite(q["trace"]).all()
+
+
+@pytest.mark.parametrize("k_s", [60.0, 200.0])
+def test_sharp_sigmoids_stay_finite(oracle, g_small, models, small_grid, k_s, gp_info_kernel):
+    """Sharp visibility sigmoids: exponent arguments |x| = k_s |u.z - cos a| log2(e) reach
+    ~500, far past FP32's 2^x range and the trace kernel's paired-reciprocal clamp
+    (x <= 63); the builds stay finite and within tolerance of the oracle."""
+    m0 = models["gp30"]
+    m = F.GpVisibility(m0.samples, m0.params, m0.alpha, k_s, m0.kinv)
+    pts = g_small["points"]
+    cen = small_grid.centers()
+    for kind in ("trace", "info"):
+        mine = reference_order(F.Field.build(pts, small_grid, m, kind))
+        assert np.isfinite(mine).all()
+        ref = oracle_field(oracle, m, cen, pts, kind)
+        err = trace_rel_l2(mine, ref) if kind == "trace" else info_rel_fro(mine, ref)
+        assert err.max() <= (TRACE_TOL if kind == "trace" else INFO_TOL), (kind, err.max())
