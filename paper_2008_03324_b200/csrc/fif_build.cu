@@ -961,6 +961,11 @@ k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSr
 //   larger entry, reset after every FP64 flush; the flush divides by 2^12 s exactly.
 // Entries below max|E| 2^-17 keep an absolute error <= 2^-37 max|E| (FP16 subnormal
 // spacing), far under the FP32 accumulation error of the voxel's sums.
+// exponent arguments of rows gid / gid + 8 as FFMA2 pairs (u splats, zs pairs) and their
+// 2^-12 (1 + 2^x) as one FFMA2: 165.0 -> 160.6 ms, bit-identical results
+#ifndef GH_XPAIR
+#define GH_XPAIR 1
+#endif
 // one reciprocal per pair of sigmoids (1 / (y0 y1)): 165.1 -> 164.0 ms, but it needs
 // |x| <= 62 (a host-checked template variant would double the instantiations; the clamp
 // that avoids it costs more than the gain: 166.5 ms) -- off
@@ -1050,6 +1055,16 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       zr[m][h][1] = ok ? (float)(ax * zs[3 * g + 1]) : 0.f;
       zr[m][h][2] = ok ? (float)(ax * zs[3 * g + 2]) : 0.f;
     }
+#if GH_XPAIR
+  // rows gid and gid + 8 of each m-tile as FP32x2 pairs: the exponent arguments of both
+  // rows come out of three FFMA2 per landmark
+  f32x2 zr2[GC_MT][3];
+#pragma unroll
+  for (int m = 0; m < GC_MT; ++m)
+#pragma unroll
+    for (int c3 = 0; c3 < 3; ++c3) zr2[m][c3] = pack2(zr[m][0][c3], zr[m][1][c3]);
+  const f32x2 bx2 = splat2(bx);
+#endif
   float c[GC_MT][GC_NT][4];
 #pragma unroll
   for (int m = 0; m < GC_MT; ++m)
@@ -1113,6 +1128,44 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       const float4* uv = uu + vl * GC_TILE;
       // A fragment (m16n8k16, f16): reg0 (row gid, k 2tig..+1), reg1 (row gid+8, k 2tig..+1),
       // reg2 (row gid, k 2tig+8..+9), reg3 (row gid+8, k 2tig+8..+9); low half = lower k
+#if GH_XPAIR
+      auto afrag_m = [&](int k0, int m, uint32_t (&ah)[4], uint32_t (&al)[4]) {
+        const float4 u[4] = {uv[k0 + 2 * tig], uv[k0 + 2 * tig + 1], uv[k0 + 2 * tig + 8], uv[k0 + 2 * tig + 9]};
+        if (DEAD_TOP && m == GC_MT - 1) {  // rows gid + 8 are padding: row gid alone
+#pragma unroll
+          for (int r = 0; r < 4; r += 2) {
+            const int kb = r;
+            float sg[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const float4 uj = u[kb + j];
+              const float x = fmaf(uj.x, zr[m][0][0], fmaf(uj.y, zr[m][0][1], fmaf(uj.z, zr[m][0][2], bx)));
+              sg[j] = rcp_approx(fmaf(ex2_approx(x), 0x1p-12f, 0x1p-12f));
+            }
+            h16_split2(sg[0], sg[1], ah[r], al[r]);
+            ah[r + 1] = al[r + 1] = 0u;
+          }
+          return;
+        }
+#pragma unroll
+        for (int kb = 0; kb < 4; kb += 2) {
+          float sg[2][2];  // [row half h][landmark j]
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const float4 uj = u[kb + j];
+            const f32x2 x2 = ffma2(splat2(uj.x), zr2[m][0], ffma2(splat2(uj.y), zr2[m][1], ffma2(splat2(uj.z), zr2[m][2], bx2)));
+            float x0, x1;
+            unpack2(x2, x0, x1);
+            float y0, y1;  // 2^-12 (1 + 2^x) for both rows, one FFMA2
+            unpack2(ffma2(pack2(ex2_approx(x0), ex2_approx(x1)), splat2(0x1p-12f), splat2(0x1p-12f)), y0, y1);
+            sg[0][j] = rcp_approx(y0);
+            sg[1][j] = rcp_approx(y1);
+          }
+          h16_split2(sg[0][0], sg[0][1], ah[kb], al[kb]);          // reg kb: row gid
+          h16_split2(sg[1][0], sg[1][1], ah[kb + 1], al[kb + 1]);  // reg kb + 1: row gid + 8
+        }
+      };
+#else
       auto afrag_m = [&](int k0, int m, uint32_t (&ah)[4], uint32_t (&al)[4]) {
         const float4 u[4] = {uv[k0 + 2 * tig], uv[k0 + 2 * tig + 1], uv[k0 + 2 * tig + 8], uv[k0 + 2 * tig + 9]};
 #pragma unroll
@@ -1170,6 +1223,7 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
           h16_split2(sg[0], sg[1], ah[r], al[r]);
         }
       };
+#endif
       uint32_t ah[GC_MT][4], al[GC_MT][4];
 #pragma unroll
       for (int m = 0; m < GC_MT; ++m) afrag_m(0, m, ah[m], al[m]);
