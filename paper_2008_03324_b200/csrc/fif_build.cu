@@ -479,52 +479,52 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
 #pragma unroll 2
         for (int j = j0; j < j0 + GT_FLUSH; ++j) {
           const PairT pr = pv[j];
-          if (GT_PAIR) {
+          if constexpr (GT_PAIR) {
 #pragma unroll
-          for (int s = 0; s < GT_G; s += 2) {
-            // two sigmoids, one reciprocal: r = 1 / ((1 + 2^x0)(1 + 2^x1)),
-            // vs0 = (1 + 2^x1) r, vs1 = (1 + 2^x0) r; x <= 63 keeps the product finite
-            // (a sigmoid below 2^-63 is then off by < 2^-63 absolute)
-            const float x0 =
-                fminf(f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs)))), 63.f);
-            const float x1 =
-                fminf(f64s_to_f32_alu(fma(pr.ux, zx[s + 1], fma(pr.uy, zy[s + 1], fma(pr.uz, zz[s + 1], bxs)))), 63.f);
-            const float a0 = 1.0f + ex2_approx(x0), a1 = 1.0f + ex2_approx(x1);
-            const float tr_r = pr.tr * rcp_approx(a0 * a1);
-            part[s] = fmaf(tr_r, a1, part[s]);
-            part[s + 1] = fmaf(tr_r, a0, part[s + 1]);
-          }
+            for (int s = 0; s < GT_G; s += 2) {
+              // two sigmoids, one reciprocal: r = 1 / ((1 + 2^x0)(1 + 2^x1)),
+              // vs0 = (1 + 2^x1) r, vs1 = (1 + 2^x0) r; x <= 63 keeps the product finite
+              // (a sigmoid below 2^-63 is then off by < 2^-63 absolute)
+              const float x0 =
+                  fminf(f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs)))), 63.f);
+              const float x1 =
+                  fminf(f64s_to_f32_alu(fma(pr.ux, zx[s + 1], fma(pr.uy, zy[s + 1], fma(pr.uz, zz[s + 1], bxs)))), 63.f);
+              const float a0 = 1.0f + ex2_approx(x0), a1 = 1.0f + ex2_approx(x1);
+              const float tr_r = pr.tr * rcp_approx(a0 * a1);
+              part[s] = fmaf(tr_r, a1, part[s]);
+              part[s + 1] = fmaf(tr_r, a0, part[s + 1]);
+            }
           } else {
 #if GT_RCP == 2
-          const f32x2 tr2 = splat2(pr.tr);
+            const f32x2 tr2 = splat2(pr.tr);
 #pragma unroll
-          for (int s = 0; s < GT_G; s += 2) {
-            // -k_s (u.z - cos a) log2(e) in FP64 (zx..bxs carry the exact 2^-896
-            // pre-scale of f64s_to_f32_alu), converted to FP32 with two ALU ops;
-            // clamped so 1 + 2^x stays finite for the FMA-pipe reciprocal
-            const float x0 = fminf(f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs)))), 126.f);
-            const float x1 =
-                fminf(f64s_to_f32_alu(fma(pr.ux, zx[s + 1], fma(pr.uy, zy[s + 1], fma(pr.uz, zz[s + 1], bxs)))), 126.f);
-            const f32x2 ny = ffma2(pack2(ex2_approx(x0), ex2_approx(x1)), splat2(-1.0f), splat2(-1.0f));
-            const f32x2 vs = rcp_nr2_neg(ny);
-            float p0, p1;
-            unpack2(ffma2(tr2, vs, pack2(part[s], part[s + 1])), p0, p1);
-            part[s] = p0;
-            part[s + 1] = p1;
-          }
+            for (int s = 0; s < GT_G; s += 2) {
+              // -k_s (u.z - cos a) log2(e) in FP64 (zx..bxs carry the exact 2^-896
+              // pre-scale of f64s_to_f32_alu), converted to FP32 with two ALU ops;
+              // clamped so 1 + 2^x stays finite for the FMA-pipe reciprocal
+              const float x0 = fminf(f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs)))), 126.f);
+              const float x1 =
+                  fminf(f64s_to_f32_alu(fma(pr.ux, zx[s + 1], fma(pr.uy, zy[s + 1], fma(pr.uz, zz[s + 1], bxs)))), 126.f);
+              const f32x2 ny = ffma2(pack2(ex2_approx(x0), ex2_approx(x1)), splat2(-1.0f), splat2(-1.0f));
+              const f32x2 vs = rcp_nr2_neg(ny);
+              float p0, p1;
+              unpack2(ffma2(tr2, vs, pack2(part[s], part[s + 1])), p0, p1);
+              part[s] = p0;
+              part[s + 1] = p1;
+            }
 #else
 #pragma unroll
-          for (int s = 0; s < GT_G; ++s) {
-            // -k_s (u.z - cos a) log2(e) in FP64 (zx..bxs carry the exact 2^-896
-            // pre-scale of f64s_to_f32_alu), converted to FP32 with two ALU ops
-            const float x = f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs))));
+            for (int s = 0; s < GT_G; ++s) {
+              // -k_s (u.z - cos a) log2(e) in FP64 (zx..bxs carry the exact 2^-896
+              // pre-scale of f64s_to_f32_alu), converted to FP32 with two ALU ops
+              const float x = f64s_to_f32_alu(fma(pr.ux, zx[s], fma(pr.uy, zy[s], fma(pr.uz, zz[s], bxs))));
 #if GT_RCP == 1
-            const float vs = rcp_nr_neg(-1.0f - ex2_approx(fminf(x, 126.f)));
+              const float vs = rcp_nr_neg(-1.0f - ex2_approx(fminf(x, 126.f)));
 #else
-            const float vs = rcp_approx(1.0f + ex2_approx(x));
+              const float vs = rcp_approx(1.0f + ex2_approx(x));
 #endif
-            part[s] = fmaf(pr.tr, vs, part[s]);
-          }
+              part[s] = fmaf(pr.tr, vs, part[s]);
+            }
 #endif
           }
         }
