@@ -1045,9 +1045,11 @@ k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSr
 #define GH_PAIR_RCP 0
 #endif
 // packed FP32x2 arithmetic where pairs of sigmoids or entries meet (bit mask):
-// 1 split residuals (FADD2), 2 sigmoid denominators (FFMA2), 4 B-operand scaling (FMUL2)
+// 1 split residuals (FADD2), 2 sigmoid denominators (FFMA2), 4 B-operand scaling (FMUL2).
+// With the row-paired exponent arguments (GH_XPAIR) the residual pairs need register
+// moves: 2 alone is best (155.4 ms vs 156.2 with 3 and 157.2 with 7)
 #ifndef GH_PACKED
-#define GH_PACKED 3
+#define GH_PACKED 2
 #endif
 __device__ __forceinline__ void h16_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
