@@ -589,17 +589,6 @@ __device__ __forceinline__ void entries21(const PairF& q, float4 a, float* e) {
 // ── phase A of the GP info kernels on FP32x2 pairs: the same landmark against two voxels
 // (lo half: voxel A, hi half: voxel B), every operation of pair_prologue / entries21
 // issued once as FFMA2 / FMUL2 / FADD2 (rsqrt stays per lane on MUFU).
-__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 fsub2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 fneg2(f32x2 a) { return a ^ 0x8000000080000000ull; }
 struct PairF2 {
   f32x2 ux, uy, uz, w;
 };

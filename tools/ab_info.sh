@@ -4,6 +4,6 @@
 for i in 1 2; do
   for v in base "$@"; do
     if [ $v = base ]; then unset FIF_LIB; else export FIF_LIB=$PWD/$v; fi
-    echo "$v $(python tools/prof_build.py --kind info --reps 4 2>&1 | tail -1)"
+    echo "$v $(python tools/prof_build.py --kind ${KIND:-info} --reps 4 2>&1 | tail -1)"
   done
 done
