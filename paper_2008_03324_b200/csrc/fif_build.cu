@@ -1066,6 +1066,9 @@ __device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], u
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 constexpr int H16_BEXP = 13;  // |B'| < 2^14
+#ifndef GH_WARPS
+#define GH_WARPS 4  // warps (voxels) per CTA
+#endif
 #ifndef GH_MINB
 #define GH_MINB 3  // 12 warps per SM when the shared memory allows it (N_s <= 70)
 #endif
@@ -1077,18 +1080,18 @@ constexpr int H16_BEXP = 13;  // |B'| < 2^14
 #endif
 
 template <bool HAS_MASK, bool DEAD_TOP>
-__global__ void __launch_bounds__(GC_WARPS * 32, GH_MINB)
+__global__ void __launch_bounds__(GH_WARPS * 32, GH_MINB)
 k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1,
               int ns, int wpv, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax,
               float bx, double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int vpc = GC_WARPS / wpv;                                   // voxels per CTA
+  const int vpc = GH_WARPS / wpv;                                   // voxels per CTA
   float* eh = reinterpret_cast<float*>(smem_raw);                   // [vpc][GC_TILE][21] entries (FP32)
   float4* uu = reinterpret_cast<float4*>(eh + ((vpc * GC_TILE * 21 + 3) & ~3));  // [vpc][GC_TILE] bearings
   float4* tile = uu + vpc * GC_TILE;                                // [GC_TILE][2] landmarks
   float* cs = reinterpret_cast<float*>(tile + GC_TILE * 2);         // [vpc][6] centre hi/lo
-  int* tmax = reinterpret_cast<int*>(cs + 6 * GC_WARPS);            // [vpc] max |entry| of the tile (bits)
-  double* acc = reinterpret_cast<double*>(tmax + 2 * GC_WARPS);     // [GC_WARPS][rw][21] FP64 sums (valid rows only)
+  int* tmax = reinterpret_cast<int*>(cs + 6 * GH_WARPS);            // [vpc] max |entry| of the tile (bits)
+  double* acc = reinterpret_cast<double*>(tmax + 2 * GH_WARPS);     // [GH_WARPS][rw][21] FP64 sums (valid rows only)
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int vl = warp / wpv, mg = warp - vl * wpv;
@@ -1145,17 +1148,18 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
     __syncthreads();
     // phase A: per (voxel, landmark) bearing + 21 entries, and the voxel's max |entry|
 #if GH_PACKED_A
-    if (npairs == 2 * (int)blockDim.x) {  // vpc = 4: voxels pv and pv + 2 against landmark pj, packed
+    if (npairs == 2 * (int)blockDim.x) {  // two voxels per thread (pv, pv + blockDim / tile) against landmark pj, packed
       const int pv = t / GC_TILE, pj = t - pv * GC_TILE;  // warp-uniform pv (32 | GC_TILE)
       const float4 a = tile[2 * pj], b = tile[2 * pj + 1];
-      bool okA = b.w != 0.f && (vbase + pv) < v1, okB = b.w != 0.f && (vbase + pv + 2) < v1;
+      const int pv2 = pv + (int)blockDim.x / GC_TILE;  // the thread's second voxel
+      bool okA = b.w != 0.f && (vbase + pv) < v1, okB = b.w != 0.f && (vbase + pv2) < v1;
       if (HAS_MASK) {
         const int64_t i = base + pj;
         if (okA && mask[(vbase + pv - v0) * n_real + i] == 0) okA = false;
-        if (okB && mask[(vbase + pv + 2 - v0) * n_real + i] == 0) okB = false;
+        if (okB && mask[(vbase + pv2 - v0) * n_real + i] == 0) okB = false;
       }
       const float* cA = cs + 6 * pv;
-      const float* cB = cs + 6 * (pv + 2);
+      const float* cB = cs + 6 * pv2;
       const f32x2 ch2[3] = {pack2(cA[0], cB[0]), pack2(cA[1], cB[1]), pack2(cA[2], cB[2])};
       const f32x2 cl2[3] = {pack2(cA[3], cB[3]), pack2(cA[4], cB[4]), pack2(cA[5], cB[5])};
       const PairF2 q = pair_prologue2(a, b, ch2, cl2, inv_s2, okA, okB);
@@ -1171,10 +1175,10 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       }
       if (lane == 0) {
         atomicMax(&tmax[pv], __float_as_int(mxA));
-        atomicMax(&tmax[pv + 2], __float_as_int(mxB));
+        atomicMax(&tmax[pv2], __float_as_int(mxB));
       }
       float* dA = eh + (pv * GC_TILE + pj) * 21;
-      float* dB = eh + ((pv + 2) * GC_TILE + pj) * 21;
+      float* dB = eh + (pv2 * GC_TILE + pj) * 21;
 #pragma unroll
       for (int k2 = 0; k2 < 21; ++k2) unpack2(e[k2], dA[k2], dB[k2]);
       float uxA, uxB, uyA, uyB, uzA, uzB;
@@ -1182,7 +1186,7 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       unpack2(q.uy, uyA, uyB);
       unpack2(q.uz, uzA, uzB);
       uu[pv * GC_TILE + pj] = make_float4(uxA, uyA, uzA, 0.f);
-      uu[(pv + 2) * GC_TILE + pj] = make_float4(uxB, uyB, uzB, 0.f);
+      uu[pv2 * GC_TILE + pj] = make_float4(uxB, uyB, uzB, 0.f);
     } else
 #endif
     for (int pidx = t; pidx < npairs; pidx += blockDim.x) {
@@ -1575,12 +1579,12 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
   } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32))) {
     // tensor-pipe path, FP16 split (mma.sync m16n8k16): a warp covers 80 samples of one voxel
     const int wpv = (ns + 16 * GC_MT - 1) / (16 * GC_MT);
-    FIF_CHECK_ARG(wpv >= 1 && wpv <= GC_WARPS, "fif_build: N_s=%d too large for k_gp_info_h16", ns);
-    const int vpc = GC_WARPS / wpv;
+    FIF_CHECK_ARG(wpv >= 1 && wpv <= GH_WARPS, "fif_build: N_s=%d too large for k_gp_info_h16", ns);
+    const int vpc = GH_WARPS / wpv;
     const unsigned blocks_c = (unsigned)((rows + vpc - 1) / vpc);
     const int rw = ns < GC_MT * 16 ? ns : GC_MT * 16;
     size_t smem = sizeof(float) * ((vpc * GC_TILE * 21 + 3) & ~3) + sizeof(float4) * (vpc * GC_TILE + GC_TILE * 2) +
-                  sizeof(float) * 6 * GC_WARPS + sizeof(int) * 2 * GC_WARPS + sizeof(double) * GC_WARPS * rw * 21;
+                  sizeof(float) * 6 * GH_WARPS + sizeof(int) * 2 * GH_WARPS + sizeof(double) * GH_WARPS * rw * 21;
     static bool carve_h = false;
     if (!carve_h) {
       for (auto f : {k_gp_info_h16<true, true>, k_gp_info_h16<false, true>, k_gp_info_h16<true, false>,
@@ -1592,7 +1596,7 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     }
     const bool dead_top = wpv == 1 && (GC_MT - 1) * 16 + 8 >= ns;
 #define GH_LAUNCH(M, D)                                                                                        \
-  k_gp_info_h16<M, D><<<blocks_c, GC_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv, \
+  k_gp_info_h16<M, D><<<blocks_c, GH_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv, \
                                                             model->zs, d_mask, (float)inv_s2, (float)ax, (float)bx, \
                                                             d_out64, d_out32)
     if (has_mask) { if (dead_top) GH_LAUNCH(true, true); else GH_LAUNCH(true, false); }
