@@ -167,22 +167,72 @@ int fif_query_ex(int factor_kind, const fif_model* model, const fif_grid* grid, 
 int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, const double* d_points, int64_t n_points,
                const fif_camera* cam, double sigma, double* d_out, uint8_t* d_mask, void* stream);
 
-/* Matchability gates — replaces the range and view-cone parts of
- * Matchability.mask (field.py:143-165).  d_mask (rows, n_points) uint8, row-major:
+/* Scalar information metrics (kernels.py:602-608 _nb_metric_of / metric_id). */
+#define FIF_METRIC_DET 0
+#define FIF_METRIC_LMIN 1
+#define FIF_METRIC_TRACE 2
+
+/* Exact point-cloud metric at yaw-only poses — replaces kernels.pc_metric_yaw_batch
+ * (kernels.py:1599-1606 -> _nb_pc_metric_yaw_batch 611-625), the exact comparator behind
+ * rrt.ExactInfoRepr.metric_batch (rrt.py:54-71).  Per pose: R = Rz(yaw) r_base with the
+ * reference's operation order, the point-cloud 6x6 of fif_pc_fim, then det / lambda_min /
+ * trace.  d_positions (Q,3) f64; d_cos_sin (Q,2) f64 = cos, sin of each yaw, computed on
+ * the HOST (libm, like np.cos / np.sin; the device's cos / sin would move mask bits);
+ * r_base: HOST (3,3) row-major (rrt.R_CAM_MOUNT).  d_values (Q) f64.  Optional d_fim
+ * (Q,36) and d_mask (Q,N) as in fif_pc_fim.                                            */
+int fif_pc_metric_yaw(const double* d_positions, const double* d_cos_sin, int64_t q, const double* d_points,
+                      int64_t n_points, const fif_camera* cam, double sigma, const double* r_base, int metric,
+                      double* d_values, double* d_fim, uint8_t* d_mask, void* stream);
+
+/* Corner table of a batch of positions — the bit-exact indexing rule of the queries as a
+ * debug / parity entry point: kernels._nb_locate_nearest (kernels.py:628-635) and the
+ * trilinear corner block of _nb_query_fim (678-702; twin _np_trilinear_corners 247-272).
+ * d_index (Q,8) int64: the reference's x-major linear voxel indices (field.py:81-83);
+ * d_weight (Q,8) f64; d_status (Q) uint8 (FIF_STATUS_*).  Nearest: corner 0 only
+ * (weight 1), the other seven -1 / 0; out of field: all eight -1 / 0.  d_index and
+ * d_weight are optional.                                                              */
+int fif_locate(const fif_grid* grid, const double* d_positions, int64_t q, int mode, int64_t* d_index,
+               double* d_weight, uint8_t* d_status, void* stream);
+
+/* Matchability gates — replaces Matchability.mask (field.py:143-177) for range, view
+ * cone and ObstacleWorld occlusion (world.segment_blocked, world.py:96-140).  d_mask (rows, n_points) uint8, row-major:
  * 1 = the (centre, landmark) pair contributes.  FP64, bit-identical with the
  * reference's numpy arithmetic (norm order (x^2 + y^2) + z^2; einsum order
- * (x + z) + y).  Occlusion and Python predicates stay on the host.          */
+ * (x + z) + y; occlusion as fif_gate.cuh documents).  Python predicates stay on
+ * the host, as in the reference.                                               */
 #define FIF_MATCH_NEAR 1u  /* dist >= d_near     */
 #define FIF_MATCH_FAR 2u   /* dist <= d_far      */
 #define FIF_MATCH_CONE 4u  /* cos(angle to view_dir) >= cos_beta (needs d_view_dirs (N,3)) */
+#define FIF_MATCH_OCCLUDE 8u /* sight line centre -> landmark not blocked (world.segment_blocked) */
 typedef struct fif_match {
   double d_near;
   double d_far;
   double cos_beta;
   uint32_t flags;
+  /* occluders of an ObstacleWorld (world.py:18-56), DEVICE arrays:
+   * spheres (n_spheres, 4) = centre xyz, radius; boxes (n_boxes, 6) = lo xyz, hi xyz */
+  const double* spheres;
+  int64_t n_spheres;
+  const double* boxes;
+  int64_t n_boxes;
 } fif_match;
 int fif_match_mask(const fif_match* match, const double* d_centers, int64_t rows, const double* d_points,
                    const double* d_view_dirs, int64_t n_points, uint8_t* d_mask, void* stream);
+
+/* Per-centre occupancy under the gates: d_any (rows) uint8, 1 iff some landmark matches
+ * (the reference gives a voxel a row iff its mask row has a 1, field.py:253-257).       */
+int fif_match_any(const fif_match* match, const double* d_centers, int64_t rows, const double* d_points,
+                  const double* d_view_dirs, int64_t n_points, uint8_t* d_any, void* stream);
+
+/* Matchability-gated build with the gates FUSED into the build kernels' pair loops (no
+ * (V, N) mask is materialised) — replaces the masked path of Field.build (field.py:229-268:
+ * Matchability.mask, then build_*_factors(..., mask)).  Voxels: the (rows, 3) f64 centres
+ * (normally the occupied voxels from fif_match_any, in the reference's row order).  Output
+ * layout and d_scratch as fif_build.  match->flags == 0 builds unmasked.                  */
+int fif_build_matched(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
+                      const double* d_centers, int64_t rows, const fif_match* match, const double* d_view_dirs,
+                      double sigma, uint32_t build_flags, void* d_scratch, double* d_out64, float* d_out32,
+                      void* stream);
 
 /* Number of kernel launches issued by this library since load (for bench
  * accounting of gpu_launches). */

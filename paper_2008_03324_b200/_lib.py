@@ -22,11 +22,12 @@ Q_TRACE, Q_FULL, Q_GRAD, Q_DET, Q_LMIN, Q_FIELD_F64 = 1, 2, 4, 8, 16, 32
 BUILD_EXACT = 1
 BUILD_SIMT = 2
 BUILD_TF32 = 4
+METRIC_IDS = {"det": 0, "lmin": 1, "trace": 2}  # kernels.metric_id (kernels.py:602-608)
 
 EXPORTED = (
     "fif_abi_version", "fif_last_error", "fif_grid_centers", "fif_build_scratch_bytes", "fif_build",
     "fif_export_reference", "fif_query", "fif_query_ex", "fif_pc_fim", "fif_match_mask",
-    "fif_launch_count",
+    "fif_launch_count", "fif_locate", "fif_pc_metric_yaw", "fif_match_any", "fif_build_matched",
 )
 
 
@@ -56,10 +57,11 @@ class QueryOut(ctypes.Structure):
 
 class Match(ctypes.Structure):
     _fields_ = [("d_near", ctypes.c_double), ("d_far", ctypes.c_double), ("cos_beta", ctypes.c_double),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("spheres", ctypes.c_void_p), ("n_spheres", ctypes.c_int64),
+                ("boxes", ctypes.c_void_p), ("n_boxes", ctypes.c_int64)]
 
 
-MATCH_NEAR, MATCH_FAR, MATCH_CONE = 1, 2, 4
+MATCH_NEAR, MATCH_FAR, MATCH_CONE, MATCH_OCCLUDE = 1, 2, 4, 8
 
 
 class Camera(ctypes.Structure):
@@ -105,6 +107,16 @@ def load():
         L.fif_match_mask.argtypes = [ctypes.POINTER(Match), _p, _i64, _p, _p, _i64, _p, _p]
         L.fif_pc_fim.restype = _int
         L.fif_pc_fim.argtypes = [_p, _p, _i64, _p, _i64, ctypes.POINTER(Camera), _d, _p, _p, _p]
+        L.fif_locate.restype = _int
+        L.fif_locate.argtypes = [ctypes.POINTER(Grid), _p, _i64, _int, _p, _p, _p, _p]
+        L.fif_pc_metric_yaw.restype = _int
+        L.fif_pc_metric_yaw.argtypes = [_p, _p, _i64, _p, _i64, ctypes.POINTER(Camera), _d,
+                                        ctypes.POINTER(ctypes.c_double * 9), _int, _p, _p, _p, _p]
+        L.fif_match_any.restype = _int
+        L.fif_match_any.argtypes = [ctypes.POINTER(Match), _p, _i64, _p, _p, _i64, _p, _p]
+        L.fif_build_matched.restype = _int
+        L.fif_build_matched.argtypes = [_int, ctypes.POINTER(Model), _p, _i64, _p, _i64, ctypes.POINTER(Match), _p, _d,
+                                        ctypes.c_uint32, _p, _p, _p, _p]
         if L.fif_abi_version() != 1:
             raise FifCudaError(f"libfif_b200 ABI {L.fif_abi_version()} != 1")
         _lib = L

@@ -20,6 +20,7 @@
 #include <cuda_fp16.h>
 
 #include "fif_common.cuh"
+#include "fif_gate.cuh"
 
 namespace fif {
 
@@ -181,7 +182,7 @@ __device__ __forceinline__ double entry64(int e, const PairD& q, double4 p, doub
 template <bool EXACT, bool HAS_MASK>
 __global__ void __launch_bounds__(QD_THREADS) k_quad_trace(const double4* __restrict__ lm, int64_t n_pad, int64_t n_real,
                                                            VoxSrc src, int64_t v0, int64_t v1,
-                                                           const uint8_t* __restrict__ mask, double inv_s2,
+                                                           const PairGate gate, double inv_s2,
                                                            double* __restrict__ out) {
   __shared__ double4 tile[QD_TILE];
   const int64_t v = v0 + blockIdx.x * (int64_t)QD_THREADS + threadIdx.x;
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(QD_THREADS) k_quad_trace(const double4* __rest
       bool keep = active;
       if (HAS_MASK) {
         int64_t i = base + j;
-        keep = keep && i < n_real && mask[(v - v0) * n_real + i] != 0;
+        keep = keep && i < n_real && gate_keep(gate, v, i);
       }
       const PairD q = pair64<EXACT>(p, cx, cy, cz, inv_s2, keep);
       double tr;
@@ -262,7 +263,7 @@ __host__ __device__ constexpr int qidx(int G, int t) {
 template <int G, bool EXACT, bool HAS_MASK>
 __device__ __forceinline__ void quad_info_tiles(const double4* __restrict__ lm, double4* tile, double* rec,
                                                 int64_t n_pad, int64_t n_real, int64_t v, int64_t v0, bool active,
-                                                double cx, double cy, double cz, const uint8_t* __restrict__ mask,
+                                                double cx, double cy, double cz, const PairGate gate,
                                                 double inv_s2, double* __restrict__ out) {
   constexpr int NE = QGroup<G>::NE;
   constexpr int RS = QI_TILE * 32;  // stride between record components
@@ -281,7 +282,7 @@ __device__ __forceinline__ void quad_info_tiles(const double4* __restrict__ lm, 
       bool keep = active;
       if (HAS_MASK) {
         const int64_t i = base + j;
-        keep = keep && i < n_real && mask[(v - v0) * n_real + i] != 0;
+        keep = keep && i < n_real && gate_keep(gate, v, i);
       }
       const PairD q = pair64<EXACT>(p, cx, cy, cz, inv_s2, keep);
       double c2x, c2y, c2z;
@@ -338,7 +339,7 @@ __device__ __forceinline__ void quad_info_tiles(const double4* __restrict__ lm, 
 template <bool EXACT, bool HAS_MASK>
 __global__ void __launch_bounds__(QI_THREADS, QI_MINB) k_quad_info(const double4* __restrict__ lm, int64_t n_pad, int64_t n_real,
                                                           VoxSrc src, int64_t v0, int64_t v1,
-                                                          const uint8_t* __restrict__ mask, double inv_s2,
+                                                          const PairGate gate, double inv_s2,
                                                           double* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char qi_raw[];
   double4* tile = reinterpret_cast<double4*>(qi_raw);                        // [QI_TILE]
@@ -349,10 +350,10 @@ __global__ void __launch_bounds__(QI_THREADS, QI_MINB) k_quad_info(const double4
   double cx, cy, cz;
   voxel_center(src, active ? v : v0, cx, cy, cz);
   switch (warp) {
-    case 0: quad_info_tiles<0, EXACT, HAS_MASK>(lm, tile, rec, n_pad, n_real, v, v0, active, cx, cy, cz, mask, inv_s2, out); break;
-    case 1: quad_info_tiles<1, EXACT, HAS_MASK>(lm, tile, rec, n_pad, n_real, v, v0, active, cx, cy, cz, mask, inv_s2, out); break;
-    case 2: quad_info_tiles<2, EXACT, HAS_MASK>(lm, tile, rec, n_pad, n_real, v, v0, active, cx, cy, cz, mask, inv_s2, out); break;
-    default: quad_info_tiles<3, EXACT, HAS_MASK>(lm, tile, rec, n_pad, n_real, v, v0, active, cx, cy, cz, mask, inv_s2, out); break;
+    case 0: quad_info_tiles<0, EXACT, HAS_MASK>(lm, tile, rec, n_pad, n_real, v, v0, active, cx, cy, cz, gate, inv_s2, out); break;
+    case 1: quad_info_tiles<1, EXACT, HAS_MASK>(lm, tile, rec, n_pad, n_real, v, v0, active, cx, cy, cz, gate, inv_s2, out); break;
+    case 2: quad_info_tiles<2, EXACT, HAS_MASK>(lm, tile, rec, n_pad, n_real, v, v0, active, cx, cy, cz, gate, inv_s2, out); break;
+    default: quad_info_tiles<3, EXACT, HAS_MASK>(lm, tile, rec, n_pad, n_real, v, v0, active, cx, cy, cz, gate, inv_s2, out); break;
   }
 }
 
@@ -396,7 +397,7 @@ struct __align__(16) PairT {
 template <bool HAS_MASK>
 __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* __restrict__ pts, int64_t n_real, VoxSrc src,
                                                          int64_t v0, int64_t v1, int vb, int ns,
-                                                         const double* __restrict__ zs, const uint8_t* __restrict__ mask,
+                                                         const double* __restrict__ zs, const PairGate gate,
                                                          double inv_s2, double ax, double bx,
                                                          double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(GT_THREADS, GT_MINB) k_gp_trace(const double* 
       const double dx = px - cen[3 * pv], dy = py - cen[3 * pv + 1], dz = pz - cen[3 * pv + 2];
       const double n2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
       bool ok = i < n_real && n2 >= 1e-300 && (vbase + pv) < v1;  // kernels.py:494
-      if (HAS_MASK && ok) ok = mask[(vbase + pv - v0) * n_real + i] != 0;
+      if (HAS_MASK && ok) ok = gate_keep(gate, vbase + pv, i);
       PairT pr;
       if (ok) {
         const double rn = rsqrt_nr(n2);
@@ -654,7 +655,7 @@ constexpr int GI_VB_THREADS = 128;
 template <bool HAS_MASK>
 __global__ void __launch_bounds__(GI_VB_THREADS, 2)
 k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1, int vb,
-          int ns, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax, float bx,
+          int ns, const double* __restrict__ zs, const PairGate gate, float inv_s2, float ax, float bx,
           double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tpv = (ns + GI_G - 1) / GI_G;                        // threads per voxel
@@ -708,7 +709,7 @@ k_gp_info(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc s
       if ((vbase + pv) >= v1) b.w = 0.f;
       if (HAS_MASK) {
         int64_t i = base + pj;
-        if (b.w != 0.f && mask[(vbase + pv - v0) * n_real + i] == 0) b.w = 0.f;
+        if (b.w != 0.f && !gate_keep(gate, vbase + pv, i)) b.w = 0.f;
       }
       const float* c = cs + 6 * pv;
       const float ch[3] = {c[0], c[1], c[2]}, cl[3] = {c[3], c[4], c[5]};
@@ -837,7 +838,7 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
 template <bool HAS_MASK, bool DEAD_TOP>
 __global__ void __launch_bounds__(GC_WARPS * 32, 2)
 k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1,
-             int ns, int wpv, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax,
+             int ns, int wpv, const double* __restrict__ zs, const PairGate gate, float inv_s2, float ax,
              float bx, double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int vpc = GC_WARPS / wpv;                                   // voxels per CTA
@@ -895,7 +896,7 @@ k_gp_info_tc(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSr
       if ((vbase + pv) >= v1) b.w = 0.f;
       if (HAS_MASK) {
         const int64_t i = base + pj;
-        if (b.w != 0.f && mask[(vbase + pv - v0) * n_real + i] == 0) b.w = 0.f;
+        if (b.w != 0.f && !gate_keep(gate, vbase + pv, i)) b.w = 0.f;
       }
       const float* cc = cs + 6 * pv;
       const float ch[3] = {cc[0], cc[1], cc[2]}, cl[3] = {cc[3], cc[4], cc[5]};
@@ -1082,7 +1083,7 @@ constexpr int H16_BEXP = 13;  // |B'| < 2^14
 template <bool HAS_MASK, bool DEAD_TOP>
 __global__ void __launch_bounds__(GH_WARPS * 32, GH_MINB)
 k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxSrc src, int64_t v0, int64_t v1,
-              int ns, int wpv, const double* __restrict__ zs, const uint8_t* __restrict__ mask, float inv_s2, float ax,
+              int ns, int wpv, const double* __restrict__ zs, const PairGate gate, float inv_s2, float ax,
               float bx, double* __restrict__ out64, float* __restrict__ out32) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int vpc = GH_WARPS / wpv;                                   // voxels per CTA
@@ -1155,8 +1156,8 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       bool okA = b.w != 0.f && (vbase + pv) < v1, okB = b.w != 0.f && (vbase + pv2) < v1;
       if (HAS_MASK) {
         const int64_t i = base + pj;
-        if (okA && mask[(vbase + pv - v0) * n_real + i] == 0) okA = false;
-        if (okB && mask[(vbase + pv2 - v0) * n_real + i] == 0) okB = false;
+        if (okA && !gate_keep(gate, vbase + pv, i)) okA = false;
+        if (okB && !gate_keep(gate, vbase + pv2, i)) okB = false;
       }
       const float* cA = cs + 6 * pv;
       const float* cB = cs + 6 * pv2;
@@ -1195,7 +1196,7 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
       if ((vbase + pv) >= v1) b.w = 0.f;
       if (HAS_MASK) {
         const int64_t i = base + pj;
-        if (b.w != 0.f && mask[(vbase + pv - v0) * n_real + i] == 0) b.w = 0.f;
+        if (b.w != 0.f && !gate_keep(gate, vbase + pv, i)) b.w = 0.f;
       }
       const float* cc = cs + 6 * pv;
       const float ch[3] = {cc[0], cc[1], cc[2]}, cl[3] = {cc[3], cc[4], cc[5]};
@@ -1458,10 +1459,12 @@ extern "C" int64_t fif_build_scratch_bytes(int64_t n_points) {
   return n_pad * 2 * (int64_t)sizeof(float4);
 }
 
-extern "C" int fif_build(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
-                         const fif_grid* grid, const double* d_centers, int64_t v_begin, int64_t v_end,
-                         const uint8_t* d_mask, double sigma, uint32_t build_flags, void* d_scratch, double* d_out64,
-                         float* d_out32, void* stream) {
+// The build proper; `gate` (when has_gate) is the per-pair matchability test: an explicit
+// mask (fif_build) or the fused gate predicates (fif_build_matched).
+static int build_impl(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
+                      const fif_grid* grid, const double* d_centers, int64_t v_begin, int64_t v_end, PairGate gate,
+                      bool has_gate, double sigma, uint32_t build_flags, void* d_scratch, double* d_out64,
+                      float* d_out32, void* stream) {
   FIF_CHECK_ARG(model != nullptr, "fif_build: model is NULL");
   FIF_CHECK_ARG(factor_kind == FIF_KIND_INFO || factor_kind == FIF_KIND_TRACE, "fif_build: bad factor_kind %d",
                 factor_kind);
@@ -1504,7 +1507,8 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     }
   }
   const double inv_s2 = 1.0 / (sigma * sigma);
-  const bool has_mask = d_mask != nullptr;
+  const bool has_mask = has_gate;
+  gate.src = src;
   int64_t n_pad = ((n_points + kLmPad - 1) / kLmPad) * kLmPad;
   float4* lm = reinterpret_cast<float4*>(d_scratch);
   FIF_CHECK_ARG(d_scratch != nullptr || (model->kind == FIF_MODEL_GP && trace), "fif_build: d_scratch is NULL");
@@ -1521,7 +1525,7 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     FIF_CHECK_LAUNCH("k_prep_landmarks64");
     if (trace) {
       unsigned blocks = (unsigned)((rows + QD_THREADS - 1) / QD_THREADS);
-#define QT_LAUNCH(E, M) k_quad_trace<E, M><<<blocks, QD_THREADS, 0, st>>>(lm64, n_pad, n_points, src, v_begin, v_end, d_mask, inv_s2, d_out64)
+#define QT_LAUNCH(E, M) k_quad_trace<E, M><<<blocks, QD_THREADS, 0, st>>>(lm64, n_pad, n_points, src, v_begin, v_end, gate, inv_s2, d_out64)
       if (exact) { if (has_mask) QT_LAUNCH(true, true); else QT_LAUNCH(true, false); }
       else { if (has_mask) QT_LAUNCH(false, true); else QT_LAUNCH(false, false); }
 #undef QT_LAUNCH
@@ -1529,14 +1533,14 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     } else {
       unsigned blocks = (unsigned)((rows + 31) / 32);
       const size_t qi_smem = sizeof(double4) * QI_TILE + sizeof(double) * 7 * QI_TILE * 32;
-      static bool qi_attr = false;
-      if (!qi_attr) {
+      static std::atomic<uint64_t> qi_attr{0};
+      if (needs_setup(qi_attr)) {
         for (auto f : {k_quad_info<true, true>, k_quad_info<true, false>, k_quad_info<false, true>, k_quad_info<false, false>})
           cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qi_smem);
-        qi_attr = true;
+        mark_setup(qi_attr);
       }
 #define QI_LAUNCH(E, M) \
-  k_quad_info<E, M><<<blocks, QI_THREADS, qi_smem, st>>>(lm64, n_pad, n_points, src, v_begin, v_end, d_mask, inv_s2, d_out64)
+  k_quad_info<E, M><<<blocks, QI_THREADS, qi_smem, st>>>(lm64, n_pad, n_points, src, v_begin, v_end, gate, inv_s2, d_out64)
       if (exact) { if (has_mask) QI_LAUNCH(true, true); else QI_LAUNCH(true, false); }
       else { if (has_mask) QI_LAUNCH(false, true); else QI_LAUNCH(false, false); }
 #undef QI_LAUNCH
@@ -1561,20 +1565,20 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     FIF_CHECK_ARG(threads_t <= GT_THREADS, "fif_build: N_s=%d too large for k_gp_trace", ns);
     const unsigned blocks_t = (unsigned)((rows + vbt - 1) / vbt);
     size_t smem = sizeof(PairT) * vbt * (GT_TILE + 1) + sizeof(double) * 3 * vbt + sizeof(double) * 3 * GT_TILE;
-    static bool carve = false;
-    if (!carve) {
+    static std::atomic<uint64_t> carve{0};
+    if (needs_setup(carve)) {
       for (auto f : {k_gp_trace<true>, k_gp_trace<false>}) {
         cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
       }
-      carve = true;
+      mark_setup(carve);
     }
     if (has_mask)
       k_gp_trace<true><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns, model->zs,
-                                                          d_mask, inv_s2, ax, bx, d_out64, d_out32);
+                                                          gate, inv_s2, ax, bx, d_out64, d_out32);
     else
       k_gp_trace<false><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns,
-                                                           model->zs, d_mask, inv_s2, ax, bx, d_out64, d_out32);
+                                                           model->zs, gate, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
   } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32))) {
     // tensor-pipe path, FP16 split (mma.sync m16n8k16): a warp covers 80 samples of one voxel
@@ -1585,19 +1589,19 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     const int rw = ns < GC_MT * 16 ? ns : GC_MT * 16;
     size_t smem = sizeof(float) * ((vpc * GC_TILE * 21 + 3) & ~3) + sizeof(float4) * (vpc * GC_TILE + GC_TILE * 2) +
                   sizeof(float) * 6 * GH_WARPS + sizeof(int) * 2 * GH_WARPS + sizeof(double) * GH_WARPS * rw * 21;
-    static bool carve_h = false;
-    if (!carve_h) {
+    static std::atomic<uint64_t> carve_h{0};
+    if (needs_setup(carve_h)) {
       for (auto f : {k_gp_info_h16<true, true>, k_gp_info_h16<false, true>, k_gp_info_h16<true, false>,
                      k_gp_info_h16<false, false>}) {
         cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
-      carve_h = true;
+      mark_setup(carve_h);
     }
     const bool dead_top = wpv == 1 && (GC_MT - 1) * 16 + 8 >= ns;
 #define GH_LAUNCH(M, D)                                                                                        \
   k_gp_info_h16<M, D><<<blocks_c, GH_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv, \
-                                                            model->zs, d_mask, (float)inv_s2, (float)ax, (float)bx, \
+                                                            model->zs, gate, (float)inv_s2, (float)ax, (float)bx, \
                                                             d_out64, d_out32)
     if (has_mask) { if (dead_top) GH_LAUNCH(true, true); else GH_LAUNCH(true, false); }
     else { if (dead_top) GH_LAUNCH(false, true); else GH_LAUNCH(false, false); }
@@ -1611,21 +1615,21 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     const unsigned blocks_c = (unsigned)((rows + vpc - 1) / vpc);
     size_t smem = sizeof(float) * (vpc * GC_TILE * 24) + sizeof(float4) * (vpc * GC_TILE + GC_TILE * 2) +
                   sizeof(float) * ((6 * vpc + 1) & ~1) + sizeof(double) * GC_WARPS * GC_MT * GC_NT * 4 * 32;
-    static bool carve_tc = false;
-    if (!carve_tc) {
+    static std::atomic<uint64_t> carve_tc{0};
+    if (needs_setup(carve_tc)) {
       for (auto f : {k_gp_info_tc<true, true>, k_gp_info_tc<false, true>, k_gp_info_tc<true, false>,
                      k_gp_info_tc<false, false>}) {
         cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
-      carve_tc = true;
+      mark_setup(carve_tc);
     }
     // the top 8 rows of the last warp's last m-tile are padding for every warp of the
     // voxel only when wpv == 1; with wpv > 1 earlier warps' tiles are real
     const bool dead_top = wpv == 1 && (GC_MT - 1) * 16 + 8 >= ns;
 #define GC_LAUNCH(M, D)                                                                                       \
   k_gp_info_tc<M, D><<<blocks_c, GC_WARPS * 32, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, ns, wpv, \
-                                                           model->zs, d_mask, (float)inv_s2, (float)ax, (float)bx, \
+                                                           model->zs, gate, (float)inv_s2, (float)ax, (float)bx, \
                                                            d_out64, d_out32)
     if (has_mask) { if (dead_top) GC_LAUNCH(true, true); else GC_LAUNCH(true, false); }
     else { if (dead_top) GC_LAUNCH(false, true); else GC_LAUNCH(false, false); }
@@ -1640,24 +1644,56 @@ extern "C" int fif_build(int factor_kind, const fif_model* model, const double* 
     const unsigned blocks_i = (unsigned)((rows + vbi - 1) / vbi);
     size_t smem = sizeof(double) * 21 * GI_G * threads_i + sizeof(float4) * (vbi * (GI_TILE * 6 + 1) + GI_TILE * 2) +
                   sizeof(float) * 6 * vbi;
-    static bool carve = false;
-    if (!carve) {  // prefer the max shared-memory carveout so several CTAs fit per SM
+    static std::atomic<uint64_t> carve{0};
+    if (needs_setup(carve)) {  // prefer the max shared-memory carveout so several CTAs fit per SM
       for (auto f : {k_gp_info<true>, k_gp_info<false>}) {
         cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
-      carve = true;
+      mark_setup(carve);
     }
     if (has_mask)
       k_gp_info<true><<<blocks_i, threads_i, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, vbi, ns, model->zs,
-                                                         d_mask, (float)inv_s2, (float)ax, (float)bx, d_out64, d_out32);
+                                                         gate, (float)inv_s2, (float)ax, (float)bx, d_out64, d_out32);
     else
       k_gp_info<false><<<blocks_i, threads_i, smem, st>>>(lm, n_pad, n_points, src, v_begin, v_end, vbi, ns,
-                                                          model->zs, d_mask, (float)inv_s2, (float)ax, (float)bx,
+                                                          model->zs, gate, (float)inv_s2, (float)ax, (float)bx,
                                                           d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_info");
   }
   return FIF_OK;
+}
+
+extern "C" int fif_build(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
+                         const fif_grid* grid, const double* d_centers, int64_t v_begin, int64_t v_end,
+                         const uint8_t* d_mask, double sigma, uint32_t build_flags, void* d_scratch, double* d_out64,
+                         float* d_out32, void* stream) {
+  PairGate gate{};
+  gate.mask = d_mask;
+  gate.v0 = v_begin;
+  gate.n = n_points;
+  return build_impl(factor_kind, model, d_points, n_points, grid, d_centers, v_begin, v_end, gate, d_mask != nullptr,
+                    sigma, build_flags, d_scratch, d_out64, d_out32, stream);
+}
+
+extern "C" int fif_build_matched(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
+                                 const double* d_centers, int64_t rows, const fif_match* match,
+                                 const double* d_view_dirs, double sigma, uint32_t build_flags, void* d_scratch,
+                                 double* d_out64, float* d_out32, void* stream) {
+  FIF_CHECK_ARG(match != nullptr && d_centers != nullptr, "fif_build_matched: NULL match / centres");
+  FIF_CHECK_ARG(!(match->flags & FIF_MATCH_CONE) || d_view_dirs,
+                "fif_build_matched: view cone requires landmark view directions");
+  FIF_CHECK_ARG(!(match->flags & FIF_MATCH_OCCLUDE) || ((match->n_spheres == 0 || match->spheres) &&
+                                                        (match->n_boxes == 0 || match->boxes)),
+                "fif_build_matched: occlusion needs the sphere / box arrays");
+  PairGate gate{};
+  gate.m = *match;
+  gate.pts = d_points;
+  gate.vdir = d_view_dirs;
+  gate.v0 = 0;
+  gate.n = n_points;
+  return build_impl(factor_kind, model, d_points, n_points, nullptr, d_centers, 0, rows, gate, match->flags != 0,
+                    sigma, build_flags, d_scratch, d_out64, d_out32, stream);
 }
 
 extern "C" int fif_export_reference(int factor_kind, const fif_model* model, const double* d_in64, int64_t rows,

@@ -17,6 +17,18 @@ void set_error(const char* fmt, ...) {
 }
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+int num_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int v = cache[dev & 63].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 __global__ void k_centers(VoxSrc s, int order, int64_t v0, int64_t v1, double* __restrict__ out) {
   int64_t v = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (v >= v1) return;

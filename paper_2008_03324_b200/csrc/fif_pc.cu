@@ -12,6 +12,7 @@
 // evaluated exactly otherwise.  Visible landmarks are compacted through a
 // per-warp smem queue so the FP32 6x6 accumulation runs on full warps.
 #include "fif_common.cuh"
+#include "fif_linalg.cuh"
 
 #include <cub/cub.cuh>
 
@@ -409,6 +410,52 @@ __global__ void k_pc_keys(const double* __restrict__ rot, const double* __restri
   idx[q] = (int32_t)q;
 }
 
+// World-from-camera rotation of a yaw-only pose, R = Rz(yaw) R_base, in the reference's
+// operation order (kernels.py:615-621): row 0 = c b0 - s b1, row 1 = s b0 + c b1, row 2 = b2,
+// every product and sum rounded separately (numba emits no FMA here).  cos / sin come from
+// the host (libm), like the reference's np.cos / np.sin.
+struct Mat3 {
+  double m[9];
+};
+__global__ void k_yaw_rot(const double* __restrict__ cs, int64_t q, Mat3 b, double* __restrict__ rot) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  const double c = cs[2 * i], s = cs[2 * i + 1];
+  double* r = rot + 9 * i;
+#pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    r[col] = __dsub_rn(__dmul_rn(c, b.m[col]), __dmul_rn(s, b.m[3 + col]));
+    r[3 + col] = __dadd_rn(__dmul_rn(s, b.m[col]), __dmul_rn(c, b.m[3 + col]));
+    r[6 + col] = b.m[6 + col];
+  }
+}
+
+// Scalar metric of each 6x6 (kernels.py:602-608 _nb_metric_of): 0 det (partial-pivot LU),
+// 1 smallest eigenvalue (cyclic Jacobi), 2 trace (diagonal summed left to right).
+__global__ void k_metric6(const double* __restrict__ fim, int64_t q, int mid, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  const double* f = fim + 36 * i;
+  if (mid == FIF_METRIC_TRACE) {
+    double t = f[0];
+#pragma unroll
+    for (int k = 1; k < 6; ++k) t = __dadd_rn(t, f[7 * k]);
+    out[i] = t;
+    return;
+  }
+  double a[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) a[k] = f[k];
+  if (mid == FIF_METRIC_DET) {
+    bool ok;
+    double inv[36];
+    out[i] = det6_core<false>(a, inv, ok);
+  } else {
+    double v[6];
+    out[i] = lmin6_core<false>(a, v);
+  }
+}
+
 }  // namespace fif
 
 using namespace fif;
@@ -428,7 +475,7 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
   }
   FIF_CHECK_ARG(d_points != nullptr, "fif_pc_fim: NULL points");
   int64_t need = (q + PC_WARPS - 1) / PC_WARPS;
-  int64_t cap = (int64_t)kSMs;  // persistent: one CTA (16 warps, ~190 KB smem) per SM
+  int64_t cap = (int64_t)num_sms();  // persistent: one CTA (16 warps, ~190 KB smem) per SM
   unsigned blocks = (unsigned)(need < cap ? need : cap);
   const float inv_s2 = (float)(1.0 / (sigma * sigma));
   float4* ptab = nullptr;
@@ -441,18 +488,18 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
   k_pc_prep<<<(unsigned)((n_points + 255) / 256), 256, 0, st>>>(d_points, n_points, ptab, p1max);
   FIF_CHECK_LAUNCH("k_pc_prep");
   const size_t smem = sizeof(float4) * (2 * PC_NBUF * PC_TILE + PC_WARPS * PC_QCAP * 2) + 2 * PC_NBUF * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (needs_setup(attr)) {
     for (auto f : {k_pc_fim<true>, k_pc_fim<false>}) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
-    attr = true;
+    mark_setup(attr);
   }
   // similar poses share a CTA (load balance across its pose warps)
   int32_t* perm = nullptr;
   unsigned char* sbuf = nullptr;
-  if (q >= (int64_t)PC_WARPS * kSMs * 4 && q < (int64_t)INT32_MAX) {
+  if (q >= (int64_t)PC_WARPS * num_sms() * 4 && q < (int64_t)INT32_MAX) {
     size_t temp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (const int32_t*)nullptr, (int32_t*)nullptr, (int)q, 0, 19, st);
@@ -482,4 +529,41 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
   cudaFreeAsync(ptab, st);
   FIF_CHECK_LAUNCH("k_pc_fim");
   return FIF_OK;
+}
+
+extern "C" int fif_pc_metric_yaw(const double* d_positions, const double* d_cos_sin, int64_t q, const double* d_points,
+                                 int64_t n_points, const fif_camera* cam, double sigma, const double* r_base, int metric,
+                                 double* d_values, double* d_fim, uint8_t* d_mask, void* stream) {
+  FIF_CHECK_ARG(cam != nullptr && r_base != nullptr, "fif_pc_metric_yaw: NULL camera / r_base");
+  FIF_CHECK_ARG(metric == FIF_METRIC_DET || metric == FIF_METRIC_LMIN || metric == FIF_METRIC_TRACE,
+                "fif_pc_metric_yaw: unknown metric %d", metric);
+  FIF_CHECK_ARG(q >= 0 && n_points >= 0, "fif_pc_metric_yaw: negative size");
+  if (q == 0) return FIF_OK;
+  FIF_CHECK_ARG(d_positions && d_cos_sin && d_values, "fif_pc_metric_yaw: NULL pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  Mat3 b;
+  for (int k = 0; k < 9; ++k) b.m[k] = r_base[k];
+  double* buf = nullptr;
+  const size_t bytes = sizeof(double) * (size_t)q * (9 + (d_fim ? 0 : 36));
+  if (cudaMallocAsync(&buf, bytes, st) != cudaSuccess) {
+    set_error("fif_pc_metric_yaw: cudaMallocAsync of %zu bytes failed", bytes);
+    return FIF_ERR_CUDA;
+  }
+  double* rot = buf;
+  double* fim = d_fim ? d_fim : buf + 9 * q;
+  k_yaw_rot<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(d_cos_sin, q, b, rot);
+  FIF_CHECK_LAUNCH("k_yaw_rot");
+  int rc = fif_pc_fim(rot, d_positions, q, d_points, n_points, cam, sigma, fim, d_mask, stream);
+  if (rc == FIF_OK) {
+    k_metric6<<<(unsigned)((q + 127) / 128), 128, 0, st>>>(fim, q, metric, d_values);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_error("k_metric6: %s", cudaGetErrorString(e));
+      rc = FIF_ERR_CUDA;
+    } else {
+      count_launch();
+    }
+  }
+  cudaFreeAsync(buf, st);
+  return rc;
 }

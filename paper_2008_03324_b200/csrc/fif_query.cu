@@ -13,6 +13,7 @@
 // the field can hold the pre-kinv sums S in FP32.  The field
 // rows are streamed once per corner (HBM-bound) and blended in FP64.
 #include "fif_common.cuh"
+#include "fif_linalg.cuh"
 
 #include <cstdlib>
 
@@ -79,164 +80,6 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-// 6x6 determinant (partial-pivot LU) and smallest eigenvalue (cyclic Jacobi), FP64.
-// Every loop is fully unrolled with compile-time indices (row swaps and the pivot
-// permutation as selects), so the matrices stay in registers instead of local memory.
-// Arithmetic order is that of the straightforward loops (and of the oracle's).
-__host__ __device__ constexpr int pack_r(int x) { return x < 6 ? 0 : x < 11 ? 1 : x < 15 ? 2 : x < 18 ? 3 : x < 20 ? 4 : 5; }
-__host__ __device__ constexpr int pack_c(int x) { return pack_r(x) + x - (pack_r(x) * 6 - pack_r(x) * (pack_r(x) - 1) / 2); }
-
-// LU with partial pivoting (rows swapped whole, multipliers kept below the diagonal so
-// P A = L U); returns det, or 0 with ok = false for a singular matrix.  INV: F^-1.
-template <bool INV>
-__device__ __forceinline__ double det6_core(double (&a)[36], double (&inv)[36], bool& ok) {
-  int perm[6];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) perm[i] = i;
-  double det = 1.0;
-  ok = false;
-#pragma unroll
-  for (int c = 0; c < 6; ++c) {
-    int p = c;
-    double best = fabs(a[6 * c + c]);
-#pragma unroll
-    for (int r = c + 1; r < 6; ++r)
-      if (fabs(a[6 * r + c]) > best) { best = fabs(a[6 * r + c]); p = r; }
-    if (best == 0.0) return 0.0;
-#pragma unroll
-    for (int r = c + 1; r < 6; ++r) {
-      const bool sw = p == r;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        const double t = a[6 * c + k];
-        a[6 * c + k] = sw ? a[6 * r + k] : t;
-        a[6 * r + k] = sw ? t : a[6 * r + k];
-      }
-      if (INV) {
-        const int tp = perm[c];
-        perm[c] = sw ? perm[r] : tp;
-        perm[r] = sw ? tp : perm[r];
-      }
-    }
-    if (p != c) det = -det;
-    const double piv = a[6 * c + c];
-    det *= piv;
-#pragma unroll
-    for (int r = c + 1; r < 6; ++r) {
-      const double f = a[6 * r + c] / piv;
-#pragma unroll
-      for (int k = c + 1; k < 6; ++k) a[6 * r + k] -= f * a[6 * c + k];
-      if (INV) a[6 * r + c] = f;
-    }
-  }
-  if (INV) {
-    double rd[6];  // one division per pivot, then multiplies in the 6 back substitutions
-#pragma unroll
-    for (int i = 0; i < 6; ++i) rd[i] = 1.0 / a[6 * i + i];
-#pragma unroll
-    for (int j = 0; j < 6; ++j) {  // column j of A^-1: solve L U x = P e_j
-      double x[6];
-#pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        double y = perm[i] == j ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = 0; k < i; ++k) y -= a[6 * i + k] * x[k];
-        x[i] = y;
-      }
-#pragma unroll
-      for (int i = 5; i >= 0; --i) {
-        double y = x[i];
-#pragma unroll
-        for (int k = i + 1; k < 6; ++k) y -= a[6 * i + k] * x[k];
-        x[i] = y * rd[i];
-      }
-#pragma unroll
-      for (int i = 0; i < 6; ++i) inv[6 * i + j] = x[i];
-    }
-  }
-  ok = true;
-  return det;
-}
-
-// cyclic Jacobi; VEC: accumulate the rotations and return the unit eigenvector of the
-// smallest eigenvalue in vec
-template <bool VEC>
-__device__ __forceinline__ double lmin6_core(double (&a)[36], double (&vec)[6]) {
-  double V[VEC ? 36 : 1];
-  if (VEC) {
-#pragma unroll
-    for (int i = 0; i < (VEC ? 36 : 1); ++i) V[i] = (i % 7 == 0) ? 1.0 : 0.0;
-  }
-  for (int sweep = 0; sweep < 64; ++sweep) {
-    double off = 0.0, tot = 0.0;
-#pragma unroll
-    for (int r = 0; r < 6; ++r)
-#pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        const double v = a[6 * r + c] * a[6 * r + c];
-        tot += v;
-        if (r != c) off += v;
-      }
-    if (off <= 1e-30 * tot || off == 0.0) break;
-#pragma unroll
-    for (int p = 0; p < 5; ++p)
-#pragma unroll
-      for (int q = p + 1; q < 6; ++q) {
-        const double apq = a[6 * p + q];
-        if (apq != 0.0) {
-          const double theta = (a[6 * q + q] - a[6 * p + p]) / (2.0 * apq);
-          const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          const double cs = rsqrt(fma(t, t, 1.0)), sn = t * cs;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) {
-            const double akp = a[6 * k + p], akq = a[6 * k + q];
-            a[6 * k + p] = cs * akp - sn * akq;
-            a[6 * k + q] = sn * akp + cs * akq;
-            if (VEC) {
-              const double vkp = V[6 * k + p], vkq = V[6 * k + q];
-              V[6 * k + p] = cs * vkp - sn * vkq;
-              V[6 * k + q] = sn * vkp + cs * vkq;
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 6; ++k) {
-            const double apk = a[6 * p + k], aqk = a[6 * q + k];
-            a[6 * p + k] = cs * apk - sn * aqk;
-            a[6 * q + k] = sn * apk + cs * aqk;
-          }
-        }
-      }
-  }
-  double m = a[0];
-#pragma unroll
-  for (int k = 1; k < 6; ++k) m = fmin(m, a[7 * k]);
-  if (VEC) {
-    double best = a[0];
-    int im = 0;
-#pragma unroll
-    for (int k = 1; k < 6; ++k)
-      if (a[7 * k] < best) { best = a[7 * k]; im = k; }
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      double v = V[6 * i];
-#pragma unroll
-      for (int k = 1; k < 6; ++k) v = im == k ? V[6 * i + k] : v;
-      vec[i] = v;
-    }
-  }
-  return m;
-}
-
-// unpack a corner's 21 packed entries into a symmetric 6x6 (registers)
-__device__ __forceinline__ void unpack21(const double* cf, double (&a)[36]) {
-#pragma unroll
-  for (int x = 0; x < 21; ++x) {
-    const double v = cf[x];
-    a[pack_r(x) * 6 + pack_c(x)] = v;
-    a[pack_c(x) * 6 + pack_r(x)] = v;
-  }
 }
 
 __constant__ int kPackR[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
@@ -1123,7 +966,7 @@ static void launch_small(const fif_model& m, const QueryGeom& gm, const int32_t*
                       sizeof(double) * (((nv + 1) & ~1) + QS_WARPS * qs_np<NC, GRAD, METRIC, MGRAD>() * 32 +
                                         8 * qw_cf<METRIC, MGRAD>() + (size_t)nv * nv);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t cap = (int64_t)kSMs * 4;
+  const int64_t cap = (int64_t)num_sms() * 4;
   kern<<<(unsigned)(q < cap ? q : cap), QS_WARPS * 32, smem, st>>>(m, gm, slots, pos, axes, q, trilinear, field, out);
 }
 
@@ -1203,7 +1046,7 @@ __global__ void __launch_bounds__(QC_WARPS * 32) k_query_trace(int nv, const T* 
 
 static unsigned query_blocks(int64_t q) {
   int64_t need = (q + QC_WARPS - 1) / QC_WARPS;
-  int64_t cap = (int64_t)kSMs * 32;
+  int64_t cap = (int64_t)num_sms() * 32;
   return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
 
@@ -1246,7 +1089,7 @@ static void launch_info(int nv, const T* f, const double* axes, int64_t q, const
   constexpr int WPB = qw_wpb(STAGES);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem);
   const int64_t need = (q + WPB - 1) / WPB;
-  const int64_t cap = (int64_t)kSMs * (per_sm > 0 ? per_sm : 1);
+  const int64_t cap = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
   kern<<<(unsigned)(need < cap ? need : cap), WPB * 32, smem, st>>>(nv, f, axes, q, status, rows, cw, wt, out, perm);
 }
 
@@ -1257,7 +1100,7 @@ static void launch_info_nc(bool grad, bool metric, bool mgrad, int nv, const T* 
   // value/gradient streaming: 2 stages, 3 CTAs/SM; metric variants (det/lmin, LU and
   // Jacobi per corner, more registers): 3 stages, 2 CTAs/SM
   static const int stages_env = getenv("FIF_QW_STAGES") ? atoi(getenv("FIF_QW_STAGES")) : 2;
-  if (q <= (int64_t)kSMs * 3) {  // small batch: one query per CTA, all k-chunks in flight
+  if (q <= (int64_t)num_sms() * 3) {  // small batch: one query per CTA, all k-chunks in flight
     constexpr int S = QW_SMALL_STAGES;
     if (mgrad) launch_info<T, NC, S, true, true, true>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
     else if (metric && grad) launch_info<T, NC, S, true, true, false>(nv, f, axes, q, status, rows, cw, wt, out, perm, st);
@@ -1313,6 +1156,50 @@ extern "C" int fif_query(int factor_kind, const fif_model* model, const fif_grid
   return fif_query_ex(factor_kind, model, grid, d_field, d_slots, d_positions, d_axes, q, mode, flags, &o, stream);
 }
 
+// Corner table of a batch of positions (debug / parity ABI fif_locate): exactly the
+// locate() the query kernels run, with rows reported as the reference's x-major linear
+// voxel index (field.py:81-83) so they compare with kernels._nb_locate_nearest /
+// the trilinear corner block (kernels.py:628-635, 678-702) bit for bit.
+__global__ void k_locate(QueryGeom gm, const double* __restrict__ pos, int64_t q, int trilinear,
+                         int64_t* __restrict__ index, double* __restrict__ weight, uint8_t* __restrict__ status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  int nc = 0;
+  int64_t rows[8];
+  double w[8], dw[8][3];
+  const int s = locate(gm, nullptr, pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], trilinear != 0, nc, rows, w, dw);
+  status[i] = (uint8_t)s;
+  for (int k = 0; k < 8; ++k) {
+    int64_t lin = -1;
+    double wk = 0.0;
+    if (s == FIF_STATUS_OK && k < nc) {
+      const int64_t j = rows[k];  // internal z-major row of the dense grid
+      const int64_t ix = j % gm.nx, r = j / gm.nx, iy = r % gm.ny, iz = r / gm.ny;
+      lin = (ix * gm.ny + iy) * gm.nz + iz;
+      wk = w[k];
+    }
+    if (index) index[8 * i + k] = lin;
+    if (weight) weight[8 * i + k] = wk;
+  }
+}
+
+extern "C" int fif_locate(const fif_grid* grid, const double* d_positions, int64_t q, int mode, int64_t* d_index,
+                          double* d_weight, uint8_t* d_status, void* stream) {
+  FIF_CHECK_ARG(grid && d_status && (q == 0 || d_positions), "fif_locate: NULL argument");
+  FIF_CHECK_ARG(q >= 0, "fif_locate: negative query count");
+  FIF_CHECK_ARG(mode == FIF_MODE_NEAREST || mode == FIF_MODE_TRILINEAR, "fif_locate: unknown mode %d", mode);
+  FIF_CHECK_ARG(grid->voxel_size > 0 && grid->dims[0] > 0 && grid->dims[1] > 0 && grid->dims[2] > 0,
+                "fif_locate: empty grid");
+  if (q == 0) return FIF_OK;
+  QueryGeom gm{grid->origin[0], grid->origin[1], grid->origin[2], grid->voxel_size,
+               grid->dims[0],   grid->dims[1],   grid->dims[2]};
+  k_locate<<<(unsigned)((q + 255) / 256), 256, 0, (cudaStream_t)stream>>>(gm, d_positions, q,
+                                                                         mode == FIF_MODE_TRILINEAR, d_index,
+                                                                         d_weight, d_status);
+  FIF_CHECK_LAUNCH("k_locate");
+  return FIF_OK;
+}
+
 extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_grid* grid, const void* d_field,
                             const int32_t* d_slots, const double* d_positions, const double* d_axes, int64_t q,
                             int mode, uint32_t flags, const fif_query_out* o, void* stream) {
@@ -1334,7 +1221,9 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
   FIF_CHECK_ARG(nv >= 1 && nv <= 1024, "fif_query: n_v out of range");
   // bound the per-call scratch (32 nv bytes of rotation weights per query): very large
   // batches run as consecutive slices of kQueryChunk queries on the same stream
-  constexpr int64_t kQueryChunk = 1 << 21;
+  // (capped so the scratch of one slice stays near 1 GiB: 2^18..2^21 queries)
+  int64_t kQueryChunk = ((int64_t)1 << 30) / ((int64_t)nv * 32 + 320);
+  kQueryChunk = kQueryChunk < ((int64_t)1 << 18) ? ((int64_t)1 << 18) : (kQueryChunk > ((int64_t)1 << 21) ? ((int64_t)1 << 21) : kQueryChunk);
   if (q > kQueryChunk) {
     for (int64_t q0 = 0; q0 < q; q0 += kQueryChunk) {
       const int64_t n = q - q0 < kQueryChunk ? q - q0 : kQueryChunk;
@@ -1366,7 +1255,7 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
   cudaStream_t st = (cudaStream_t)stream;
   // small GP info batches (latency-bound): one fused kernel, one CTA per query
   static const bool no_small = getenv("FIF_QUERY_NO_FUSED_SMALL") != nullptr;
-  if (info && model->kind == FIF_MODEL_GP && !(flags & FIF_Q_FIELD_F64) && q <= (int64_t)kSMs * 3 && !no_small &&
+  if (info && model->kind == FIF_MODEL_GP && !(flags & FIF_Q_FIELD_F64) && q <= (int64_t)num_sms() * 3 && !no_small &&
       (size_t)nv * 21 * 4 * (trilinear ? 8 : 1) + (size_t)nv * nv * 8 <= 150 * 1024) {
     const float* ff = reinterpret_cast<const float*>(d_field);
     const int tri = trilinear ? 1 : 0;
@@ -1389,16 +1278,19 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
   const size_t b_rows = (size_t)q * 8 * sizeof(int32_t);
   const size_t b_cw = (size_t)q * 8 * sizeof(double4);
   const size_t b_wt = (size_t)q * nv * sizeof(double4);
-  static bool pool_set = false;
-  if (!pool_set) {
+  static std::atomic<uint64_t> pool_set{0};
+  if (needs_setup(pool_set)) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
+      // keep up to 1 GiB of freed scratch reserved between calls (no re-allocation for
+      // planner-sized batches); anything above is returned to the device at the next
+      // synchronisation, so one huge batch does not pin memory torch may need later
+      uint64_t thr = 1ull << 30;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    pool_set = true;
+    mark_setup(pool_set);
   }
   unsigned char* scratch = nullptr;
   if (cudaMallocAsync(&scratch, b_status + b_rows + b_cw + b_wt + 256, st) != cudaSuccess) {

@@ -117,11 +117,60 @@ def _grid_of(cfg) -> GridConfig:
     return GridConfig(np.asarray(cfg.origin), float(cfg.voxel_size), np.asarray(cfg.dims))
 
 
+def _world_arrays(occ):
+    """(spheres (S,4), boxes (B,6)) float64 of an ObstacleWorld (world.py:44-56), duck-typed
+    through its `spheres` (centre, radius) and `boxes` (lo, hi) lists; None if `occ` is not one."""
+    spheres, boxes = getattr(occ, "spheres", None), getattr(occ, "boxes", None)
+    if spheres is None and boxes is None:
+        return None
+    sph = np.array([[*np.asarray(s.center, dtype=np.float64).reshape(3), float(s.radius)] for s in (spheres or [])],
+                   dtype=np.float64).reshape(-1, 4)
+    box = np.array([[*np.asarray(b.lo, dtype=np.float64).reshape(3), *np.asarray(b.hi, dtype=np.float64).reshape(3)]
+                    for b in (boxes or [])], dtype=np.float64).reshape(-1, 6)
+    return sph, box
+
+
+def _segment_blocked(occ, start, ends) -> np.ndarray:
+    """world.segment_blocked (world.py:96-140) restated in numpy with the reference's
+    expressions (host parity reference for the device gate)."""
+    start = np.asarray(start, dtype=np.float64).reshape(3)
+    ends = np.asarray(ends, dtype=np.float64).reshape(-1, 3)
+    blocked = np.zeros(ends.shape[0], dtype=bool)
+    sph, box = _world_arrays(occ)
+    if sph.shape[0] == 0 and box.shape[0] == 0:
+        return blocked
+    seg = ends - start
+    t_hi = 1.0 - 1e-6
+    for cx, cy, cz, r in sph:
+        c = np.array([cx, cy, cz])
+        rel = start - c
+        a = np.einsum("ij,ij->i", seg, seg)
+        b = 2.0 * seg @ rel
+        t = np.where(a > 0, np.clip(-b / (2 * np.maximum(a, 1e-300)), 0.0, t_hi), 0.0)
+        dist = np.linalg.norm(start + t[:, None] * seg - c, axis=1)
+        blocked |= dist < r - 1e-9
+    for row in box:
+        lo, hi = row[:3] + 1e-9, row[3:] - 1e-9
+        with np.errstate(divide="ignore", invalid="ignore"):
+            inv = np.where(seg != 0.0, 1.0 / seg, np.inf)
+            t0, t1 = (lo - start) * inv, (hi - start) * inv
+        tmin, tmax = np.minimum(t0, t1), np.maximum(t0, t1)
+        flat = seg == 0.0
+        inside = (start >= lo) & (start <= hi)
+        tmin = np.where(flat, np.where(inside, -np.inf, np.inf), tmin)
+        tmax = np.where(flat, np.where(inside, np.inf, -np.inf), tmax)
+        enter, leave = tmin.max(axis=1), tmax.min(axis=1)
+        blocked |= (enter < leave) & (leave > 0.0) & (enter < t_hi)
+    return blocked
+
+
 @dataclass(frozen=True)
 class Matchability:
-    """Which landmarks contribute to a voxel (field.py:101-180).  The default
-    accepts every pair; the gates are evaluated on the host in FP64 with the
-    reference's arithmetic, the resulting mask is applied inside the kernels."""
+    """Which landmarks contribute to a voxel (field.py:101-180).  The default accepts every
+    pair.  Range, view cone and ObstacleWorld occlusion are device predicates (fif_gate.cuh,
+    the reference's FP64 arithmetic, bit-identical masks) that the build kernels evaluate
+    inside their pair loops; a Python `predicate` is evaluated pairwise on the host, as in
+    the reference, and applied as an explicit mask."""
 
     d_near: float | None = None
     d_far: float | None = None
@@ -149,46 +198,76 @@ class Matchability:
 
     @property
     def gpu_gates(self) -> bool:
-        """Range / view-cone gates present (evaluated on the GPU by fif_match_mask)."""
-        return self.d_near is not None or self.d_far is not None or self.view_cone_beta is not None
+        """Gates evaluated on the GPU: range, view cone, ObstacleWorld occlusion."""
+        return (self.d_near is not None or self.d_far is not None or self.view_cone_beta is not None
+                or (self.occluders is not None and _world_arrays(self.occluders) is not None))
 
     @property
     def host_gates(self) -> bool:
-        """Occlusion / Python predicate present (host only, as in the reference)."""
-        return self.occluders is not None or self.predicate is not None
+        """Gates only the host can evaluate: a Python predicate, or an occluder object that is
+        not an ObstacleWorld but provides segment_blocked(center, points)."""
+        return self.predicate is not None or (self.occluders is not None and _world_arrays(self.occluders) is None)
+
+    def device_match(self, device: torch.device, view_dirs=None):
+        """(fif_match struct, device tensors it points to) for the GPU gates."""
+        m = _lib.Match()
+        m.flags = 0
+        keep = []
+        if self.d_near is not None:
+            m.d_near, m.flags = float(self.d_near), m.flags | _lib.MATCH_NEAR
+        if self.d_far is not None:
+            m.d_far, m.flags = float(self.d_far), m.flags | _lib.MATCH_FAR
+        vd = None
+        if self.view_cone_beta is not None:
+            if view_dirs is None:
+                raise ValueError("view_cone_beta requires landmark view directions")
+            m.cos_beta, m.flags = float(np.cos(self.view_cone_beta)), m.flags | _lib.MATCH_CONE
+            vd = _device.to_device_f64(view_dirs, device, (3,))
+            keep.append(vd)
+        arrays = _world_arrays(self.occluders) if self.occluders is not None else None
+        if arrays is not None:
+            sph = torch.from_numpy(np.ascontiguousarray(arrays[0])).to(device)
+            box = torch.from_numpy(np.ascontiguousarray(arrays[1])).to(device)
+            keep += [sph, box]
+            m.spheres, m.n_spheres = (sph.data_ptr() if sph.shape[0] else None), sph.shape[0]
+            m.boxes, m.n_boxes = (box.data_ptr() if box.shape[0] else None), box.shape[0]
+            m.flags |= _lib.MATCH_OCCLUDE
+        return m, vd, keep
+
+    def device_any(self, centers: torch.Tensor, points: torch.Tensor, view_dirs=None) -> torch.Tensor:
+        """(V,) bool on the device: some landmark passes the GPU gates (fif_match_any)."""
+        dev = points.device
+        m, vd, _keep = self.device_match(dev, view_dirs)
+        out = torch.empty(centers.shape[0], dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.load().fif_match_any(m, _lib.ptr(centers), centers.shape[0], _lib.ptr(points),
+                                                 _lib.ptr(vd), points.shape[0], _lib.ptr(out),
+                                                 _device.stream_handle(dev)), "fif_match_any")
+        return out.bool()
 
     def device_mask(self, centers: torch.Tensor, points: torch.Tensor, view_dirs=None) -> torch.Tensor:
-        """(V, N) uint8 mask on the device: the range / view-cone gates on the GPU
-        (fif_match_mask, bit-identical with `mask`), AND the host-only gates."""
+        """(V, N) uint8 mask on the device: the GPU gates (fif_match_mask, bit-identical with
+        `mask`), AND the host-only gates."""
         dev = points.device
         V, N = centers.shape[0], points.shape[0]
         if self.gpu_gates:
-            m = _lib.Match()
-            m.flags = 0
-            if self.d_near is not None:
-                m.d_near, m.flags = float(self.d_near), m.flags | _lib.MATCH_NEAR
-            if self.d_far is not None:
-                m.d_far, m.flags = float(self.d_far), m.flags | _lib.MATCH_FAR
-            vd = None
-            if self.view_cone_beta is not None:
-                if view_dirs is None:
-                    raise ValueError("view_cone_beta requires landmark view directions")
-                m.cos_beta, m.flags = float(np.cos(self.view_cone_beta)), m.flags | _lib.MATCH_CONE
-                vd = _device.to_device_f64(view_dirs, dev, (3,))
+            m, vd, _keep = self.device_match(dev, view_dirs)
             out = torch.empty((V, N), dtype=torch.uint8, device=dev)
-            _lib.check(_lib.load().fif_match_mask(m, _lib.ptr(centers), V, _lib.ptr(points), _lib.ptr(vd), N,
-                                                  _lib.ptr(out), _device.stream_handle(dev)), "fif_match_mask")
+            with torch.cuda.device(dev):
+                _lib.check(_lib.load().fif_match_mask(m, _lib.ptr(centers), V, _lib.ptr(points), _lib.ptr(vd), N,
+                                                      _lib.ptr(out), _device.stream_handle(dev)), "fif_match_mask")
         else:
             out = torch.ones((V, N), dtype=torch.uint8, device=dev)
         if self.host_gates:
-            host = Matchability(occluders=self.occluders, predicate=self.predicate)
+            occ = None if (self.occluders is None or _world_arrays(self.occluders) is not None) else self.occluders
+            host = Matchability(occluders=occ, predicate=self.predicate)
             hm = host.mask(_device.to_numpy(centers), _device.to_numpy(points), view_dirs)
             out &= torch.from_numpy(hm).to(dev)
         return out
 
     def mask(self, centers, points, view_dirs=None):
-        """Host restatement of the reference's mask (field.py:143-177); the build uses
-        `device_mask`, this is the parity reference for it."""
+        """Host restatement of the reference's mask (field.py:143-177); the build evaluates the
+        same gates on the device, this is the parity reference for them."""
         if self.is_trivial:
             return None
         d = points[None, :, :] - centers[:, None, :]
@@ -204,9 +283,13 @@ class Matchability:
             cosang = np.einsum("vnk,nk->vn", d / np.maximum(dist, 1e-12)[..., None], view_dirs)
             ok &= cosang >= np.cos(self.view_cone_beta)
         if self.occluders is not None:
-            blocked_fn = getattr(self.occluders, "segment_blocked", None)
-            if blocked_fn is None:
-                raise TypeError("occluders must provide segment_blocked(center, points) -> bool array")
+            if _world_arrays(self.occluders) is not None:
+                blocked_fn = lambda c, p: _segment_blocked(self.occluders, c, p)  # noqa: E731
+            else:
+                blocked_fn = getattr(self.occluders, "segment_blocked", None)
+                if blocked_fn is None:
+                    raise TypeError("occluders must be an ObstacleWorld (spheres / boxes) or provide "
+                                    "segment_blocked(center, points)")
             for v in range(centers.shape[0]):
                 ok[v] &= ~np.asarray(blocked_fn(centers[v], points), dtype=bool)
         if self.predicate is not None:
@@ -283,12 +366,49 @@ def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, devi
     scratch = torch.empty(int(_lib.load().fif_build_scratch_bytes(n)), dtype=torch.uint8, device=device)
     g = _lib.make_grid(grid.origin, grid.voxel_size, grid.dims) if grid is not None else None
     kind = _lib.KIND_TRACE if want_trace else _lib.KIND_INFO
-    st = _lib.load().fif_build(kind, dm.c, _lib.ptr(points), n, g, _lib.ptr(centers), v_begin, v_end, _lib.ptr(mask),
-                               float(sigma), (_lib.BUILD_EXACT if exact else 0) | _GP_INFO_FLAGS[GP_INFO_KERNEL],
-                               _lib.ptr(scratch), _lib.ptr(out64),
-                               _lib.ptr(out32), _device.stream_handle(device))
+    with torch.cuda.device(device):  # the library launches on the current device
+        st = _lib.load().fif_build(kind, dm.c, _lib.ptr(points), n, g, _lib.ptr(centers), v_begin, v_end,
+                                   _lib.ptr(mask), float(sigma),
+                                   (_lib.BUILD_EXACT if exact else 0) | _GP_INFO_FLAGS[GP_INFO_KERNEL],
+                                   _lib.ptr(scratch), _lib.ptr(out64), _lib.ptr(out32), _device.stream_handle(device))
     _lib.check(st, "fif_build")
     return out64, out32
+
+
+def build_matched_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, device: torch.device,
+                       centers: torch.Tensor, matchability: "Matchability", view_dirs=None,
+                       dmodel: _DeviceModel | None = None, f32_copy: bool = True, exact: bool = False):
+    """One fif_build_matched launch: rows for the given centres with the GPU gates of
+    `matchability` evaluated inside the build kernels (no (V, N) mask)."""
+    dm = dmodel or _DeviceModel(model, device)
+    n_v = model.n_v
+    width = n_v if want_trace else n_v * 21
+    rows = centers.shape[0]
+    out64 = torch.empty((rows, width), dtype=torch.float64, device=device)
+    gp = isinstance(model, GpVisibility)
+    out32 = torch.empty((rows, width), dtype=torch.float32, device=device) if (gp and f32_copy) else None
+    scratch = torch.empty(int(_lib.load().fif_build_scratch_bytes(points.shape[0])), dtype=torch.uint8, device=device)
+    m, vd, _keep = matchability.device_match(device, view_dirs)
+    kind = _lib.KIND_TRACE if want_trace else _lib.KIND_INFO
+    with torch.cuda.device(device):
+        _lib.check(_lib.load().fif_build_matched(kind, dm.c, _lib.ptr(points), points.shape[0], _lib.ptr(centers), rows,
+                                                 m, _lib.ptr(vd), float(sigma),
+                                                 (_lib.BUILD_EXACT if exact else 0) | _GP_INFO_FLAGS[GP_INFO_KERNEL],
+                                                 _lib.ptr(scratch), _lib.ptr(out64), _lib.ptr(out32),
+                                                 _device.stream_handle(device)), "fif_build_matched")
+    return out64, out32
+
+
+def device_centers(config: GridConfig, device: torch.device, order: int = 0) -> torch.Tensor:
+    """(V,3) voxel centres on the device (fif_grid_centers; order 0 = the reference's x-major
+    linear order, 1 = internal z-major), bit-identical to GridConfig.centers."""
+    V = config.voxel_count
+    out = torch.empty((V, 3), dtype=torch.float64, device=device)
+    g = _lib.make_grid(config.origin, config.voxel_size, config.dims)
+    with torch.cuda.device(device):
+        _lib.check(_lib.load().fif_grid_centers(g, order, 0, V, _lib.ptr(out), _device.stream_handle(device)),
+                   "fif_grid_centers")
+    return out
 
 
 class Field:
@@ -360,8 +480,9 @@ class Field:
         src = src.contiguous()
         out = torch.empty((src.shape[0], self.row_width), dtype=torch.float64, device=self.device)
         kind = _lib.KIND_INFO if self._is_info else _lib.KIND_TRACE
-        _lib.check(_lib.load().fif_export_reference(kind, self._dm.c, _lib.ptr(src), src.shape[0], _lib.ptr(out),
-                                                    _device.stream_handle(self.device)), "fif_export_reference")
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().fif_export_reference(kind, self._dm.c, _lib.ptr(src), src.shape[0], _lib.ptr(out),
+                                                        _device.stream_handle(self.device)), "fif_export_reference")
         return out
 
     @property
@@ -395,8 +516,22 @@ class Field:
         if matchability.is_trivial:
             s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, grid=config, exact=exact)
             return Field(config, model, factor_kind, sigma, s64, s32, None, matchability, dense=True)
-        # matchability-masked build: gates on the GPU, voxel chunks bounded to
-        # _MASK_CHUNK_BYTES of mask, occupied rows kept in the reference's linear order
+        if not matchability.host_gates:
+            # gates fused into the build kernels: occupancy pass (fif_match_any), then the
+            # occupied voxels' rows in the reference's linear order (field.py:253-265)
+            cen = device_centers(config, dev)
+            occ = torch.nonzero(matchability.device_any(cen, pts_dev, view_dirs)).flatten()
+            if occ.numel() == 0:
+                s64 = torch.zeros((0, width), dtype=torch.float64, device=dev)
+                return Field(config, model, factor_kind, sigma, s64, s64.float() if gp else None,
+                             np.zeros((0, 3), np.int32), matchability, dense=False)
+            s64, s32 = build_matched_rows(pts_dev, model, want_trace, sigma, dev, cen[occ].contiguous(), matchability,
+                                          view_dirs, exact=exact)
+            lin = occ.cpu().numpy()
+            return Field(config, model, factor_kind, sigma, s64, s32, config.index3_of(lin).astype(np.int32),
+                         matchability, dense=False)
+        # a Python predicate (host, as in the reference): explicit masks in voxel chunks bounded
+        # to _MASK_CHUNK_BYTES, occupied rows kept in the reference's linear order
         centers = config.centers()
         n = points.shape[0]
         chunk = max(1, min(config.voxel_count, _MASK_CHUNK_BYTES // max(1, n)))
@@ -499,10 +634,11 @@ class Field:
         if self.rows == 0:
             slots = torch.full((self.config.voxel_count,), -1, dtype=torch.int32, device=dev)
         o = _lib.QueryOut(*(_lib.ptr(t) for t in (tr_t, trg_t, fim_t, fimg_t, det_t, detg_t, lmin_t, lming_t, st_t)))
-        _lib.check(_lib.load().fif_query_ex(kind, self._dm.c, self._grid_c, _lib.ptr(field_t), _lib.ptr(slots),
-                                            _lib.ptr(positions), _lib.ptr(axes), q,
-                                            _lib.MODE_TRILINEAR if trilinear else _lib.MODE_NEAREST, flags, o,
-                                            _device.stream_handle(dev)), "fif_query")
+        with torch.cuda.device(dev):
+            _lib.check(_lib.load().fif_query_ex(kind, self._dm.c, self._grid_c, _lib.ptr(field_t), _lib.ptr(slots),
+                                                _lib.ptr(positions), _lib.ptr(axes), q,
+                                                _lib.MODE_TRILINEAR if trilinear else _lib.MODE_NEAREST, flags, o,
+                                                _device.stream_handle(dev)), "fif_query")
         return out
 
     def query_graph(self, batch: int, mode: str = "trilinear", outputs=("trace", "full"), grad: bool = False,
@@ -583,40 +719,48 @@ class Field:
             raise OutOfField(f"position {pose.translation.tolist()} outside field coverage")
         return float(vals[0])
 
-    def query_factor(self, position, mode: str = "nearest") -> np.ndarray:
-        """Raw (blended) reference-layout factor at a position (field.py:277-303)."""
+    def locate(self, positions, mode: str = "trilinear") -> dict:
+        """Corner table of each position on the device (fif_locate): the bit-exact indexing
+        rule the queries use (kernels.py:628-635 nearest, 678-702 trilinear).  Returns numpy
+        arrays index (Q,8) int64 reference linear voxel indices (-1 = unused corner),
+        weight (Q,8) and status (Q,) uint8 (0 ok, 1 out of field)."""
         trilinear = self._check_mode(mode)
-        cfg = self.config
-        pos = np.asarray(position, dtype=np.float64)
-        if trilinear:
-            g = (pos - cfg.origin) / cfg.voxel_size - 0.5
-            base = np.floor(g).astype(np.int64)
-            f = g - base
-            for a in range(3):
-                if base[a] + 1 == cfg.dims[a] and f[a] == 0.0:
-                    base[a] -= 1
-                    f[a] = 1.0
-            if (base < 0).any() or (base + 1 > cfg.dims - 1).any():
+        dev = self.device
+        pos = _device.to_device_f64(positions, dev, (3,))
+        q = pos.shape[0]
+        idx = torch.empty((q, 8), dtype=torch.int64, device=dev)
+        w = torch.empty((q, 8), dtype=torch.float64, device=dev)
+        st = torch.empty(q, dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.load().fif_locate(self._grid_c, _lib.ptr(pos), q,
+                                              _lib.MODE_TRILINEAR if trilinear else _lib.MODE_NEAREST, _lib.ptr(idx),
+                                              _lib.ptr(w), _lib.ptr(st), _device.stream_handle(dev)), "fif_locate")
+        return {"index": _device.to_numpy(idx), "weight": _device.to_numpy(w), "status": _device.to_numpy(st)}
+
+    def query_factor(self, position, mode: str = "nearest") -> np.ndarray:
+        """Raw (blended) reference-layout factor at a position (field.py:277-303): the
+        corners come from the device locate (the queries' bit-exact rule), the rows from
+        the reference-layout export, blended in FP64 in corner order like the reference."""
+        trilinear = self._check_mode(mode)
+        pos = np.asarray(position, dtype=np.float64).reshape(3)
+        loc = self.locate(pos[None], mode)
+        if loc["status"][0] != 0:
+            if trilinear:
                 raise OutOfField(f"position {pos.tolist()} lacks 8 interpolation neighbors")
-            corners, wts = [], []
-            for dx in (0, 1):
-                for dy in (0, 1):
-                    for dz in (0, 1):
-                        corners.append(cfg.linear_index(base + np.array([dx, dy, dz])))
-                        wts.append((f[0] if dx else 1 - f[0]) * (f[1] if dy else 1 - f[1]) * (f[2] if dz else 1 - f[2]))
-        else:
-            i3 = np.floor((pos - cfg.origin) / cfg.voxel_size).astype(np.int64)
-            if (i3 < 0).any() or (i3 >= cfg.dims).any():
-                raise OutOfField(f"position {pos.tolist()} outside grid")
-            corners, wts = [cfg.linear_index(i3)], [1.0]
-        rows = self.slots[np.array(corners)]
+            raise OutOfField(f"position {pos.tolist()} outside grid")
+        ncorner = 8 if trilinear else 1
+        idx, wts = loc["index"][0, :ncorner], loc["weight"][0, :ncorner]
+        rows = self.slots[idx]
         out = np.zeros(self.row_width)
         valid = rows >= 0
         if valid.any():
             ref = _device.to_numpy(self.export_reference(rows[valid]))
-            for w, row in zip(np.array(wts)[valid], ref):
-                if w != 0.0:
-                    out += w * row
+            if not trilinear:
+                out = ref[0].copy()
+            else:
+                for w, row in zip(wts[valid], ref):
+                    if w != 0.0:
+                        out += w * row
         return out.reshape(self.model.n_v, 6, 6) if self._is_info else out
 
     # ── incremental updates (field.py:461-505) ──────────────────────
@@ -632,22 +776,30 @@ class Field:
                                 dmodel=self._dm, f32_copy=False)
             self._s64.add_(inc, alpha=sign)
         else:
-            centers = self.config.centers()
-            cen = torch.from_numpy(np.ascontiguousarray(centers)).to(dev)
-            if self.matchability.is_trivial:
+            cen = device_centers(self.config, dev)
+            vdirs = vd if vd is not None else view_dirs
+            mt = self.matchability
+            if mt.is_trivial:
                 mask = None
                 touched = np.ones(self.config.voxel_count, bool)
+            elif not mt.host_gates:  # fused gates: occupancy only
+                mask = None
+                touched = _device.to_numpy(mt.device_any(cen, pts_dev, vdirs))
             else:
-                mask = self.matchability.device_mask(cen, pts_dev, vd if vd is not None else view_dirs)
+                mask = mt.device_mask(cen, pts_dev, vdirs)
                 touched = _device.to_numpy(mask.any(dim=1))
             if not touched.any():
                 return
             lin = np.nonzero(touched)[0]
             sel = torch.from_numpy(lin).to(dev)
             sub_c = cen[sel].contiguous()
-            sub_m = None if mask is None else mask[sel].contiguous()
-            inc, _ = build_rows(pts_dev, self.model, want_trace, self.sigma, dev, centers=sub_c, mask=sub_m,
-                                dmodel=self._dm, f32_copy=False)
+            if not mt.is_trivial and not mt.host_gates:
+                inc, _ = build_matched_rows(pts_dev, self.model, want_trace, self.sigma, dev, sub_c, mt, vdirs,
+                                            dmodel=self._dm, f32_copy=False)
+            else:
+                sub_m = None if mask is None else mask[sel].contiguous()
+                inc, _ = build_rows(pts_dev, self.model, want_trace, self.sigma, dev, centers=sub_c, mask=sub_m,
+                                    dmodel=self._dm, f32_copy=False)
             if self._dense:
                 rows = self.slots[lin]
             else:
@@ -773,7 +925,7 @@ class Field:
             raise TruncatedFile("voxel index outside grid")
         dev = _device.require_cuda(device)
         s64 = _device.to_device_f64(_from_reference_rows(factors, model, factor_kind), dev)
-        s64 = s64.reshape(rows, -1)
+        s64 = s64.reshape(rows, model.n_v * (21 if factor_kind == "info" else 1))  # explicit width: rows may be 0
         s32 = s64.float() if isinstance(model, GpVisibility) else None
         fld = Field(config, model, factor_kind, sigma, s64, s32, occ3, ALWAYS_MATCH, dense=False)
         fld._ref_cache = factors  # bitwise round trip of the stored reference rows
@@ -783,6 +935,7 @@ class Field:
 def _from_reference_rows(factors: np.ndarray, model, factor_kind: str) -> np.ndarray:
     """Reference-layout rows -> device storage layout (packed; GP: S = K F)."""
     n_v = model.n_v
+    factors = np.asarray(factors, dtype=np.float64).reshape(-1, n_v * (36 if factor_kind == "info" else 1))
     rows = factors.shape[0]
     if factor_kind == "info":
         packed = factors.reshape(rows, n_v, 36)[:, :, _PACK36]
@@ -792,7 +945,7 @@ def _from_reference_rows(factors: np.ndarray, model, factor_kind: str) -> np.nda
         from .visibility import _gram
 
         packed = np.einsum("gk,rkw->rgw", _gram(model.samples, model.params), packed)
-    return np.ascontiguousarray(packed.reshape(rows, -1))
+    return np.ascontiguousarray(packed.reshape(rows, n_v * (21 if factor_kind == "info" else 1)))
 
 
 def build(landmarks, config, model, factor_kind="info", matchability=ALWAYS_MATCH, sigma=DEFAULT_SIGMA,

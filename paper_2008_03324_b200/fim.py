@@ -7,6 +7,7 @@ I_i = (1/sigma^2) [-I3, skew(p)]^T (I3 - u u^T)/n^2 [-I3, skew(p)]  (fim.py:1-11
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -103,9 +104,10 @@ def exact_pose_fim_batch_device(rotations: torch.Tensor, translations: torch.Ten
     if out is None:
         out = torch.empty((q, 36), dtype=torch.float64, device=dev)
     cam = _lib.make_camera(camera.as_tuple())
-    _lib.check(_lib.load().fif_pc_fim(_lib.ptr(rotations), _lib.ptr(translations), q, _lib.ptr(landmarks),
-                                      landmarks.shape[0], cam, float(sigma), _lib.ptr(out), _lib.ptr(mask),
-                                      _device.stream_handle(dev)), "fif_pc_fim")
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().fif_pc_fim(_lib.ptr(rotations), _lib.ptr(translations), q, _lib.ptr(landmarks),
+                                          landmarks.shape[0], cam, float(sigma), _lib.ptr(out), _lib.ptr(mask),
+                                          _device.stream_handle(dev)), "fif_pc_fim")
     return out
 
 
@@ -118,6 +120,43 @@ def exact_pose_fim_batch(rotations, translations, landmark_positions, camera: Pi
     p = _device.to_device_f64(landmark_positions, dev, (3,))
     out = exact_pose_fim_batch_device(r, t, p, camera, sigma)
     return _device.to_numpy(out).reshape(-1, 6, 6)
+
+
+def pc_metric_yaw_batch_device(positions: torch.Tensor, yaws, landmarks: torch.Tensor, camera: PinholeCamera,
+                               sigma: float, r_base, metric: str, out: torch.Tensor | None = None,
+                               fim: torch.Tensor | None = None, mask: torch.Tensor | None = None) -> torch.Tensor:
+    """Exact point-cloud metric at yaw-only poses on the device (kernels.pc_metric_yaw_batch,
+    kernels.py:1599-1606 -> _nb_pc_metric_yaw_batch 611-625): R = Rz(yaw) r_base in the
+    reference's operation order, the point-cloud 6x6, then det / lmin / trace.  cos / sin of
+    the yaws are taken on the host with numpy, as the reference does."""
+    if metric not in _lib.METRIC_IDS:
+        raise ValueError(f"unknown metric {metric!r}; expected one of {METRICS}")
+    dev = positions.device
+    q = positions.shape[0]
+    y = np.asarray(yaws.cpu().numpy() if isinstance(yaws, torch.Tensor) else yaws, dtype=np.float64).reshape(-1)
+    if y.shape[0] != q:
+        raise ValueError("positions and yaws must have the same length")
+    cs = torch.from_numpy(np.ascontiguousarray(np.stack([np.cos(y), np.sin(y)], axis=1))).to(dev)
+    rb = (ctypes.c_double * 9)(*np.asarray(r_base, dtype=np.float64).reshape(9).tolist())
+    if out is None:
+        out = torch.empty(q, dtype=torch.float64, device=dev)
+    cam = _lib.make_camera(camera.as_tuple())
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().fif_pc_metric_yaw(_lib.ptr(positions), _lib.ptr(cs), q, _lib.ptr(landmarks),
+                                                 landmarks.shape[0], cam, float(sigma), ctypes.byref(rb),
+                                                 _lib.METRIC_IDS[metric], _lib.ptr(out), _lib.ptr(fim), _lib.ptr(mask),
+                                                 _device.stream_handle(dev)), "fif_pc_metric_yaw")
+    return out
+
+
+def pc_metric_yaw_batch(positions, yaws, landmark_positions, camera: PinholeCamera, sigma: float, r_base,
+                        metric: str) -> np.ndarray:
+    """Host-array front end of pc_metric_yaw_batch_device (the reference kernel boundary's
+    pc_metric_yaw_batch(positions, yaws, points, cam, sigma, r_base, mid))."""
+    dev = _device.require_cuda()
+    pos = _device.to_device_f64(positions, dev, (3,))
+    pts = _device.to_device_f64(landmark_positions, dev, (3,))
+    return _device.to_numpy(pc_metric_yaw_batch_device(pos, yaws, pts, camera, sigma, r_base, metric))
 
 
 def exact_pose_fim(pose: Pose, landmark_positions, camera: PinholeCamera, sigma: float = DEFAULT_SIGMA) -> np.ndarray:

@@ -23,9 +23,34 @@ import torch
 from . import _device
 from .errors import WrongFactorKind
 from .field import Field
+from .fim import DEFAULT_SIGMA, METRICS, PinholeCamera, pc_metric_yaw_batch_device
+from .scenes import R_CAM_MOUNT, yaw_rotation
 
-__all__ = ["yaw_axes", "metric_yaw_batch", "gate_ok", "PotentialParams", "info_potential", "info_potential_grad",
+__all__ = ["R_CAM_MOUNT", "yaw_rotation", "ExactInfoRepr", "yaw_axes", "metric_yaw_batch", "gate_ok",
+           "PotentialParams", "info_potential", "info_potential_grad",
            "info_cost_grad", "poly_eval", "poly_info_cost_grad"]
+
+
+class ExactInfoRepr:
+    """Information evaluation against the raw landmark set (rrt.py:54-71) on the GPU:
+    `metric_batch(positions, yaws, metric)` runs fif_pc_metric_yaw (the point-cloud 6x6 of
+    each yaw pose, then det / lmin / trace), the planners' exact comparator for a field."""
+
+    def __init__(self, points, camera: PinholeCamera | None = None, sigma: float = DEFAULT_SIGMA, device=None):
+        self.points = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+        self.camera = camera if camera is not None else PinholeCamera.from_fov()
+        self.sigma = float(sigma)
+        self.device = _device.require_cuda(device)
+        self._pts = _device.to_device_f64(self.points, self.device, (3,))
+
+    def metric_batch(self, positions, yaws, metric: str):
+        if metric not in METRICS:
+            raise ValueError(f"unknown metric {metric!r}")
+        pos = _device.to_device_f64(positions, self.device, (3,))
+        vals = pc_metric_yaw_batch_device(pos, np.asarray(yaws, dtype=np.float64).reshape(-1), self._pts,
+                                          self.camera, self.sigma, R_CAM_MOUNT, metric)
+        v = _device.to_numpy(vals)
+        return v, np.ones(len(v), dtype=bool)
 
 
 def yaw_axes(yaws) -> np.ndarray:

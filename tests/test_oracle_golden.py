@@ -136,3 +136,25 @@ def test_fast_cpu_port_matches_reference(g_small, g_models):
         mine = O.build_gp_factors_fast(c, g_small["points"], 1.0, m.samples, m.kinv, m.k_s, np.cos(m.alpha),
                                        kind == "trace", nthreads=2)
         assert np.abs(mine - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_pc_yaw_metric_golden(oracle):
+    """The oracle restatement of pc_metric_yaw_batch (rotation in the reference's operation
+    order, exact FIM, det / lmin / trace) against the reference (tests/golden/pc_yaw.npz)."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "pc_yaw.npz"))
+    c, s, b = np.cos(g["yaws"]), np.sin(g["yaws"]), g["r_base"]
+    q = c.shape[0]
+    rots = np.empty((q, 3, 3))
+    for col in range(3):  # kernels.py:615-621
+        rots[:, 0, col] = c * b[0, col] - s * b[1, col]
+        rots[:, 1, col] = s * b[0, col] + c * b[1, col]
+        rots[:, 2, col] = b[2, col]
+    cam = tuple(g["camera"])
+    fims = oracle.exact_fim_batch(rots, g["positions"], g["points"], cam)
+    assert np.array_equal(oracle.pc_mask(rots, g["positions"], g["points"], cam), g["visible_kernel"])
+    for metric in ("det", "lmin", "trace"):
+        mine = np.array([oracle.metric_of(f, metric) for f in fims])
+        ref = g[metric]
+        assert np.abs(mine - ref).max() <= 1e-12 * np.abs(ref).max(), metric
