@@ -6,12 +6,20 @@ PIF build of the GP-70 model (the reference CLI's default model, cli.py:537)
 over 20 000 room landmarks x an 81x81x21 grid (2.756e9 voxel-landmark pairs).
 A step = one build of this rank's z-slab of the grid; with N ranks the grid is
 split by voxel count (strong scaling, no collective in the inner loop; the
-landmarks are broadcast once over NCCL).  Secondary lines in the same JSON:
-config-2 batched queries (100 000 poses, full 6x6 + analytic gradient) and the
-config-3 point-cloud baseline kernel.
+landmarks are broadcast once over NCCL).
 
---impl reference times the reference algorithm on the host CPU (the C oracle
-port of fifield's numba kernels, all host threads) on the same metric.
+Secondary measurements in the same JSON line:
+  e2e / e2e_export — the public API (Field.build) from pinned host landmarks, with a
+      D2H checksum, and with the reference-layout factors (kinv @ S) exported to host;
+  parity           — the built rows of the CPU-baseline sample voxels vs the CPU port;
+  query            — config-2 queries (1e5 poses, full 6x6 + trace + gradient) + roofline;
+  pc               — config-3 point-cloud kernel (1e6 poses x 2e4 landmarks) + roofline;
+  pc_vs_fif        — FIF queries on the SAME 1e6 poses (speed-up, Table II-style error);
+  masked_build     — config-2 build with range + occlusion gates fused into the kernels.
+
+--impl reference times the reference algorithm on the host CPU (the CPU port of
+fifield's numba kernels, all host threads) on the same metric and config: its K timed
+steps partition the config-2 grid, so together they build the whole field once.
 """
 from __future__ import annotations
 
@@ -31,6 +39,8 @@ sys.path.insert(0, ROOT)
 GP_INFO_FLOPS_PER_PAIR = lambda ns: 94 + 50 * ns   # SURVEY.md §8(d) algorithmic count, FMA = 2
 GP_INFO_MUFU_PER_PAIR = lambda ns: 1 + 2 * ns
 QUERY_ROW_BYTES_GP_INFO = lambda ns: ns * 21 * 4  # FP32 S rows, packed 21 entries
+QUERY_TRACE_ROW_BYTES = lambda ns: ns * 8         # FP64 trace table row (trace outputs of an info field)
+PC_FLOPS_TEST, PC_FLOPS_VISIBLE = 28, 110         # SURVEY.md §8(d) config-3 per-pair count
 METRIC = "FIF build voxel·landmark pairs/s"
 UNIT = "pairs/s"
 
@@ -44,7 +54,7 @@ def parse():
     ap.add_argument("--ns", type=int, default=70)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds for the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip the query / PC secondary measurements")
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary measurements")
     return ap.parse_args()
 
 
@@ -103,12 +113,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-# ── CPU reference leg (oracle port of the reference kernels) ────────
-def cpu_gp_info_rate(points, centers, model, seconds, threads):
-    """Reference GP info build (fast C port) on a voxel sample sized to ~`seconds` of work; returns (pairs/s, sample text)."""
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+PORT_DESC = ("reference algorithm (_nb_build_gp, kernels.py:471-524: vs per landmark, vp = vs @ kinv, vp x I6) as a "
+             "blocked AVX2/FMA C port, OpenMP over voxels (oracle/fif_cpu_fast.c; 1.94x faster per thread than the "
+             "reference's numba+BLAS, so the ratio understates the speed-up over the reference itself)")
+
+
+# ── CPU legs (the reference's algorithm on the host cores) ──────────
+def cpu_gp_info_rate(points, centers, model, seconds, threads, seed=123):
+    """The CPU port on a random voxel sample sized to ~`seconds` of work.
+    Returns (pairs/s, sample text, selected voxel indices, port output rows)."""
     from oracle import oracle as O
 
-    rng = np.random.default_rng(123)
+    rng = np.random.default_rng(seed)
     n = points.shape[0]
     k = max(threads, 16)
     sel = rng.choice(centers.shape[0], k, replace=False)
@@ -120,50 +143,60 @@ def cpu_gp_info_rate(points, centers, model, seconds, threads):
     k2 = max(threads, (k2 // threads) * threads)
     sel = rng.choice(centers.shape[0], k2, replace=False)
     t0 = time.perf_counter()
-    O.build_gp_factors_fast(centers[sel], points, 1.0, model.samples, model.kinv, model.k_s, np.cos(model.alpha),
-                            False, nthreads=threads)
+    out = O.build_gp_factors_fast(centers[sel], points, 1.0, model.samples, model.kinv, model.k_s,
+                                  np.cos(model.alpha), False, nthreads=threads)
     dt = time.perf_counter() - t0
-    return k2 * n / dt, (f"{k2} random config-2 voxels x {n} landmarks (GP-{model.n_v} info), {dt:.2f} s; "
-                         "reference algorithm (vs @ kinv, vp x I6 per landmark) as a blocked AVX2/FMA C port, "
-                         "OpenMP over voxels (oracle/fif_cpu_fast.c)")
-
-
-def host_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except AttributeError:
-        return os.cpu_count() or 1
+    return k2 * n / dt, f"{k2} random config-2 voxels x {n} landmarks (GP-{model.n_v} info), {dt:.2f} s; " + PORT_DESC, \
+        sel, out
 
 
 def run_reference(args, rank, world):
+    """The driver's reference arm: the reference algorithm on every host core, same metric and
+    config.  The K timed steps partition the config-2 voxels (contiguous slices, like the GPU
+    z-slabs), so the run builds the complete 81x81x21 field exactly once; value = all pairs /
+    total time.  Warm-up steps run small samples (untimed)."""
     if rank != 0:
         return 0
+    from oracle import oracle as O
     from paper_2008_03324_b200 import scenes as SC
     from paper_2008_03324_b200.field import GridConfig
+    from paper_2008_03324_b200.parallel import slab_range
     from paper_2008_03324_b200.visibility import build_gp_model
 
     w2 = SC.config2(0)
     grid = GridConfig(*w2.grid)
     model = build_gp_model(args.ns)
     centers = grid.centers()
+    V, N = centers.shape[0], w2.points.shape[0]
     thr = host_threads()
-    for _ in range(max(1, min(args.warmup, 1))):
-        cpu_gp_info_rate(w2.points, centers, model, 1.0, thr)
-    rates = []
-    sample = ""
-    per_step = max(2.0, 60.0 / max(args.steps, 1))
-    for _ in range(args.steps):
-        r, sample = cpu_gp_info_rate(w2.points, centers, model, per_step, thr)
-        rates.append(r)
-    value = float(np.median(rates))
+    cosa = float(np.cos(model.alpha))
+    rng = np.random.default_rng(7)
+    for _ in range(args.warmup):
+        sel = rng.choice(V, 2 * thr, replace=False)
+        O.build_gp_factors_fast(centers[sel], w2.points, 1.0, model.samples, model.kinv, model.k_s, cosa, False,
+                                nthreads=thr)
+    K = max(1, args.steps)
+    step_s = []
+    for s in range(K):
+        v0, v1 = slab_range(V, K, s)
+        t0 = time.perf_counter()
+        O.build_gp_factors_fast(centers[v0:v1], w2.points, 1.0, model.samples, model.kinv, model.k_s, cosa, False,
+                                nthreads=thr)
+        step_s.append(time.perf_counter() - t0)
+    total = float(sum(step_s))
+    value = V * N / total
+    sample = (f"the {K} timed steps partition all {V} config-2 voxels ({V // K}-{-(-V // K)} voxels x {N} landmarks "
+              f"each): together one complete GP-{model.n_v} info build of the 81x81x21 grid, {total:.1f} s; "
+              + PORT_DESC)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": float(2.756e9 / value * 1e3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config-2 room landmarks)",
-        "config": {"workload": f"config2: GP-{args.ns} info build, 20000 room landmarks x 81x81x21 grid @0.25 m",
-                   "global_batch": 137781 * 20000, "sample": sample},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": total / K * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config-2 room landmarks)",
+        "config": {"workload": f"config2: GP-{args.ns} info PIF build, {N} room landmarks x 81x81x21 grid @0.25 m",
+                   "global_batch": int(V * N), "sample": sample, "full_grid_s": total},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_ms_each": [x * 1e3 for x in step_s],
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -245,30 +278,9 @@ def run_ours(args, rank, world, local):
     ms_per_step = dev_ms / args.steps
     pairs_total = V * N
     value = pairs_total / (ms_per_step / 1e3)
+    k_ms = ms_per_step  # the step is k_prep_landmarks (~µs) + k_gp_info_h16
 
-    # dominant kernel: k_gp_info alone (the step also runs the landmark-table prep)
-    k_ms = ms_per_step
-    # e2e through the public API: host landmarks (pinned) -> build -> D2H checksum
-    pts_host = torch.tensor(w2.points).pin_memory()
-    e2e_ms = []
-    for i in range(args.warmup + args.steps):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        d_pts = pts_host.to(dev, non_blocking=True)
-        s64, s32 = FD.build_rows(d_pts, model, False, 1.0, dev, grid=grid, v_begin=v0, v_end=v1, dmodel=dm)
-        chk = s32.sum(dtype=torch.float64).to("cpu", non_blocking=True)
-        b.record(stream)
-        b.synchronize()
-        if i >= args.warmup:
-            e2e_ms.append(a.elapsed_time(b))
-        del s64, s32
-    e2e_step = float(np.mean(e2e_ms))
-    if world > 1:
-        tt = torch.tensor([e2e_step], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_step = float(tt.item())
-    e2e_value = pairs_total / (e2e_step / 1e3)
+    e2e, e2e_export = measure_e2e(args, F, FD, w2, grid, model, dev, stream, flush, world, rank, v0, v1)
 
     clk = clocks.summary()
     peaks = {}
@@ -298,9 +310,8 @@ def run_ours(args, rank, world, local):
                    "wall_s_timed_region": t_wall},
         "gpu_launches": int(launches),
         "clocks": clk,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(pts_host.numel() * 8),
-                "d2h_bytes_per_step": 8, "ms_per_step": e2e_step,
-                "path": "host float64 landmarks (pinned) -> H2D -> fif_build -> D2H checksum"},
+        "e2e": e2e,
+        "e2e_export": e2e_export,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": traffic,
                      "kernel": "k_gp_info_h16", "flops_per_pair": GP_INFO_FLOPS_PER_PAIR(model.n_v),
@@ -309,17 +320,17 @@ def run_ours(args, rank, world, local):
                                   / (sms * 16 * max_mhz * 1e6)},
         "step_ms_each": step_ms,
     }
-    extras = {}
     if not args.no_extras:
-        extras = secondary(args, F, FD, SC, w2, grid, model, dm, pts, dev, stream, flush, world, rank, peaks, sms,
-                           max_mhz)
-        line.update(extras)
+        line.update(secondary(args, F, FD, SC, w2, grid, model, pts, dev, stream, flush, world, rank, peaks, sms,
+                              max_mhz))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         thr = host_threads()
-        cpu_v, sample = cpu_gp_info_rate(w2.points, grid.centers(), model, args.cpu_seconds, thr)
+        centers = grid.centers()
+        cpu_v, sample, sel, port_rows = cpu_gp_info_rate(w2.points, centers, model, args.cpu_seconds, thr)
         line["cpu_baseline"] = {"value": cpu_v, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample}
-        v1, s1 = cpu_gp_info_rate(w2.points, grid.centers(), model, min(4.0, args.cpu_seconds / 3), 1)
-        line["cpu_baseline"]["single_thread"] = {"value": v1, "unit": UNIT, "sample": s1}
+        v1_, s1, _, _ = cpu_gp_info_rate(w2.points, centers, model, min(4.0, args.cpu_seconds / 3), 1, seed=5)
+        line["cpu_baseline"]["single_thread"] = {"value": v1_, "unit": UNIT, "sample": s1}
+        line["parity"] = sampled_parity(FD, grid, model, out64, dm, dev, sel, port_rows)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -327,47 +338,132 @@ def run_ours(args, rank, world, local):
     return 0
 
 
-def secondary(args, F, FD, SC, w2, grid, model, dm, pts, dev, stream, flush, world, rank, peaks, sms, max_mhz):
-    """Config-2 queries (full 6x6 + gradient) and config-3 point-cloud kernel, timed the same way."""
+def measure_e2e(args, F, FD, w2, grid, model, dev, stream, flush, world, rank, v0, v1):
+    """e2e through the public API: Field.build from PINNED host landmarks (H2D inside the timed
+    region; with N ranks the process_group build broadcasts them from rank 0), the field stays
+    on the device (what the GPU queries use), a D2H checksum of it ends the step.  e2e_export
+    adds what the reference's Field.build hands back: the reference-layout factors (kinv @ S,
+    36 per block, FP64) exported and copied to pinned host memory."""
+    import torch
+    import torch.distributed as dist
+
+    pts_host = torch.tensor(w2.points).pin_memory()
+    pg = dist.group.WORLD if world > 1 else None
+    res = {}
+    for export in (False, True):
+        host_out = None
+        if export:
+            host_out = torch.empty(((v1 - v0), model.n_v * 36), dtype=torch.float64).pin_memory()
+        times = []
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fld = F.Field.build(pts_host, grid, model, "info", device=dev, process_group=pg, replicate=False)
+            if export:
+                rows_dev = fld.export_reference()
+                host_out.copy_(rows_dev, non_blocking=True)
+                d2h = host_out.numel() * 8
+            else:
+                chk = fld.storage["f32"].sum(dtype=torch.float64).to("cpu", non_blocking=True)
+                d2h = 8
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                times.append(a.elapsed_time(b))
+            del fld
+        ms = float(np.mean(times))
+        if world > 1:
+            tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        tot_pairs = grid.voxel_count * w2.points.shape[0]
+        res[export] = {"value": tot_pairs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(pts_host.numel() * 8),
+                       "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
+                       "path": ("Field.build(pinned host landmarks) -> device field -> export_reference (kinv @ S, "
+                                "reference layout FP64) -> D2H into pinned host memory" if export else
+                                "Field.build(pinned host landmarks) -> device-resident field (the GPU queries' "
+                                "operand) -> D2H checksum")}
+        del host_out
+    return res[False], res[True]
+
+
+def sampled_parity(FD, grid, model, out64, dm, dev, sel, port_rows):
+    """The timed build's rows for the CPU-baseline sample voxels against the CPU port's rows
+    for the same voxels (reference layout, max |delta| / voxel Frobenius norm; tolerance 1e-4)."""
+    import torch
+
+    from paper_2008_03324_b200 import _lib
+
+    idx = torch.as_tensor(grid.internal_index(grid.index3_of(sel)), device=dev)
+    src = out64[idx].contiguous()
+    ref_dev = torch.empty((src.shape[0], model.n_v * 36), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().fif_export_reference(_lib.KIND_INFO, dm.c, src.data_ptr(), src.shape[0],
+                                                ref_dev.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+               "fif_export_reference")
+    mine = ref_dev.cpu().numpy()
+    err = np.abs(mine - port_rows).max(axis=1) / np.maximum(np.linalg.norm(port_rows, axis=1), 1e-300)
+    return {"voxels": int(len(sel)), "max_entry_over_voxel_frobenius": float(err.max()),
+            "median": float(np.median(err)), "tol": 1e-4, "ok": bool(err.max() <= 1e-4),
+            "against": "the CPU port's rows for the cpu_baseline sample (reference algorithm, FP64)"}
+
+
+def _time(stream, fn, reps, flush=None):
+    import torch
+
+    times = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    return float(np.mean(times))
+
+
+def secondary(args, F, FD, SC, w2, grid, model, pts, dev, stream, flush, world, rank, peaks, sms, max_mhz):
     import torch
 
     from paper_2008_03324_b200.parallel import slab_range
 
     res = {}
+    hbm = float(peaks.get("hbm_gbs", 6550.4))
+    fp32_peak = sms * 128 * 2 * max_mhz * 1e6 / 1e12
+    reps = max(3, args.steps)
+    # ── config-2 queries: replicated field, queries sharded ──
     fld = F.Field.build(pts, grid, model, "info", device=dev)
-    q0, q1 = slab_range(w2.positions.shape[0], world, rank)  # replicated field, queries sharded
+    q0, q1 = slab_range(w2.positions.shape[0], world, rank)
     pos = torch.tensor(w2.positions[q0:q1], device=dev)
     ax = torch.tensor(np.ascontiguousarray(w2.rotations[q0:q1, :, 2]), device=dev)
     out = {}
-    fld.query_device(pos, ax, "trilinear", trace=True, full=True, grad=True, out=out)
-    times = []
-    for _ in range(args.steps):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        fld.query_device(pos, ax, "trilinear", trace=True, full=True, grad=True, out=out)
-        b.record(stream)
-        b.synchronize()
-        times.append(a.elapsed_time(b))
-    qms = float(np.mean(times))
+    run_q = lambda: fld.query_device(pos, ax, "trilinear", trace=True, full=True, grad=True, out=out)  # noqa: E731
+    run_q()
+    qms = _time(stream, run_q, reps, flush)
     q_traffic = None
-    try:  # ncu dram bytes of k_query_prep_gp + k_query_info per query (profiles/ncu_summary.json)
+    try:  # ncu dram bytes of the query kernels per query (profiles/ncu_summary.json)
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         q_traffic = prof["query_per_query"]["dram_bytes"]
     except (OSError, ValueError, KeyError):
         pass
     nq = q1 - q0
-    row = QUERY_ROW_BYTES_GP_INFO(model.n_v)
-    bytes_q = 8 * row + 48 + 8 * (1 + 6 + 36 + 216)  # 8 corner rows + pose in + outputs
-    hbm = float(peaks.get("hbm_gbs", 6550.4))
+    ns = model.n_v
+    bytes_q = 8 * (QUERY_ROW_BYTES_GP_INFO(ns) + QUERY_TRACE_ROW_BYTES(ns)) + 48 + 8 * (1 + 6 + 36 + 216)
     res["query"] = {
         "workload": "config2: 100000 poses, trilinear, full 6x6 + trace + analytic d/d[t;theta], GP-70 info field",
         "value": nq * world / (qms / 1e3), "unit": "queries/s", "ms": qms,
         "roofline": {"bound": "hbm", "achieved": nq * bytes_q / (qms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                      "frac": nq * bytes_q / (qms / 1e3) / 1e9 / hbm, "traffic": q_traffic,
-                     "bytes_per_query": bytes_q},
+                     "bytes_per_query": bytes_q,
+                     "bytes_note": "8 corners x (FP32 S row 21 x N_s x 4 B + FP64 trace-table row N_s x 8 B) + "
+                                   "pose + outputs (trace, 6x6, their gradients) in FP64"},
     }
-    # point cloud (config 3): poses sharded across ranks
+    # ── config-3 point cloud + FIF on the same poses ──
     npose = 1000000
     w3 = SC.config3(npose)
     p0, p1 = slab_range(npose, world, rank)
@@ -375,20 +471,92 @@ def secondary(args, F, FD, SC, w2, grid, model, dm, pts, dev, stream, flush, wor
     t = torch.tensor(w3.positions[p0:p1], device=dev)
     cam = F.PinholeCamera.from_fov()
     outpc = torch.empty((p1 - p0, 36), dtype=torch.float64, device=dev)
-    F.exact_pose_fim_batch_device(r, t, pts, cam, out=outpc)
-    times = []
-    for _ in range(max(1, args.steps // 2)):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        F.exact_pose_fim_batch_device(r, t, pts, cam, out=outpc)
-        b.record(stream)
-        b.synchronize()
-        times.append(a.elapsed_time(b))
-    pms = float(np.mean(times))
+    run_pc = lambda: F.exact_pose_fim_batch_device(r, t, pts, cam, out=outpc)  # noqa: E731
+    run_pc()
+    pms = _time(stream, run_pc, max(1, reps // 2))
+    # visible fraction (needed for the roofline's per-pair count) from a 4 000-pose mask sample
+    ns_vis = min(4000, p1 - p0)
+    vmask = torch.zeros((ns_vis, pts.shape[0]), dtype=torch.uint8, device=dev)
+    F.exact_pose_fim_batch_device(r[:ns_vis].contiguous(), t[:ns_vis].contiguous(), pts, cam, mask=vmask)
+    vis = float(vmask.float().mean().item())
+    del vmask
+    pairs_pc = (p1 - p0) * pts.shape[0]
+    flops_pair = PC_FLOPS_TEST + PC_FLOPS_VISIBLE * vis
+    pc_ach = pairs_pc * flops_pair / (pms / 1e3) / 1e12
     res["pc"] = {"workload": "config3: 1e6 poses x 20000 landmarks, exact pinhole FIM (trace + 6x6)",
-                 "value": (p1 - p0) * w2.points.shape[0] * world / (pms / 1e3), "unit": "pose-landmark pairs/s",
-                 "ms": pms}
+                 "value": pairs_pc * world / (pms / 1e3), "unit": "pose-landmark pairs/s", "ms": pms,
+                 "visible_fraction": vis,
+                 "roofline": {"bound": "fp32", "achieved": pc_ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                              "frac": pc_ach / fp32_peak, "kernel": "k_pc_fim",
+                              "flops_per_pair": flops_pair,
+                              "count": f"SURVEY 8(d): {PC_FLOPS_TEST} flop visibility test + {PC_FLOPS_VISIBLE} flop "
+                                       f"6x6 accumulation x visible fraction {vis:.4f}; the exact FP64 test inside "
+                                       "the FP32 pre-test's margin is not counted"}}
+    res["pc_vs_fif"] = pc_vs_fif(F, w3, p0, p1, fld, pts, outpc, dev, stream, reps, pms, model, grid)
+    # ── masked build: range + occlusion gates fused into the build kernels ──
+    if world == 1:
+        res["masked_build"] = masked_build(F, FD, w2, grid, model, pts, dev, stream, reps)
     return res
+
+
+def pc_vs_fif(F, w3, p0, p1, fld, pts, outpc, dev, stream, reps, pms, model, grid):
+    """N1 / BASELINE configs[2]: FIF queries on the same config-3 poses as the point-cloud
+    kernel (one device), and the FIF-vs-exact error in the style of the paper's Table II
+    (relative Frobenius norm of the 6x6 and relative trace error, median and p90)."""
+    import torch
+
+    q = p1 - p0
+    pos = torch.tensor(w3.positions[p0:p1], device=dev)
+    ax = torch.tensor(np.ascontiguousarray(w3.rotations[p0:p1, :, 2]), device=dev)
+    quad = F.build_quad_model()
+    fq = F.Field.build(pts, grid, quad, "info", device=dev)
+    out = {}
+    for name, f in (("gp70", fld), ("quad", fq)):
+        o = {}
+        run = lambda: f.query_device(pos, ax, "trilinear", trace=True, full=True, out=o)  # noqa: E731
+        run()
+        ms = _time(stream, run, reps)
+        fim = o["fim"]
+        ok = o["status"] == 0
+        d = (fim - outpc).reshape(q, 36)
+        nf = torch.linalg.norm(outpc.reshape(q, 36), dim=1)
+        rel = (torch.linalg.norm(d, dim=1) / torch.clamp(nf, min=1e-300))[ok & (nf > 0)]
+        trp = outpc.reshape(q, 6, 6).diagonal(dim1=1, dim2=2).sum(-1)
+        tre = (torch.abs(o["trace"] - trp) / torch.clamp(trp, min=1e-300))[ok & (trp > 0)]
+        qs = torch.tensor([0.5, 0.9], dtype=torch.float64, device=dev)
+        rq = torch.quantile(rel[:1_000_000].double(), qs).tolist() if rel.numel() else [None, None]
+        tq = torch.quantile(tre[:1_000_000].double(), qs).tolist() if tre.numel() else [None, None]
+        out[name] = {"ms": ms, "queries_per_s": q / (ms / 1e3), "speedup_vs_pc": pms / ms,
+                     "in_field_fraction": float(ok.float().mean().item()),
+                     "rel_fro_6x6": {"median": rq[0], "p90": rq[1]}, "rel_trace": {"median": tq[0], "p90": tq[1]}}
+    return {"workload": f"{q} config-3 poses: exact point-cloud FIM (k_pc_fim, {pms:.2f} ms) vs FIF queries "
+                        "(trilinear, full 6x6 + trace) on the config-2 fields; errors of FIF against the exact FIM",
+            "pc_ms": pms, **out}
+
+
+def masked_build(F, FD, w2, grid, model, pts, dev, stream, reps):
+    """(f)3: config-2 GP-70 info build with range gates and an occluding pillar, the gates
+    evaluated inside the build kernels (no (V, N) mask); occupancy pass + build timed."""
+    import torch
+
+    class _Box:
+        def __init__(self, lo, hi):
+            self.lo, self.hi = np.asarray(lo, float), np.asarray(hi, float)
+
+    class _World:
+        spheres = []
+        boxes = [_Box([-1.0, -1.0, 0.0], [1.0, 1.0, 5.0])]
+
+    mt = F.Matchability(d_near=0.25, d_far=8.0, occluders=_World())
+    run = lambda: F.Field.build(pts, grid, model, "info", matchability=mt, device=dev)  # noqa: E731
+    f = run()
+    ms = _time(stream, run, max(2, reps // 3))
+    cen = FD.device_centers(grid, dev)
+    n_any = int(mt.device_any(cen, pts).sum().item())
+    return {"workload": "config2 GP-70 info build, Matchability(d_near=0.25, d_far=8.0, occluders=2x2x5 m pillar) "
+                        "fused into the build kernels",
+            "ms": ms, "occupied_voxels": n_any, "rows": f.rows, "unit": "ms",
+            "mask_bytes_avoided": int(grid.voxel_count * pts.shape[0])}
 
 
 def main():

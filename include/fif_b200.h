@@ -159,6 +159,17 @@ int fif_query_ex(int factor_kind, const fif_model* model, const fif_grid* grid, 
                  const int32_t* d_slots, const double* d_positions, const double* d_axes, int64_t q, int mode,
                  uint32_t flags, const fif_query_out* out, void* stream);
 
+/* fif_query_ex with the trace outputs of an INFO field taken from d_trace_rows: its FP64
+ * trace table (rows, n_v), T[r][k] = sum of the 6 diagonal entries of block k of the row
+ * (the per-sample trace kernels.py:1414-1423 contracts).  With the FP32 GP query copy the
+ * trace of the contraction cancels (omega = kinv v^r alternates in sign: measured 3.2e-4
+ * relative on config-2 nearest queries, over the 1e-4 tolerance), so the trace is
+ * contracted from FP64 rows (+8 n_v bytes per corner) while the 6x6, det and lambda_min
+ * stream the FP32 rows; one prep serves both.  d_trace_rows NULL = fif_query_ex.      */
+int fif_query_ex2(int factor_kind, const fif_model* model, const fif_grid* grid, const void* d_field,
+                  const double* d_trace_rows, const int32_t* d_slots, const double* d_positions, const double* d_axes,
+                  int64_t q, int mode, uint32_t flags, const fif_query_out* out, void* stream);
+
 /* Point-cloud brute force — replaces kernels.exact_fim_batch
  * (kernels.py:1638-1645 -> _nb_exact_fim 571-599).  R (Q,9) row-major
  * world-from-camera rotations, t (Q,3), landmarks (N,3), all f64.

@@ -28,6 +28,7 @@ EXPORTED = (
     "fif_abi_version", "fif_last_error", "fif_grid_centers", "fif_build_scratch_bytes", "fif_build",
     "fif_export_reference", "fif_query", "fif_query_ex", "fif_pc_fim", "fif_match_mask",
     "fif_launch_count", "fif_locate", "fif_pc_metric_yaw", "fif_match_any", "fif_build_matched",
+    "fif_query_ex2",
 )
 
 
@@ -112,6 +113,9 @@ def load():
         L.fif_pc_metric_yaw.restype = _int
         L.fif_pc_metric_yaw.argtypes = [_p, _p, _i64, _p, _i64, ctypes.POINTER(Camera), _d,
                                         ctypes.POINTER(ctypes.c_double * 9), _int, _p, _p, _p, _p]
+        L.fif_query_ex2.restype = _int
+        L.fif_query_ex2.argtypes = [_int, ctypes.POINTER(Model), ctypes.POINTER(Grid), _p, _p, _p, _p, _p, _i64, _int,
+                                    ctypes.c_uint32, ctypes.POINTER(QueryOut), _p]
         L.fif_match_any.restype = _int
         L.fif_match_any.argtypes = [ctypes.POINTER(Match), _p, _i64, _p, _p, _i64, _p, _p]
         L.fif_build_matched.restype = _int

@@ -1203,6 +1203,14 @@ extern "C" int fif_locate(const fif_grid* grid, const double* d_positions, int64
 extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_grid* grid, const void* d_field,
                             const int32_t* d_slots, const double* d_positions, const double* d_axes, int64_t q,
                             int mode, uint32_t flags, const fif_query_out* o, void* stream) {
+  return fif_query_ex2(factor_kind, model, grid, d_field, nullptr, d_slots, d_positions, d_axes, q, mode, flags, o,
+                       stream);
+}
+
+extern "C" int fif_query_ex2(int factor_kind, const fif_model* model, const fif_grid* grid, const void* d_field,
+                             const double* d_trace_rows, const int32_t* d_slots, const double* d_positions,
+                             const double* d_axes, int64_t q, int mode, uint32_t flags, const fif_query_out* o,
+                             void* stream) {
   FIF_CHECK_ARG(model && grid && o, "fif_query: NULL model/grid/outputs");
   FIF_CHECK_ARG(factor_kind == FIF_KIND_INFO || factor_kind == FIF_KIND_TRACE, "fif_query: bad factor_kind");
   FIF_CHECK_ARG(mode == FIF_MODE_NEAREST || mode == FIF_MODE_TRILINEAR, "fif_query: bad mode %d", mode);
@@ -1231,8 +1239,8 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
       fif_query_out os{sl(o->trace, 1),    sl(o->trace_grad, 6), sl(o->fim, 36),     sl(o->fim_grad, 216),
                        sl(o->det, 1),      sl(o->det_grad, 6),   sl(o->lmin, 1),     sl(o->lmin_grad, 6),
                        o->status ? o->status + q0 : nullptr};
-      const int rc = fif_query_ex(factor_kind, model, grid, d_field, d_slots, d_positions + 3 * q0, d_axes + 3 * q0,
-                                  n, mode, flags, &os, stream);
+      const int rc = fif_query_ex2(factor_kind, model, grid, d_field, d_trace_rows, d_slots, d_positions + 3 * q0,
+                                   d_axes + 3 * q0, n, mode, flags, &os, stream);
       if (rc != FIF_OK) return rc;
     }
     return FIF_OK;
@@ -1248,14 +1256,31 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
                (flags & FIF_Q_LMIN) ? o->lmin : nullptr,
                (flags & FIF_Q_LMIN) && want_g ? o->lmin_grad : nullptr,
                o->status};
+  // trace outputs of an info field from its FP64 trace table (d_trace_rows): the trace
+  // contraction runs as a trace-field contraction on those rows, the remaining outputs on
+  // d_field, both from one prep (corners + rotation weights)
+  const bool split_trace = info && d_trace_rows != nullptr && out.trace != nullptr;
+  QueryOut out_tr{};
+  if (split_trace) {
+    out_tr.trace = out.trace;
+    out_tr.trace_grad = out.trace_grad;
+    out.trace = out.trace_grad = nullptr;
+  }
+  const bool main_work = out.trace || out.fim || out.det || out.lmin;
+  if (split_trace && !main_work) {  // the trace contraction reports the status
+    out_tr.status = out.status;
+    out.status = nullptr;
+  }
   const bool mgrad = info && (out.det_grad || out.lmin_grad);
   const bool grad = want_g && (out.trace_grad || out.fim_grad || mgrad);
+  const bool grad_tr = want_g && out_tr.trace_grad;
   const bool metric = info && (out.det || out.lmin);
   const bool trilinear = mode == FIF_MODE_TRILINEAR;
   cudaStream_t st = (cudaStream_t)stream;
   // small GP info batches (latency-bound): one fused kernel, one CTA per query
   static const bool no_small = getenv("FIF_QUERY_NO_FUSED_SMALL") != nullptr;
-  if (info && model->kind == FIF_MODEL_GP && !(flags & FIF_Q_FIELD_F64) && q <= (int64_t)num_sms() * 3 && !no_small &&
+  if (!split_trace && info && model->kind == FIF_MODEL_GP && !(flags & FIF_Q_FIELD_F64) &&
+      q <= (int64_t)num_sms() * 3 && !no_small &&
       (size_t)nv * 21 * 4 * (trilinear ? 8 : 1) + (size_t)nv * nv * 8 <= 150 * 1024) {
     const float* ff = reinterpret_cast<const float*>(d_field);
     const int tri = trilinear ? 1 : 0;
@@ -1333,14 +1358,15 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
     const int tri = trilinear ? 1 : 0;
     const bool small = q <= 1024;
     const size_t sm = small ? dmma_smem - sizeof(double) * (size_t)(QD_Q - 8) * np8 : dmma_smem;
+    const bool pgrad = grad || grad_tr;
     switch (ntiles) {
 #define PG(NT)                                                                                                   \
   case NT:                                                                                                       \
-    if (small && grad) launch_prep_gp<NT, 8, 4>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, \
+    if (small && pgrad) launch_prep_gp<NT, 8, 4>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, \
                                                 s_rows, s_cw, wtd, perm);                                        \
     else if (small) launch_prep_gp<NT, 8, 1>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status,   \
                                              s_rows, s_cw, wtd, perm);                                           \
-    else if (grad) launch_prep_gp<NT, 32, 4>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status,   \
+    else if (pgrad) launch_prep_gp<NT, 32, 4>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status,   \
                                              s_rows, s_cw, wtd, perm);                                           \
     else launch_prep_gp<NT, 32, 1>(sm, q, st, *model, gm, d_slots, d_positions, d_axes, tri, s_status, s_rows,     \
                                    s_cw, wtd, perm);                                                             \
@@ -1358,10 +1384,15 @@ extern "C" int fif_query_ex(int factor_kind, const fif_model* model, const fif_g
     FIF_CHECK_LAUNCH("k_query_prep");
   }
   const bool f64 = model->kind == FIF_MODEL_QUAD || (flags & FIF_Q_FIELD_F64);
-  int rc = f64 ? launch_contract<double>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q,
-                                         s_status, s_rows, s_cw, s_wt, out, perm, st)
-               : launch_contract<float>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q,
-                                        s_status, s_rows, s_cw, s_wt, out, perm, st);
+  int rc = FIF_OK;
+  if (main_work || !split_trace)
+    rc = f64 ? launch_contract<double>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q, s_status,
+                                       s_rows, s_cw, s_wt, out, perm, st)
+             : launch_contract<float>(factor_kind, trilinear, grad, metric, mgrad, nv, d_field, d_axes, q, s_status,
+                                      s_rows, s_cw, s_wt, out, perm, st);
+  if (rc == FIF_OK && split_trace)
+    rc = launch_contract<double>(FIF_KIND_TRACE, trilinear, grad_tr, false, false, nv, d_trace_rows, d_axes, q,
+                                 s_status, s_rows, s_cw, s_wt, out_tr, perm, st);
   if (sort_buf) cudaFreeAsync(sort_buf, st);
   cudaFreeAsync(scratch, st);
   return rc;

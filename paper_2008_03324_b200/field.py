@@ -432,6 +432,7 @@ class Field:
         self._dm = _DeviceModel(self.model, self.device)
         self._grid_c = _lib.make_grid(self.config.origin, self.config.voxel_size, self.config.dims)
         self._ref_cache = None
+        self._t64 = None
         if dense:
             self._occ3 = None
             self._slots_np = None
@@ -492,10 +493,25 @@ class Field:
     # ── construction ────────────────────────────────────────────────
     @staticmethod
     def build(landmarks, config, model, factor_kind: str = "info", matchability: Matchability = ALWAYS_MATCH,
-              sigma: float = DEFAULT_SIGMA, parallel: bool = False, device=None, exact: bool = False) -> "Field":
+              sigma: float = DEFAULT_SIGMA, parallel: bool = False, device=None, exact: bool = False,
+              process_group=None, replicate: bool = True) -> "Field":
         """Build every voxel's factor on the GPU.  `parallel` is accepted for API
         compatibility (the GPU build is always parallel).  exact=True (quad model)
-        reproduces the reference's FP64 operation order bit for bit."""
+        reproduces the reference's FP64 operation order bit for bit.  With a torch.distributed
+        `process_group` (one rank per GPU; the default group when it is the WORLD) the grid
+        is built as z-slabs across the ranks (parallel.build_field): replicate=True returns the
+        whole field on every rank, replicate=False this rank's slab."""
+        if process_group is not None:
+            import torch.distributed as dist
+
+            if process_group is not dist.group.WORLD:
+                raise NotImplementedError("sharded builds run on the default (WORLD) process group")
+            if not matchability.is_trivial:
+                raise NotImplementedError("sharded builds support ALWAYS_MATCH")
+            from .parallel import build_field
+
+            pts, _ = _as_points(landmarks)
+            return build_field(pts, config, model, factor_kind, sigma, _device.require_cuda(device), replicate)
         config = _grid_of(config)
         if config.voxel_count == 0:
             raise EmptyGrid("grid has zero voxels")
@@ -567,9 +583,27 @@ class Field:
         return mode == "trilinear"
 
     def _field_ptr(self, use_f64: bool):
-        if isinstance(self.model, QuadraticVisibility) or use_f64 or self._s32 is None:
+        # trace-kind GP fields always contract the FP64 master: with the FP32 copy, the
+        # trace omega . T cancels (omega = kinv v^r alternates in sign) to 3e-4 relative on
+        # config-2 nearest queries, over the 1e-4 tolerance; FP64 rows are 8 N_s B per corner
+        if (isinstance(self.model, QuadraticVisibility) or use_f64 or self._s32 is None
+                or not self._is_info):
             return self._s64, True
         return self._s32, False
+
+    def trace_table(self) -> torch.Tensor | None:
+        """FP64 (rows, n_v) per-sample trace of a GP info field's pre-kinv rows (the
+        diagonal kernels.py:1414-1423 sums, left to right); the trace outputs of info-field
+        queries contract it instead of the FP32 copy (fif_query_ex2).  Built on first use."""
+        if not (self._is_info and isinstance(self.model, GpVisibility)):
+            return None
+        if self._t64 is None or self._t64.shape[0] != self.rows:
+            v = self._s64.view(self.rows, self.model.n_v, 21)
+            t = v[:, :, 0].clone()
+            for k in (6, 11, 15, 18, 20):  # packed diagonal entries (1,1) ... (5,5)
+                t += v[:, :, k]
+            self._t64 = t.contiguous()
+        return self._t64
 
     def query_device(self, positions: torch.Tensor, axes: torch.Tensor, mode: str = "trilinear",
                      trace: bool = True, full: bool = False, grad: bool = False, det: bool = False,
@@ -634,11 +668,13 @@ class Field:
         if self.rows == 0:
             slots = torch.full((self.config.voxel_count,), -1, dtype=torch.int32, device=dev)
         o = _lib.QueryOut(*(_lib.ptr(t) for t in (tr_t, trg_t, fim_t, fimg_t, det_t, detg_t, lmin_t, lming_t, st_t)))
+        # trace outputs of a GP info field come from the FP64 trace table (see trace_table)
+        ttab = self.trace_table() if (trace and not is64 and self.rows > 0) else None
         with torch.cuda.device(dev):
-            _lib.check(_lib.load().fif_query_ex(kind, self._dm.c, self._grid_c, _lib.ptr(field_t), _lib.ptr(slots),
-                                                _lib.ptr(positions), _lib.ptr(axes), q,
-                                                _lib.MODE_TRILINEAR if trilinear else _lib.MODE_NEAREST, flags, o,
-                                                _device.stream_handle(dev)), "fif_query")
+            _lib.check(_lib.load().fif_query_ex2(kind, self._dm.c, self._grid_c, _lib.ptr(field_t), _lib.ptr(ttab),
+                                                 _lib.ptr(slots), _lib.ptr(positions), _lib.ptr(axes), q,
+                                                 _lib.MODE_TRILINEAR if trilinear else _lib.MODE_NEAREST, flags, o,
+                                                 _device.stream_handle(dev)), "fif_query")
         return out
 
     def query_graph(self, batch: int, mode: str = "trilinear", outputs=("trace", "full"), grad: bool = False,
@@ -819,6 +855,7 @@ class Field:
         if self._s32 is not None:
             self._s32 = self._s64.float()
         self._ref_cache = None
+        self._t64 = None
 
     def add_landmarks(self, landmarks, view_dirs=None) -> None:
         self._increment(landmarks, view_dirs, +1.0)
@@ -949,9 +986,9 @@ def _from_reference_rows(factors: np.ndarray, model, factor_kind: str) -> np.nda
 
 
 def build(landmarks, config, model, factor_kind="info", matchability=ALWAYS_MATCH, sigma=DEFAULT_SIGMA,
-          parallel=False, device=None) -> Field:
+          parallel=False, device=None, **kw) -> Field:
     """Module-level alias for Field.build (field.py:645-648)."""
-    return Field.build(landmarks, config, model, factor_kind, matchability, sigma, parallel, device)
+    return Field.build(landmarks, config, model, factor_kind, matchability, sigma, parallel, device, **kw)
 
 
 class QueryGraph:

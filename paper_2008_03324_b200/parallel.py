@@ -26,7 +26,10 @@ def slab_range(total: int, world: int, rank: int) -> tuple[int, int]:
 def broadcast_points(points, device, src: int = 0) -> torch.Tensor:
     """One broadcast of the (N,3) float64 landmarks from `src` to every rank."""
     if dist.get_rank() == src:
-        t = torch.as_tensor(np.ascontiguousarray(points, dtype=np.float64)).to(device)
+        if isinstance(points, torch.Tensor):  # e.g. pinned host memory: one direct H2D copy
+            t = points.to(device=device, dtype=torch.float64).reshape(-1, 3).contiguous()
+        else:
+            t = torch.as_tensor(np.ascontiguousarray(points, dtype=np.float64)).to(device)
         n = torch.tensor([t.shape[0]], dtype=torch.int64, device=device)
     else:
         n = torch.zeros(1, dtype=torch.int64, device=device)
@@ -75,6 +78,27 @@ def build_sharded(points, config, model, factor_kind: str, sigma: float = 1.0, d
     return v0, v1, rows64, rows32, full
 
 
+def build_field(points, config, model, factor_kind: str = "info", sigma: float = 1.0, device=None,
+                replicate: bool = True):
+    """Sharded build through the public Field type (Field.build(..., process_group=...)):
+    rank 0's landmarks broadcast once, each rank builds its z-slab (no collective in the
+    inner loop), then either an all-gather of the FP64 rows gives every rank the whole dense
+    field (replicate=True), or the rank keeps its slab as a Field over the global grid
+    (voxels of other ranks read as absent)."""
+    from .field import Field, GpVisibility, _grid_of
+
+    config = _grid_of(config)
+    v0, v1, rows64, rows32, full = build_sharded(points, config, model, factor_kind, sigma, device, replicate)
+    from .visibility import model_from_reference
+
+    model = model_from_reference(model)
+    if replicate:
+        f32 = full.float() if isinstance(model, GpVisibility) else None
+        return Field(config, model, factor_kind, sigma, full, f32, None, dense=True)
+    occ3 = config.index3_of_internal(np.arange(v0, v1)).astype(np.int32)
+    return Field(config, model, factor_kind, sigma, rows64, rows32, occ3, dense=False)
+
+
 # ── slab-routed queries (fields larger than one GPU's HBM) ─────────────────
 # SURVEY §8(e): each rank keeps the z-planes it owns plus a one-plane halo (the upper
 # trilinear corner), queries are routed to the owner of their base z-index with an
@@ -101,51 +125,65 @@ def slab_rows_range(config, world: int, rank: int) -> tuple[int, int, int, int]:
     return z0, z1, z0 * nx * ny, zh * nx * ny
 
 
-def query_owners(positions: np.ndarray, config, world: int, trilinear: bool) -> np.ndarray:
+def query_owners(positions, config, world: int, trilinear: bool):
     """Owner rank of each query: the rank whose planes hold its base z-index (trilinear:
     floor((z - o_z)/vs - 0.5), so both corner planes are on the owner; nearest:
     floor((z - o_z)/vs)); out-of-field queries go to the nearest plane's owner, which
-    reports the out-of-field status."""
+    reports the out-of-field status.  numpy in -> numpy out; torch in -> torch out on the
+    same device.  The FP64 expression is the query kernels' locate (kernels.py:628-635,
+    679-702) operation for operation, so the owner always holds the corners it reads."""
     nz = int(config.dims[2])
+    starts = [plane_range(nz, world, r)[0] for r in range(world)]
+    hi = max(nz - (2 if trilinear else 1), 0)
+    if isinstance(positions, torch.Tensor):
+        g = (positions[:, 2].to(torch.float64) - float(config.origin[2])) / float(config.voxel_size)
+        if trilinear:
+            g = g - 0.5
+        bz = torch.clamp(torch.floor(g), 0, hi).to(torch.int64)
+        st = torch.tensor(starts, dtype=torch.int64, device=positions.device)
+        return torch.searchsorted(st, bz, right=True) - 1
     g = (np.asarray(positions, dtype=np.float64)[:, 2] - config.origin[2]) / config.voxel_size
     if trilinear:
         g = g - 0.5
-    bz = np.clip(np.floor(g), 0, max(nz - (2 if trilinear else 1), 0)).astype(np.int64)
-    starts = np.array([plane_range(nz, world, r)[0] for r in range(world)])
-    return np.searchsorted(starts, bz, side="right") - 1
+    bz = np.clip(np.floor(g), 0, hi).astype(np.int64)
+    return np.searchsorted(np.array(starts), bz, side="right") - 1
 
 
-def route_queries(positions, axes, config, trilinear: bool, query_fn, outputs) -> dict:
+def route_queries(positions, axes, config, trilinear: bool, query_fn, outputs, device=None) -> dict:
     """Run this rank's queries on their owners.  `query_fn(pos (n,3), axes (n,3)) ->
-    {name: array (n, width)}` answers queries against this rank's slab; `outputs` names
-    the entries of QUERY_WIDTHS wanted.  Returns {name: (Q, width) float64 array} in the
-    caller's order.  Collectives: two all_to_all_single (requests, results) + sizes."""
+    {name: (n, width) tensor or array}` answers queries against this rank's slab; `outputs`
+    names the entries of QUERY_WIDTHS wanted.  Returns {name: (Q, width) float64 tensor} in
+    the caller's order, on `device` (default: the device of `positions` if it is a tensor,
+    else the CPU).  Every exchanged buffer (counts, requests, results) is a tensor on that
+    device, so the collectives run on NCCL for CUDA tensors and on gloo for CPU tensors;
+    the only host transfer is the split sizes all_to_all_single needs.  Collectives: one
+    all_to_all_single of the counts, one of the requests, one of the results."""
     world = dist.get_world_size()
-    pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
-    ax = np.ascontiguousarray(axes, dtype=np.float64).reshape(-1, 3)
+    if device is None:
+        device = positions.device if isinstance(positions, torch.Tensor) else torch.device("cpu")
+    pos = torch.as_tensor(positions, dtype=torch.float64).to(device).reshape(-1, 3)
+    ax = torch.as_tensor(axes, dtype=torch.float64).to(device).reshape(-1, 3)
     owner = query_owners(pos, config, world, trilinear)
-    order = np.argsort(owner, kind="stable")
-    send_counts = np.bincount(owner, minlength=world)
-    sc = torch.tensor(send_counts, dtype=torch.int64)
-    rc = torch.empty_like(sc)
-    dist.all_to_all_single(rc, sc)
-    recv_counts = rc.numpy()
-    req = torch.from_numpy(np.concatenate([pos[order], ax[order]], axis=1).reshape(-1))
-    got = torch.empty(int(recv_counts.sum()) * 6, dtype=torch.float64)
-    dist.all_to_all_single(got, req, output_split_sizes=[int(c) * 6 for c in recv_counts],
-                           input_split_sizes=[int(c) * 6 for c in send_counts])
-    got = got.numpy().reshape(-1, 6)
+    order = torch.argsort(owner, stable=True)
+    send_counts = torch.bincount(owner, minlength=world).to(torch.int64)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts)
+    sc, rc = send_counts.tolist(), recv_counts.tolist()
+    req = torch.cat([pos[order], ax[order]], dim=1).contiguous()
+    got = torch.empty((sum(rc), 6), dtype=torch.float64, device=device)
+    dist.all_to_all_single(got, req, output_split_sizes=rc, input_split_sizes=sc)
     names = [n for n in QUERY_WIDTHS if n in outputs or n == "status"]
     width = sum(QUERY_WIDTHS[n] for n in names)
-    res = query_fn(got[:, :3], got[:, 3:]) if got.shape[0] else {n: np.zeros((0, QUERY_WIDTHS[n])) for n in names}
-    packed = np.concatenate([np.asarray(res[n], dtype=np.float64).reshape(got.shape[0], -1) for n in names], axis=1) \
-        if got.shape[0] else np.zeros((0, width))
-    back = torch.empty(pos.shape[0] * width, dtype=torch.float64)
-    dist.all_to_all_single(back, torch.from_numpy(np.ascontiguousarray(packed).reshape(-1)),
-                           output_split_sizes=[int(c) * width for c in send_counts],
-                           input_split_sizes=[int(c) * width for c in recv_counts])
-    back = back.numpy().reshape(-1, width)
-    out = np.empty_like(back)
+    n_got = got.shape[0]
+    if n_got:
+        res = query_fn(got[:, :3].contiguous(), got[:, 3:].contiguous())
+        packed = torch.cat([torch.as_tensor(res[n]).to(device=device, dtype=torch.float64).reshape(n_got, -1)
+                            for n in names], dim=1).contiguous()
+    else:
+        packed = torch.zeros((0, width), dtype=torch.float64, device=device)
+    back = torch.empty((pos.shape[0], width), dtype=torch.float64, device=device)
+    dist.all_to_all_single(back, packed, output_split_sizes=sc, input_split_sizes=rc)
+    out = torch.empty_like(back)
     out[order] = back
     result, col = {}, 0
     for n in names:
@@ -182,10 +220,9 @@ def query_slab_field(slab_field, positions, axes, mode: str = "trilinear", outpu
         names |= {n + "_grad" for n in list(names)}
     dev = slab_field.device
 
-    def fn(p, a):
-        r = slab_field.query_device(torch.from_numpy(np.ascontiguousarray(p)).to(dev),
-                                    torch.from_numpy(np.ascontiguousarray(a)).to(dev), mode, trace="trace" in outs,
-                                    full="full" in outs, det="det" in outs, lmin="lmin" in outs, grad=grad)
-        return {k: v.reshape(v.shape[0], -1).double().cpu().numpy() for k, v in r.items()}
+    def fn(p, a):  # device tensors in, device tensors out
+        r = slab_field.query_device(p, a, mode, trace="trace" in outs, full="full" in outs, det="det" in outs,
+                                    lmin="lmin" in outs, grad=grad)
+        return {k: v.reshape(v.shape[0], -1) for k, v in r.items()}
 
-    return route_queries(positions, axes, slab_field.config, mode == "trilinear", fn, names)
+    return route_queries(positions, axes, slab_field.config, mode == "trilinear", fn, names, device=dev)

@@ -279,8 +279,8 @@ def test_config2_10k_queries_and_1k_gradients(oracle, models):
     egf = _relf(res["fim_grad"][keep], g_fim)
     print(f", {keep.size} FD gradients: trace {eg.max():.2e}, 6x6 {egf.max():.2e}")
     assert eg.max() <= Q_TOL and egf.max() <= Q_TOL
-    # nearest mode on the same batch
-    rn = f.query_batch(w.positions, rotations=w.rotations, outputs=("trace",), mode="nearest", to_numpy=True)
+    # nearest mode on the same batch (one corner: no blending to average the copy's rounding)
+    rn = f.query_batch(w.positions, rotations=w.rotations, outputs=("trace", "full"), mode="nearest", to_numpy=True)
     locn = f.locate(w.positions, "nearest")
     needn = np.unique(locn["index"][locn["index"] >= 0])
     sl = np.full(grid.voxel_count, -1, np.int32)
@@ -289,7 +289,38 @@ def test_config2_10k_queries_and_1k_gradients(oracle, models):
     ax = np.ascontiguousarray(w.rotations[:, :, 2])
     tn, stn = oracle.metric_batch(sl, rr, grid.origin, grid.voxel_size, grid.dims, w.positions, ax, oracle_model(m),
                                   "trace", False, False)
+    fn, _ = oracle.query_fim_batch(sl, rr, grid.origin, grid.voxel_size, grid.dims, w.positions, ax, oracle_model(m),
+                                   False)
+    print(f"config2 10k nearest: trace {_relv(rn['trace'], tn).max():.2e}, 6x6 {_relf(rn['fim'], fn).max():.2e}")
     assert np.array_equal(rn["in_field"], stn == 0) and _relv(rn["trace"], tn).max() <= Q_TOL
+    assert _relf(rn["fim"], fn).max() <= Q_TOL
+
+
+@pytest.mark.parametrize("mode", ["nearest", "trilinear"])
+def test_config2_trace_field_10k_queries(oracle, models, mode):
+    """GP-70 TRACE field on config 2 (the FP64 master is the query operand), 10 000 queries."""
+    w = scenes.config2(10000)
+    grid = F.GridConfig(*w.grid)
+    m = models["gp70"]
+    f = F.Field.build(w.points, grid, m, "trace")
+    res = f.query_batch(w.positions, rotations=w.rotations, outputs=("trace",), grad=mode == "trilinear",
+                        mode=mode, to_numpy=True)
+    loc = f.locate(w.positions, mode)
+    need = np.unique(loc["index"][loc["index"] >= 0])
+    slots = np.full(grid.voxel_count, -1, np.int32)
+    slots[need] = np.arange(need.size, dtype=np.int32)
+    rows = f.export_reference(f.slots[need]).cpu().numpy()
+    ax = np.ascontiguousarray(w.rotations[:, :, 2])
+    tr, st = oracle.metric_batch(slots, rows, grid.origin, grid.voxel_size, grid.dims, w.positions, ax,
+                                 oracle_model(m), "trace", True, mode == "trilinear")
+    e = _relv(res["trace"], tr)
+    print(f"config2 trace field {mode}: 10k queries trace rel {e.max():.2e}")
+    assert np.array_equal(res["in_field"], st == 0) and e.max() <= Q_TOL
+    if mode == "trilinear":
+        keep = np.nonzero(_away_from_faces(grid, w.positions))[0][:500]
+        g_tr, _ = _fd(oracle, slots, rows, grid, m, "trace", w.positions[keep], w.rotations[keep], False)
+        eg = np.linalg.norm(res["trace_grad"][keep] - g_tr, axis=1) / np.linalg.norm(g_tr, axis=1)
+        assert eg.max() <= Q_TOL
 
 
 # ── config 3: 10 000 poses, masks bit-exact ─────────────────────────

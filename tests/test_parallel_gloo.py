@@ -80,7 +80,7 @@ def _routed_worker(rank, world, port, result_path, trilinear):
     try:
         from oracle import oracle as O
         import paper_2008_03324_b200 as F
-        from paper_2008_03324_b200.parallel import route_queries, slab_rows_range
+        from paper_2008_03324_b200.parallel import query_owners, route_queries, slab_rows_range
 
         grid = F.GridConfig(np.array([-1.0, -1.0, 0.0]), 0.5, np.array([4, 3, 7]))
         model = F.build_quad_model()
@@ -97,7 +97,8 @@ def _routed_worker(rank, world, port, result_path, trilinear):
         slots[lin] = np.arange(v1 - v0, dtype=np.int32)
         slab = full[lin]
 
-        def query_fn(p, a):
+        def query_fn(p, a):  # CPU tensors in (gloo), numpy arrays out
+            p, a = p.numpy(), a.numpy()
             fim, st = O.query_fim_batch(slots, slab, grid.origin, grid.voxel_size, grid.dims, p, a, om, trilinear)
             tr, _ = O.metric_batch(slots, slab, grid.origin, grid.voxel_size, grid.dims, p, a, om, "trace", False,
                                    trilinear)
@@ -108,7 +109,10 @@ def _routed_worker(rank, world, port, result_path, trilinear):
         pos = rng.uniform(c[0] - 0.4, c[-1] + 0.4, size=(50 + 7 * rank, 3))
         ax = rng.standard_normal((pos.shape[0], 3))
         ax /= np.linalg.norm(ax, axis=1, keepdims=True)
-        got = route_queries(pos, ax, grid, trilinear, query_fn, {"trace", "fim"})
+        got = {k: v.numpy() for k, v in route_queries(pos, ax, grid, trilinear, query_fn, {"trace", "fim"}).items()}
+        own_np = query_owners(pos, grid, world, trilinear)
+        own_t = query_owners(torch.from_numpy(pos), grid, world, trilinear).numpy()
+        assert np.array_equal(own_np, own_t)  # torch routing == numpy routing, bit for bit
         all_slots = np.arange(grid.voxel_count, dtype=np.int32)
         fim, st = O.query_fim_batch(all_slots, full, grid.origin, grid.voxel_size, grid.dims, pos, ax, om, trilinear)
         tr, _ = O.metric_batch(all_slots, full, grid.origin, grid.voxel_size, grid.dims, pos, ax, om, "trace", False,
