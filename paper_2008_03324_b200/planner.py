@@ -27,7 +27,8 @@ from .fim import DEFAULT_SIGMA, METRICS, PinholeCamera, pc_metric_yaw_batch_devi
 from .scenes import R_CAM_MOUNT, yaw_rotation
 
 __all__ = ["R_CAM_MOUNT", "yaw_rotation", "ExactInfoRepr", "yaw_axes", "metric_yaw_batch", "gate_ok",
-           "PotentialParams", "info_potential", "info_potential_grad",
+           "PotentialParams", "info_potential", "info_potential_grad", "JunctionBasis", "InfoTrajectoryProblem",
+           "optimize_info_trajectory",
            "info_cost_grad", "poly_eval", "poly_info_cost_grad"]
 
 
@@ -170,3 +171,197 @@ def poly_info_cost_grad(field: Field, coeffs, durations, times, metric: str, pot
     for a in range(4):
         np.add.at(grad[a], seg, g[:, a:a + 1] * basis)
     return cost, grad
+
+
+# ── trajectory optimisation with the analytic information gradient ─────────
+# The reference optimises the free junction derivatives of a piecewise polynomial with
+# L-BFGS-B (traj.optimize_trajectory, traj.py:411-463); its gradient of the sampled cost is
+# a central difference per free parameter (traj._FreeParamProblem.gradient, traj.py:383-398:
+# 2 x n_free cost evaluations, each a batched metric query).  InfoTrajectoryProblem keeps the
+# reference's parametrisation and cost (dynamic term + information potential; the obstacle
+# term is out of scope here) and differentiates the information term analytically: one
+# batched GPU query with pose gradients, chained through the (linear) junction -> coefficient
+# -> sample maps.
+
+NDERIV = 4  # junction continuity: value + derivatives 1..3 (traj.py:27)
+
+
+def _hermite_matrix(T: float) -> np.ndarray:
+    """Coefficients (ascending powers 0..7) -> derivatives 0..3 at both ends of [0, T]."""
+    import math
+
+    A = np.zeros((8, 8))
+    for k in range(NDERIV):
+        A[k, k] = math.factorial(k)
+        for i in range(k, 8):
+            A[NDERIV + k, i] = math.perm(i, k) * T ** (i - k)
+    return A
+
+
+def _deriv_gram(T: float, k: int) -> np.ndarray:
+    """Q with c^T Q c = integral over [0, T] of the squared k-th derivative."""
+    import math
+
+    Q = np.zeros((8, 8))
+    for i in range(k, 8):
+        for j in range(k, 8):
+            p = i + j - 2 * k + 1
+            Q[i, j] = math.perm(i, k) * math.perm(j, k) * T ** p / p
+    return Q
+
+
+class JunctionBasis:
+    """Linear maps between stacked junction derivatives D (per axis, length 4 (S + 1)) and
+    per-segment coefficients, and the quadratic dynamic-cost forms (traj.py:50-89)."""
+
+    def __init__(self, durations):
+        self.durations = np.asarray(durations, dtype=np.float64).reshape(-1)
+        if (self.durations <= 0).any() or not np.isfinite(self.durations).all():
+            raise ValueError("segment durations must be positive and finite")
+        self.S = len(self.durations)
+        self.L = NDERIV * (self.S + 1)
+        self.M = [np.linalg.inv(_hermite_matrix(T)) for T in self.durations]
+
+    def cost_matrix(self, order: int) -> np.ndarray:
+        R = np.zeros((self.L, self.L))
+        for s, T in enumerate(self.durations):
+            i = NDERIV * s
+            R[i:i + 8, i:i + 8] += self.M[s].T @ _deriv_gram(T, order) @ self.M[s]
+        return R
+
+    def coeffs_from_derivs(self, D: np.ndarray) -> np.ndarray:
+        """D (..., L) -> coefficients (..., S, 8)."""
+        D = np.asarray(D, dtype=np.float64)
+        out = np.empty(D.shape[:-1] + (self.S, 8))
+        for s in range(self.S):
+            out[..., s, :] = D[..., NDERIV * s:NDERIV * s + 8] @ self.M[s].T
+        return out
+
+    def derivs_grad_from_coeffs_grad(self, G: np.ndarray) -> np.ndarray:
+        """Adjoint of coeffs_from_derivs: d cost / d coeffs (..., S, 8) -> d cost / d D (..., L)."""
+        out = np.zeros(G.shape[:-2] + (self.L,))
+        for s in range(self.S):
+            out[..., NDERIV * s:NDERIV * s + 8] += G[..., s, :] @ self.M[s]
+        return out
+
+
+class InfoTrajectoryProblem:
+    """traj._FreeParamProblem (traj.py:308-398) over a GPU field: free parameters are the
+    derivatives 0..3 of every axis at the internal junctions; cost = mu_d sum_axes D^T R D
+    (snap for x, y, z, yaw acceleration) + mu_v dt sum_t pot(metric(state_t)).
+    `gradient` is analytic (one batched query); `gradient_fd` is the reference's central
+    difference (2 x n_free sampled-cost evaluations), kept for comparison."""
+
+    def __init__(self, D0, durations, field: Field, potential: PotentialParams, metric: str = "det",
+                 mode: str = "trilinear", mu_d: float = 1.0, mu_v: float = 1.0, dt: float = 0.1,
+                 fd_step: float = 1e-4):
+        self.basis = JunctionBasis(durations)
+        self.D0 = np.asarray(D0, dtype=np.float64).reshape(4, self.basis.L).copy()
+        self.free_idx = np.arange(NDERIV, self.basis.L - NDERIV)
+        self.field, self.potential, self.metric, self.mode = field, potential, metric, mode
+        self.mu_d, self.mu_v, self.dt, self.fd_step = mu_d, mu_v, dt, fd_step
+        self.R = [self.basis.cost_matrix(4), self.basis.cost_matrix(2)]
+        k = max(1, int(round(float(self.basis.durations.sum()) / dt)))
+        self.times = np.arange(k) * dt
+        self.n_evals = 0  # sampled-cost evaluations (batched field queries), as the reference counts them
+
+    def x0(self) -> np.ndarray:
+        return self.D0[:, self.free_idx].reshape(-1).copy()
+
+    def derivs(self, x) -> np.ndarray:
+        D = self.D0.copy()
+        D[:, self.free_idx] = np.asarray(x, dtype=np.float64).reshape(4, -1)
+        return D
+
+    def coeffs(self, x) -> np.ndarray:
+        return self.basis.coeffs_from_derivs(self.derivs(x))
+
+    def _dynamic(self, D):
+        cost, grad = 0.0, np.zeros_like(D)
+        for a in range(4):
+            RD = self.R[0 if a < 3 else 1] @ D[a]
+            cost += float(D[a] @ RD)
+            grad[a] = 2.0 * RD
+        return self.mu_d * cost, self.mu_d * grad
+
+    def _sampled(self, coeffs, with_grad: bool):
+        self.n_evals += 1
+        if with_grad:
+            return poly_info_cost_grad(self.field, coeffs, self.basis.durations, self.times, self.metric,
+                                       self.potential, self.mu_v, self.dt, self.mode)
+        vals = poly_eval(coeffs, self.basis.durations, self.times)
+        r = metric_yaw_batch(self.field, vals[:, :3], vals[:, 3], self.metric, self.mode)
+        pot = np.where(r["in_field"], info_potential(r["values"], self.potential), self.potential.b_l)
+        return float(self.mu_v * pot.sum() * self.dt), None
+
+    def cost(self, x) -> float:
+        D = self.derivs(x)
+        return self._dynamic(D)[0] + self._sampled(self.basis.coeffs_from_derivs(D), False)[0]
+
+    def cost_and_gradient(self, x):
+        D = self.derivs(x)
+        dc, dg = self._dynamic(D)
+        sc, sg = self._sampled(self.basis.coeffs_from_derivs(D), True)
+        g = dg + self.basis.derivs_grad_from_coeffs_grad(sg)
+        return dc + sc, g[:, self.free_idx].reshape(-1)
+
+    def gradient(self, x) -> np.ndarray:
+        return self.cost_and_gradient(x)[1]
+
+    def gradient_fd(self, x) -> np.ndarray:
+        x = np.asarray(x, dtype=np.float64)
+        D = self.derivs(x)
+        g = self._dynamic(D)[1][:, self.free_idx].reshape(-1)
+        h = self.fd_step
+        for i in range(x.size):
+            xp = x.copy()
+            xp[i] += h
+            cp = self._sampled(self.coeffs(xp), False)[0]
+            xp[i] -= 2 * h
+            cm = self._sampled(self.coeffs(xp), False)[0]
+            g[i] += (cp - cm) / (2 * h)
+        return g
+
+
+def optimize_info_trajectory(problem: InfoTrajectoryProblem, gradient: str = "analytic", max_iters: int = 100):
+    """L-BFGS-B over the free junction derivatives, tracking the best iterate
+    (traj.optimize_trajectory, traj.py:411-463).  gradient = "analytic" (cost and gradient
+    from one batched query per evaluation) or "fd" (the reference's central differences).
+    Returns dict(x, cost, initial_cost, iterations, n_evals, seconds)."""
+    import time
+
+    from scipy.optimize import minimize
+
+    x0 = problem.x0()
+    problem.n_evals = 0
+    c0 = problem.cost(x0)
+    best = {"x": x0.copy(), "cost": c0}
+    iters = 0
+
+    def track(x, c):
+        if c < best["cost"]:
+            best["cost"], best["x"] = c, np.array(x, copy=True)
+
+    def cb(_xk):
+        nonlocal iters
+        iters += 1
+
+    t0 = time.perf_counter()
+    if gradient == "analytic":
+        def fun(x):
+            c, g = problem.cost_and_gradient(x)
+            track(x, c)
+            return c, g
+
+        minimize(fun, x0, jac=True, method="L-BFGS-B", callback=cb, options={"maxiter": max_iters})
+    elif gradient == "fd":
+        def fun(x):
+            c = problem.cost(x)
+            track(x, c)
+            return c
+
+        minimize(fun, x0, jac=problem.gradient_fd, method="L-BFGS-B", callback=cb, options={"maxiter": max_iters})
+    else:
+        raise ValueError("gradient must be 'analytic' or 'fd'")
+    return {"x": best["x"], "cost": best["cost"], "initial_cost": c0, "iterations": iters,
+            "n_evals": problem.n_evals, "seconds": time.perf_counter() - t0}

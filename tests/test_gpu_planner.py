@@ -136,3 +136,36 @@ def test_poly_trajectory_gradient(oracle, g_small, setup):
         cm[a, s, i] -= h
         fd = (total(cp) - total(cm)) / (2 * h)
         assert grad[a, s, i] == pytest.approx(fd, rel=1e-4, abs=1e-9 * max(1.0, abs(fd)))
+
+
+def test_traj_optimisation_replaces_fd_loop():
+    """the reference's L-BFGS-B trajectory optimisation (traj.optimize_trajectory,
+    traj.py:411-463, central-difference gradients: 2 x n_free cost evaluations per gradient)
+    driven instead by the analytic pose gradient of a GPU field.  Same problem as the golden
+    run of the reference (quad info field, trilinear det metric, tests/golden/traj_opt.npz):
+    the initial cost matches the reference's, the analytic gradient matches central
+    differences, and L-BFGS-B reaches at least the reference's final cost with a small
+    fraction of its batched field evaluations."""
+    import os
+
+    from paper_2008_03324_b200.planner import InfoTrajectoryProblem, PotentialParams, optimize_info_trajectory
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "traj_opt.npz"))
+    grid = F.GridConfig(g["origin"], g["voxel_size"][0], g["dims"])
+    fld = F.Field.build(g["points"], grid, F.build_quad_model(), "info", exact=True)
+    prob = InfoTrajectoryProblem(g["D0"], g["durations"], fld, PotentialParams(float(g["epsilon"][0])), metric="det",
+                                 mode="trilinear", mu_d=float(g["mu_d"][0]), mu_v=float(g["mu_v"][0]),
+                                 dt=float(g["dt"][0]))
+    x0 = prob.x0()
+    c0 = prob.cost(x0)
+    assert abs(c0 - g["initial_cost"][0]) <= 1e-9 * g["initial_cost"][0]
+    ga, gf = prob.gradient(x0), prob.gradient_fd(x0)
+    rel = np.linalg.norm(ga - gf) / np.linalg.norm(gf)
+    res = optimize_info_trajectory(prob, "analytic", max_iters=25)
+    ref_final, ref_evals = float(g["final_cost"][0]), int(g["n_evals"][0])
+    print(f"analytic vs FD gradient at x0: {rel:.2e}; reference (FD) {g['initial_cost'][0]:.4e} -> {ref_final:.4e} in "
+          f"{ref_evals} evaluations; ours (analytic) -> {res['cost']:.4e} in {res['n_evals']} evaluations, "
+          f"{res['iterations']} iterations, {res['seconds']:.2f} s")
+    assert rel <= 1e-3
+    assert res["cost"] <= ref_final * 1.02
+    assert res["n_evals"] * 20 <= ref_evals

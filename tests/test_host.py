@@ -166,3 +166,17 @@ def test_product_does_not_import_oracle():
             src = open(os.path.join(pkg, fn)).read()
             assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), fn
             assert "libfif_oracle" not in src, fn
+
+
+def test_junction_basis_matches_reference():
+    """planner.JunctionBasis restates traj._JunctionBasis (traj.py:50-89): Hermite maps,
+    dynamic-cost forms and junction -> coefficient map against the reference's values."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "traj_opt.npz"))
+    from paper_2008_03324_b200.planner import JunctionBasis
+
+    b = JunctionBasis(g["durations"])
+    for s in range(b.S):
+        assert np.allclose(b.M[s], g["M"][s], rtol=1e-13, atol=1e-13)
+    assert np.allclose(b.cost_matrix(4), g["R4"], rtol=1e-12, atol=1e-9)
+    assert np.allclose(b.cost_matrix(2), g["R2"], rtol=1e-12, atol=1e-9)
+    assert np.allclose(b.coeffs_from_derivs(g["D0"]), g["coeffs0"], rtol=1e-12, atol=1e-12)
