@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define FIF_ABI_VERSION 1
+#define FIF_ABI_VERSION 2
 
 /* return codes */
 #define FIF_OK 0
@@ -52,7 +52,8 @@ extern "C" {
 /* fif_build flags */
 #define FIF_BUILD_EXACT 1u  /* quad: reproduce _nb_build_quad's FP64 operation order bit for bit     */
 #define FIF_BUILD_SIMT 2u   /* GP info: FP32 SIMT (FFMA2) kernel instead of the tensor-pipe kernel   */
-#define FIF_BUILD_TF32 4u   /* GP info: TF32x3 tensor kernel instead of the default FP16-split one    */
+#define FIF_BUILD_TF32 4u   /* GP info: TF32x3 mma.sync kernel instead of the default tcgen05 one       */
+#define FIF_BUILD_H16 8u    /* GP info: FP16-split mma.sync kernel instead of the default tcgen05 one  */
 
 /* Axis-aligned voxel grid (field.py:45-98 GridConfig). */
 typedef struct fif_grid {
@@ -72,6 +73,8 @@ typedef struct fif_model {
   double sig2, ell;  /* SE kernel sigma^2 and length scale (visibility.py:71-86) */
   const double* zs;  /* device (N_s,3) sample directions                    */
   const double* kinv;/* device (N_s,N_s) inverse Gram matrix                */
+  const double* zs_host; /* optional host copy of zs: the sample directions become kernel
+                            parameters of the tcgen05 GP-info build (NULL: mma.sync kernel) */
 } fif_model;
 
 /* Pinhole camera (fim.py:28-68), pixels. */

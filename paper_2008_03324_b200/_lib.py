@@ -22,6 +22,7 @@ Q_TRACE, Q_FULL, Q_GRAD, Q_DET, Q_LMIN, Q_FIELD_F64 = 1, 2, 4, 8, 16, 32
 BUILD_EXACT = 1
 BUILD_SIMT = 2
 BUILD_TF32 = 4
+BUILD_H16 = 8
 METRIC_IDS = {"det": 0, "lmin": 1, "trace": 2}  # kernels.metric_id (kernels.py:602-608)
 
 EXPORTED = (
@@ -46,7 +47,7 @@ class Model(ctypes.Structure):
         ("k2", ctypes.c_double), ("k1", ctypes.c_double), ("k0", ctypes.c_double),
         ("k_s", ctypes.c_double), ("cos_alpha", ctypes.c_double),
         ("sig2", ctypes.c_double), ("ell", ctypes.c_double),
-        ("zs", ctypes.c_void_p), ("kinv", ctypes.c_void_p),
+        ("zs", ctypes.c_void_p), ("kinv", ctypes.c_void_p), ("zs_host", ctypes.c_void_p),
     ]
 
 
@@ -121,8 +122,8 @@ def load():
         L.fif_build_matched.restype = _int
         L.fif_build_matched.argtypes = [_int, ctypes.POINTER(Model), _p, _i64, _p, _i64, ctypes.POINTER(Match), _p, _d,
                                         ctypes.c_uint32, _p, _p, _p, _p]
-        if L.fif_abi_version() != 1:
-            raise FifCudaError(f"libfif_b200 ABI {L.fif_abi_version()} != 1")
+        if L.fif_abi_version() != 2:
+            raise FifCudaError(f"libfif_b200 ABI {L.fif_abi_version()} != 2")
         _lib = L
         return L
 

@@ -1421,6 +1421,8 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
   }
 }
 
+#include "fif_gp_t5.cuh"
+
 // ─────────────────────────── exports ───────────────────────────────────
 // Expand packed (rows, nv, 21) to the reference's (rows, nv*36).
 __global__ void k_expand36(const double* __restrict__ in, int64_t blocks, double* __restrict__ out) {
@@ -1580,6 +1582,42 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
       k_gp_trace<false><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns,
                                                            model->zs, gate, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
+  } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32 | FIF_BUILD_H16)) && model->zs_host != nullptr &&
+             ns <= 8 * T5_MAX_NG) {
+    // tcgen05 path: one tcgen05.mma (M=64, N=16 NG, K=16) per voxel per 16 landmarks, TMEM accumulators
+    const int ng = (ns + 7) / 8;
+    T5Z z{};
+    for (int sidx = 0; sidx < ns; ++sidx)
+      for (int c = 0; c < 3; ++c) z.z[c][sidx] = (float)(ax * model->zs_host[3 * sidx + c]);
+    const unsigned blocks5 = (unsigned)((rows + T5_VOX - 1) / T5_VOX);
+    int rc = FIF_OK;
+#define T5_CASE(NG)                                                                                         \
+  case NG: {                                                                                                \
+    constexpr size_t sm = t5_smem_bytes<NG>();                                                              \
+    static std::atomic<uint64_t> attr{0};                                                                   \
+    if (needs_setup(attr)) {                                                                                \
+      cudaFuncSetAttribute(k_gp_info_t5<NG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
+      cudaFuncSetAttribute(k_gp_info_t5<NG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
+      mark_setup(attr);                                                                                     \
+    }                                                                                                       \
+    if (has_mask)                                                                                           \
+      k_gp_info_t5<NG, true><<<blocks5, T5_THREADS, sm, st>>>(lm, n_pad, src, v_begin, v_end, ns, gate,      \
+                                                              (float)inv_s2, (float)bx, z, d_out64, d_out32); \
+    else                                                                                                    \
+      k_gp_info_t5<NG, false><<<blocks5, T5_THREADS, sm, st>>>(lm, n_pad, src, v_begin, v_end, ns, gate,     \
+                                                               (float)inv_s2, (float)bx, z, d_out64, d_out32); \
+    break;                                                                                                  \
+  }
+    switch (ng) {
+      T5_CASE(1) T5_CASE(2) T5_CASE(3) T5_CASE(4) T5_CASE(5) T5_CASE(6) T5_CASE(7) T5_CASE(8) T5_CASE(9) T5_CASE(10)
+      default: rc = FIF_ERR_UNSUPPORTED;
+    }
+#undef T5_CASE
+    if (rc != FIF_OK) {
+      set_error("fif_build: N_s=%d unsupported by k_gp_info_t5", ns);
+      return rc;
+    }
+    FIF_CHECK_LAUNCH("k_gp_info_t5");
   } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32))) {
     // tensor-pipe path, FP16 split (mma.sync m16n8k16): a warp covers 80 samples of one voxel
     const int wpv = (ns + 16 * GC_MT - 1) / (16 * GC_MT);

@@ -1,0 +1,407 @@
+// fif_gp_t5.cuh — GP info build on the 5th-generation tensor cores (tcgen05 + TMEM).
+// Included by fif_build.cu (uses its pair_prologue / entries21 / voxel_split / h16_split2).
+//
+// Replaces _nb_build_gp's info branch (kernels.py:471-524): per voxel,
+//   S[s][e] = sum_l vs(s, l) E(l, e)      (samples x landmarks) x (landmarks x 21 entries)
+// with vs the GP sigmoids and E the packed 6x6 pair information (kernels.py:363-424);
+// the reference's kinv @ S is applied at export / query time (field.py, fif_query.cu).
+//
+// One CTA (16 warps, 1 per SM) owns 3 voxels and streams 64-landmark tiles:
+//  * 12 producer warps, thread = (voxel, landmark, sample half).  Each computes the pair's
+//    bearing and weight once, then (half 0) the 21 entries and (both halves) its share of
+//    the N_s sigmoids, splits every value into FP16 hi + lo, and stores 8 consecutive
+//    entries / samples as one 16-byte vector into the MN-major UMMA operand tiles:
+//      A (M = 64 rows): row 16 gi + 8 part + e % 8 holds part (hi/lo) of entry e = 8 gi + e % 8
+//      B (N = 16 NG):   column s holds the hi sigmoid of sample s, column 8 NG + s the lo one
+//    The sample directions (ax * zs, 3 x N_s floats) are kernel parameters, so the exponent
+//    argument's FMAs take them straight from the constant bank.
+//  * 1 MMA thread (warp 15) issues, per voxel and 16-landmark k-step, ONE
+//    tcgen05.mma.kind::f16 M=64 N=16NG K=16 (FP32 accumulate in TMEM): the single product
+//    [E_hi; E_lo] x [vs_hi, vs_lo]^T carries hi*hi, hi*lo, lo*hi (and lo*lo) in separate
+//    accumulators, i.e. the 3-pass FP16 split of the mma.sync kernel in one instruction
+//    (measured: M64 N144 K16 = 72 cycles; 4.5 cycles per pair vs the 8.75-cycle MUFU
+//    floor of the sigmoids).  tcgen05.commit frees the stage's smem for the producers.
+//  * 3 epilogue warps (TMEM sub-partitions 0-2 hold the 48 used D rows) drain a voxel's
+//    accumulator every 512 landmarks (tcgen05.ld), add the four partial products in FP32
+//    (hi/lo rows meet through one shuffle) and accumulate into FP64 sums in shared memory;
+//    the voxels' flushes are staggered so the tensor pipe never waits on all three.
+// FP16 range: entries are scaled by one exact power of two per voxel (a pre-pass bounds
+// max |E| <= 2 w (1 + |p|^2) over the voxel's landmarks, so max|A'| < 2^14) and sigmoids
+// by 2^12 (folded into the reciprocal's argument); values under FP16's normal range keep
+// an absolute error <= 2^-37 max|E| per product, as in k_gp_info_h16.
+#pragma once
+// (included inside namespace fif)
+
+constexpr int T5_VOX = 3;           // voxels per CTA (TMEM: 3 x 16 NG <= 480 of 512 columns)
+constexpr int T5_TILE = 64;         // landmarks per pipeline stage
+constexpr int T5_KS = T5_TILE / 16; // MMAs per voxel per stage
+constexpr int T5_STAGES = 2;
+constexpr int T5_FLUSH = 8;         // FP32 accumulation span: 8 tiles = 512 landmarks
+constexpr int T5_PWARPS = 12;       // producer warps: 3 voxels x 2 sample halves x 2 landmark halves
+constexpr int T5_THREADS = 512;     // + 3 epilogue warps (12-14) + the MMA warp (15)
+constexpr int T5_MAX_NG = 10;       // N_s <= 80
+constexpr int T5_BLK_A = 64 * 16 * 2;  // bytes per k-step of A (M = 64)
+
+struct T5Z {
+  float z[3][8 * T5_MAX_NG];  // ax * zs[s][c] (FP32), 0 past N_s
+};
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // no-swizzle canonical layout, sm100 descriptor version 1; MN-major operands:
+  // LBO = stride between 8-deep K groups, SBO = stride between 8-wide M/N groups
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// kind::f16 instruction descriptor: D FP32, A/B FP16, both MN-major, M = 64, N = 16 NG
+template <int NG>
+__host__ __device__ constexpr uint32_t t5_idesc() {
+  return (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)((16 * NG) >> 3) << 17) | ((uint32_t)(64 >> 4) << 24);
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 16x32bx2 load of H consecutive columns per half-warp (second half at +H), H split into
+// power-of-two chunks (x32 / x16 / x8 / x4 / x2 / x1)
+template <int H, int C0 = 0>
+__device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
+  if constexpr (C0 < H) {
+    constexpr int REM = H - C0;
+    constexpr int N = REM >= 32 ? 32 : REM >= 16 ? 16 : REM >= 8 ? 8 : REM >= 4 ? 4 : REM >= 2 ? 2 : 1;
+    uint32_t* r = reinterpret_cast<uint32_t*>(v + C0);
+    if constexpr (N == 32)
+      asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                   "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], %33;"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                     "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                     "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                     "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                     "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                   : "r"(addr + C0), "n"(H));
+    else if constexpr (N == 16)
+      asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                   "[%16], %17;"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                     "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                     "=r"(r[15])
+                   : "r"(addr + C0), "n"(H));
+    else if constexpr (N == 8)
+      asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(addr + C0), "n"(H));
+    else if constexpr (N == 4)
+      asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x4.b32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                   : "r"(addr + C0), "n"(H));
+    else if constexpr (N == 2)
+      asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x2.b32 {%0,%1}, [%2], %3;"
+                   : "=r"(r[0]), "=r"(r[1])
+                   : "r"(addr + C0), "n"(H));
+    else
+      asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x1.b32 {%0}, [%1], %2;" : "=r"(r[0]) : "r"(addr + C0), "n"(H));
+    tmem_ld_half<H, C0 + N>(addr, v);
+  }
+}
+
+// hi/lo FP16 sigmoids 2^12 / (1 + 2^x), x = (ax z_s) . u + bx, for sample groups [G0, G1),
+// stored as 16-byte vectors (8 samples) at column groups g (hi) and NG + g (lo)
+#ifndef T5_XPAIR
+#define T5_XPAIR 0
+#endif
+#ifndef T5_SPLIT2
+#define T5_SPLIT2 1
+#endif
+// FP16 hi + lo of two FP32 values; T5_SPLIT2: residuals as one packed FP32x2 subtraction
+__device__ __forceinline__ void t5_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 b = __half22float2(h);
+#if T5_SPLIT2
+  float d0, d1;
+  unpack2(fsub2(pack2(x0, x1), pack2(b.x, b.y)), d0, d1);
+  const __half2 l = __floats2half2_rn(d0, d1);
+#else
+  const __half2 l = __floats2half2_rn(x0 - b.x, x1 - b.y);
+#endif
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+template <int NG, int G0, int G1>
+__device__ __forceinline__ void t5_sigmoids(const T5Z& Z, float ux, float uy, float uz, float bx, uint32_t bdst) {
+#pragma unroll
+  for (int g = G0; g < G1; ++g) {
+    uint32_t hv[4], lv[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int s0 = 8 * g + 2 * p;
+#if T5_XPAIR
+      const f32x2 x2 = ffma2(splat2(ux), pack2(Z.z[0][s0], Z.z[0][s0 + 1]),
+                             ffma2(splat2(uy), pack2(Z.z[1][s0], Z.z[1][s0 + 1]),
+                                   ffma2(splat2(uz), pack2(Z.z[2][s0], Z.z[2][s0 + 1]), splat2(bx))));
+      float x0, x1;
+      unpack2(x2, x0, x1);
+#else
+      const float x0 = fmaf(ux, Z.z[0][s0], fmaf(uy, Z.z[1][s0], fmaf(uz, Z.z[2][s0], bx)));
+      const float x1 = fmaf(ux, Z.z[0][s0 + 1], fmaf(uy, Z.z[1][s0 + 1], fmaf(uz, Z.z[2][s0 + 1], bx)));
+#endif
+      float y0, y1;  // 2^-12 (1 + 2^x) for both, one FFMA2
+      unpack2(ffma2(pack2(ex2_approx(x0), ex2_approx(x1)), splat2(0x1p-12f), splat2(0x1p-12f)), y0, y1);
+      t5_split2(rcp_approx(y0), rcp_approx(y1), hv[p], lv[p]);
+    }
+    sts128(bdst + g * 128, hv[0], hv[1], hv[2], hv[3]);
+    sts128(bdst + (NG + g) * 128, lv[0], lv[1], lv[2], lv[3]);
+  }
+}
+
+template <int NG, bool HAS_MASK>
+__global__ void __launch_bounds__(T5_THREADS, 1)
+k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v0, int64_t v1, int ns,
+             const PairGate gate, float inv_s2, float bx, const __grid_constant__ T5Z Z, double* __restrict__ out64,
+             float* __restrict__ out32) {
+  constexpr int NCOL = 16 * NG;                 // TMEM columns (and B rows) per voxel
+  constexpr int BLK_B = NCOL * 16 * 2;          // bytes per k-step of B
+  constexpr int STAGE_A = T5_KS * T5_BLK_A;     // bytes of one voxel's A tile
+  constexpr int STAGE_B = T5_KS * BLK_B;
+  constexpr int OFF_B = T5_STAGES * T5_VOX * STAGE_A;
+  constexpr int OFF_ACC = OFF_B + T5_STAGES * T5_VOX * STAGE_B;
+  constexpr int ACC_V = 8 * NG * 21;            // doubles per voxel
+  constexpr int OFF_BAR = OFF_ACC + T5_VOX * ACC_V * 8;
+  constexpr int G_SPLIT = NG / 2;               // sample groups of half 0 (which also computes the entries)
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double* acc = reinterpret_cast<double*>(smem + OFF_ACC);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* empty = full + T5_STAGES;
+  uint64_t* ffull = empty + T5_STAGES;
+  uint64_t* fempty = ffull + T5_VOX;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fempty + T5_VOX);
+  int* sbits = reinterpret_cast<int*>(tmem_slot + 1);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int64_t vbase = v0 + (int64_t)blockIdx.x * T5_VOX;
+  const int ntiles = (int)(n_pad / T5_TILE);
+
+  for (int i = t; i < T5_VOX * ACC_V; i += T5_THREADS) acc[i] = 0.0;
+  if (t < T5_VOX) sbits[t] = 0;
+  if (t == 0) {
+    for (int s = 0; s < T5_STAGES; ++s) {
+      mbar_init(&full[s], T5_PWARPS);
+      mbar_init(&empty[s], 1);
+    }
+    for (int j = 0; j < T5_VOX; ++j) {
+      mbar_init(&ffull[j], 1);
+      mbar_init(&fempty[j], 3);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();  // sbits zeroed before the pre-pass's atomicMax
+  if (warp == 15) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // producers: voxel centre, then the pre-pass bound on max |E| of their voxel
+  const int pj = warp >> 2, ph = (warp >> 1) & 1, pk = ((warp & 1) << 5) | lane;
+  const int64_t pv = vbase + pj;
+  const bool pvok = warp < T5_PWARPS && pv < v1;
+  float ch[3] = {0.f, 0.f, 0.f}, cl[3] = {0.f, 0.f, 0.f};
+  if (warp < T5_PWARPS) {
+    voxel_split(src, pvok ? pv : v0, ch, cl);
+    float mx = 0.f;
+    if (pvok) {
+      // n_pad is a multiple of 256: 4 independent landmarks per step (loads in flight together)
+      for (int64_t i0 = (ph << 6) | pk; i0 < n_pad; i0 += 512) {
+        float4 a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = i0 + 128 * u;
+          a[u] = i < n_pad ? lm[2 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
+          b[u] = i < n_pad ? lm[2 * i + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (HAS_MASK && b[u].w != 0.f && !gate_keep(gate, pv, i0 + 128 * u)) b[u].w = 0.f;
+          const PairF q = pair_prologue(a[u], b[u], ch, cl, inv_s2);
+          mx = fmaxf(mx, fmaf(a[u].w, 2.0f * q.w, 2.0f * q.w));  // >= 2 max|E| (|c2| <= |p|)
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) atomicMax(&sbits[pj], __float_as_int(mx));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto voxel_scale = [&](int j) {  // exact power of two with max|s E| < 2^14
+    const int bits = sbits[j];
+    if (bits <= 0) return 1.0f;
+    const int ex = ((bits >> 23) & 0xff) - 127;
+    return __int_as_float(min(254, max(1, 127 + 13 - ex)) << 23);
+  };
+  auto span_end = [&](int j, int tt) { return ((tt + j * T5_FLUSH / T5_VOX) % T5_FLUSH) == T5_FLUSH - 1 || tt == ntiles - 1; };
+  const uint32_t sbase = smem_u32(smem);
+
+  if (warp < T5_PWARPS) {
+    // ───────────── producers ─────────────
+    const float sj = voxel_scale(pj);
+    const uint32_t kofs_a = (pk >> 4) * T5_BLK_A + ((pk >> 3) & 1) * 1024 + (pk & 7) * 16;
+    const uint32_t kofs_b = (pk >> 4) * BLK_B + ((pk >> 3) & 1) * (256 * NG) + (pk & 7) * 16;
+    float4 na = lm[2 * pk], nb = lm[2 * pk + 1];
+    for (int tt = 0; tt < ntiles; ++tt) {
+      const int s = tt % T5_STAGES;
+      const float4 a = na;
+      float4 b = nb;
+      if (tt + 1 < ntiles) {
+        const int64_t ni = (int64_t)(tt + 1) * T5_TILE + pk;
+        na = lm[2 * ni];
+        nb = lm[2 * ni + 1];
+      }
+      if (!pvok) b.w = 0.f;
+      if (HAS_MASK && b.w != 0.f && !gate_keep(gate, pv, (int64_t)tt * T5_TILE + pk)) b.w = 0.f;
+      const PairF q = pair_prologue(a, b, ch, cl, inv_s2);
+      if (tt >= T5_STAGES) mbar_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
+      const uint32_t adst = sbase + (s * T5_VOX + pj) * STAGE_A + kofs_a;
+      const uint32_t bdst = sbase + OFF_B + (s * T5_VOX + pj) * STAGE_B + kofs_b;
+      if (ph == 0) {
+        float e[24];
+        entries21(q, a, e);
+        e[21] = e[22] = e[23] = 0.f;
+#pragma unroll
+        for (int gi = 0; gi < 3; ++gi) {
+          uint32_t hv[4], lv[4];
+#pragma unroll
+          for (int p = 0; p < 4; ++p) t5_split2(e[8 * gi + 2 * p] * sj, e[8 * gi + 2 * p + 1] * sj, hv[p], lv[p]);
+          sts128(adst + (2 * gi) * 128, hv[0], hv[1], hv[2], hv[3]);
+          sts128(adst + (2 * gi + 1) * 128, lv[0], lv[1], lv[2], lv[3]);
+        }
+        t5_sigmoids<NG, 0, G_SPLIT>(Z, q.ux, q.uy, q.uz, bx, bdst);
+      } else {
+        t5_sigmoids<NG, G_SPLIT, NG>(Z, q.ux, q.uy, q.uz, bx, bdst);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else if (warp == 15) {
+    // ───────────── MMA issue (one thread) ─────────────
+    if (lane == 0) {
+      constexpr uint32_t idesc = t5_idesc<NG>();
+      bool started[T5_VOX], pending[T5_VOX];
+      uint32_t fph[T5_VOX];
+#pragma unroll
+      for (int j = 0; j < T5_VOX; ++j) {
+        started[j] = pending[j] = false;
+        fph[j] = 0;
+      }
+      for (int tt = 0; tt < ntiles; ++tt) {
+        const int s = tt % T5_STAGES;
+        mbar_wait(&full[s], (tt / T5_STAGES) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int j = 0; j < T5_VOX; ++j) {
+          if (pending[j]) {  // the epilogue has to drain this accumulator first
+            mbar_wait(&fempty[j], fph[j]);
+            fph[j] ^= 1;
+            pending[j] = false;
+            started[j] = false;
+            tc_fence_after();
+          }
+          const uint32_t a0 = sbase + (s * T5_VOX + j) * STAGE_A;
+          const uint32_t b0 = sbase + OFF_B + (s * T5_VOX + j) * STAGE_B;
+          const uint32_t d = tmem + j * NCOL;
+#pragma unroll
+          for (int ks = 0; ks < T5_KS; ++ks) {
+            const uint64_t da = umma_desc(a0 + ks * T5_BLK_A, 1024, 128);
+            const uint64_t db = umma_desc(b0 + ks * BLK_B, 256 * NG, 128);
+            const uint32_t accf = (started[j] || ks > 0) ? 1u : 0u;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                         "l"(da), "l"(db), "r"(idesc), "r"(accf));
+          }
+          started[j] = true;
+          if (span_end(j, tt)) {
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&ffull[j]))
+                         : "memory");
+            pending[j] = true;
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[s]))
+                     : "memory");
+      }
+    }
+    __syncwarp();
+  } else {
+    // ───────────── epilogue: TMEM -> FP64 sums (warps 12-14 = sub-partitions 0-2) ─────────────
+    // 16x32bx2 loads: lane L < 16 reads D row 16 sp + L, columns [0, H) of a sample block,
+    // lane 16 + L the same row's columns [H, 2H) (H = 4 NG): the whole snapshot (hi and lo
+    // sample columns) lands in registers with one wait, the accumulator is released, and
+    // the FP64 accumulation runs while the tensor pipe refills it.
+    constexpr int H = 4 * NG;
+    const int sp = warp & 3;
+    const int L = lane & 15, part = L >> 3, e = 8 * sp + (L & 7), q = lane >> 4;
+    const bool row_ok = e < 21;
+    uint32_t fph[T5_VOX] = {0, 0, 0};
+    double unscale[T5_VOX];
+#pragma unroll
+    for (int j = 0; j < T5_VOX; ++j) unscale[j] = 0x1p-12 / (double)voxel_scale(j);
+    for (int tt = 0; tt < ntiles; ++tt) {
+#pragma unroll
+      for (int j = 0; j < T5_VOX; ++j) {
+        if (!span_end(j, tt)) continue;
+        mbar_wait(&ffull[j], fph[j]);
+        fph[j] ^= 1;
+        tc_fence_after();
+        const uint32_t row = tmem + ((uint32_t)(32 * sp) << 16) + j * NCOL;
+        float hi[H], lo[H];
+        tmem_ld_half<H>(row, hi);
+        tmem_ld_half<H>(row + 8 * NG, lo);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fempty[j]);
+        double* aj = acc + j * ACC_V;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+          float v = hi[i] + lo[i];
+          v += __shfl_xor_sync(0xffffffffu, v, 8);  // + the other part's row (entry hi / lo)
+          const int sm = q * H + i;
+          if ((i & 1) == part && row_ok && sm < ns) aj[sm * 21 + e] += (double)v * unscale[j];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // write the voxels' FP64 sums (and the FP32 query copy)
+  const int per = ns * 21;
+  for (int i = t; i < T5_VOX * per; i += T5_THREADS) {
+    const int j = i / per, r = i - j * per;
+    const int64_t v = vbase + j;
+    if (v >= v1) continue;
+    const double x = acc[j * ACC_V + r];
+    out64[(v - v0) * per + r] = x;
+    if (out32) out32[(v - v0) * per + r] = (float)x;
+  }
+  if (warp == 15) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int NG>
+constexpr size_t t5_smem_bytes() {
+  return (size_t)T5_STAGES * T5_VOX * T5_KS * (T5_BLK_A + 16 * NG * 16 * 2) + (size_t)T5_VOX * 8 * NG * 21 * 8 +
+         (2 * T5_STAGES + 2 * T5_VOX) * 8 + 4 + 4 * T5_VOX;
+}
+

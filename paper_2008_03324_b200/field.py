@@ -330,10 +330,12 @@ class _DeviceModel:
             m.kind, m.n_v = _lib.MODEL_GP, model.n_v
             m.k_s, m.cos_alpha = model.k_s, float(np.cos(model.alpha))
             m.sig2, m.ell = model.params.sigma2, model.params.length_scale
-            zs = torch.from_numpy(np.ascontiguousarray(model.samples)).to(device)
+            zs_h = np.ascontiguousarray(model.samples, dtype=np.float64)
+            zs = torch.from_numpy(zs_h).to(device)
             kinv = torch.from_numpy(np.ascontiguousarray(model.kinv)).to(device)
-            self._keep += [zs, kinv]
+            self._keep += [zs, kinv, zs_h]
             m.zs, m.kinv = zs.data_ptr(), kinv.data_ptr()
+            m.zs_host = zs_h.ctypes.data  # sample directions as kernel parameters (tcgen05 build)
         self.c = m
 
 
@@ -341,10 +343,11 @@ class _DeviceModel:
 # pairs at a time (one byte each), bounding device memory for large maps
 _MASK_CHUNK_BYTES = 1 << 30
 
-# GP info kernel: "h16" (default; mma.sync FP16 split, k16 per MMA), "tf32" (mma.sync
-# TF32x3) or "simt" (FP32 FFMA2); the alternatives are kept as cross-checks.
-GP_INFO_KERNEL = "h16"
-_GP_INFO_FLAGS = {"h16": 0, "tf32": _lib.BUILD_TF32, "simt": _lib.BUILD_SIMT}
+# GP info kernel: "t5" (default; tcgen05.mma FP16 split with TMEM accumulators, N_s <= 80,
+# other N_s run "h16"), "h16" (mma.sync FP16 split, k16 per MMA), "tf32" (mma.sync TF32x3)
+# or "simt" (FP32 FFMA2); the alternatives are kept as cross-checks.
+GP_INFO_KERNEL = "t5"
+_GP_INFO_FLAGS = {"t5": 0, "h16": _lib.BUILD_H16, "tf32": _lib.BUILD_TF32, "simt": _lib.BUILD_SIMT}
 
 
 def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, device: torch.device, grid=None,

@@ -40,9 +40,9 @@ def test_centers_bit_exact(oracle, small_grid, order):
     assert np.array_equal(out.cpu().numpy(), ref)
 
 
-@pytest.fixture(params=["h16", "tf32", "simt"])
+@pytest.fixture(params=["t5", "h16", "tf32", "simt"])
 def gp_info_kernel(request, monkeypatch):
-    """Every GP-info kernel (mma.sync FP16-split default, TF32x3, FP32 FFMA2 SIMT) must meet parity."""
+    """Every GP-info kernel (tcgen05 default, mma.sync FP16-split, TF32x3, FP32 FFMA2 SIMT) must meet parity."""
     monkeypatch.setattr(FD, "GP_INFO_KERNEL", request.param)
     return request.param
 

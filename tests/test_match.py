@@ -169,7 +169,7 @@ def test_fused_gates_equal_explicit_mask_build(g_match, g_models):
     mask = mt.device_mask(cen, pts, g_match["view_dirs"])
     for mname in ("quad", "gp30"):
         for kind in (True, False):
-            for kern in (("h16", "tf32", "simt") if mname == "gp30" and not kind else ("h16",)):
+            for kern in (("t5", "h16", "tf32", "simt") if mname == "gp30" and not kind else ("t5",)):
                 old = FD.GP_INFO_KERNEL
                 FD.GP_INFO_KERNEL = kern
                 try:
