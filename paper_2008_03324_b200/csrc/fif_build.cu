@@ -1583,7 +1583,8 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
                                                            model->zs, gate, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
   } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32 | FIF_BUILD_H16)) && model->zs_host != nullptr &&
-             ns <= 8 * T5_MAX_NG) {
+             ns <= 8 * T5_MAX_NG && bx + fabs(ax) <= 60.0) {
+    // (x = (ax zs) . u + bx <= bx + |ax| <= 60 keeps the paired sigmoid reciprocal finite)
     // tcgen05 path: one tcgen05.mma (M=64, N=16 NG, K=16) per voxel per 16 landmarks, TMEM accumulators
     const int ng = (ns + 7) / 8;
     T5Z z{};
@@ -1594,17 +1595,19 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
 #define T5_CASE(NG)                                                                                         \
   case NG: {                                                                                                \
     constexpr size_t sm = t5_smem_bytes<NG>();                                                              \
+    const size_t gb = (size_t)T5_VOX * (n_pad / 8);                                                         \
+    const int use_gb = has_mask && sm + gb <= T5_SMEM_MAX;                                                  \
     static std::atomic<uint64_t> attr{0};                                                                   \
     if (needs_setup(attr)) {                                                                                \
-      cudaFuncSetAttribute(k_gp_info_t5<NG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
+      cudaFuncSetAttribute(k_gp_info_t5<NG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, T5_SMEM_MAX); \
       cudaFuncSetAttribute(k_gp_info_t5<NG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
       mark_setup(attr);                                                                                     \
     }                                                                                                       \
     if (has_mask)                                                                                           \
-      k_gp_info_t5<NG, true><<<blocks5, T5_THREADS, sm, st>>>(lm, n_pad, src, v_begin, v_end, ns, gate,      \
-                                                              (float)inv_s2, (float)bx, z, d_out64, d_out32); \
+      k_gp_info_t5<NG, true><<<blocks5, T5_THREADS, sm + (use_gb ? gb : 0), st>>>(                            \
+          lm, n_pad, src, v_begin, v_end, ns, gate, use_gb, (float)inv_s2, (float)bx, z, d_out64, d_out32);  \
     else                                                                                                    \
-      k_gp_info_t5<NG, false><<<blocks5, T5_THREADS, sm, st>>>(lm, n_pad, src, v_begin, v_end, ns, gate,     \
+      k_gp_info_t5<NG, false><<<blocks5, T5_THREADS, sm, st>>>(lm, n_pad, src, v_begin, v_end, ns, gate, 0, \
                                                                (float)inv_s2, (float)bx, z, d_out64, d_out32); \
     break;                                                                                                  \
   }

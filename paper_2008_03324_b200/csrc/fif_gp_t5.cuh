@@ -6,7 +6,7 @@
 // with vs the GP sigmoids and E the packed 6x6 pair information (kernels.py:363-424);
 // the reference's kinv @ S is applied at export / query time (field.py, fif_query.cu).
 //
-// One CTA (16 warps, 1 per SM) owns 3 voxels and streams 64-landmark tiles:
+// One CTA (1 per SM) owns 3 voxels and streams 64-landmark tiles:
 //  * 12 producer warps, thread = (voxel, landmark, sample half).  Each computes the pair's
 //    bearing and weight once, then (half 0) the 21 entries and (both halves) its share of
 //    the N_s sigmoids, splits every value into FP16 hi + lo, and stores 8 consecutive
@@ -37,12 +37,22 @@ constexpr int T5_TILE = 64;         // landmarks per pipeline stage
 constexpr int T5_KS = T5_TILE / 16; // MMAs per voxel per stage
 constexpr int T5_STAGES = 2;
 constexpr int T5_FLUSH = 8;         // FP32 accumulation span: 8 tiles = 512 landmarks
-constexpr int T5_PWARPS = 12;       // producer warps: 3 voxels x 2 sample halves x 2 landmark halves
-constexpr int T5_THREADS = 512;     // + 3 epilogue warps (12-14) + the MMA warp (15)
+#ifndef T5_PARTS
+#define T5_PARTS 2                  // sample parts per (voxel, landmark) pair: one thread each
+#endif
+constexpr int T5_PWARPS = T5_VOX * T5_PARTS * 2;  // producer warps: voxels x parts x 2 landmark halves
+// warp roles after the producers: 3 epilogue warps whose warp % 4 = 0, 1, 2 (the TMEM
+// sub-partitions holding D rows 0-47) and one MMA warp
+constexpr int T5_EPI0 = (T5_PWARPS % 4 == 0) ? T5_PWARPS : ((T5_PWARPS + 1 + 3) / 4) * 4;
+constexpr int T5_MMAW = (T5_PWARPS % 4 == 0) ? T5_PWARPS + 3 : T5_PWARPS;
+constexpr int T5_THREADS = (T5_EPI0 + 3 + (T5_MMAW > T5_EPI0 ? 1 : 0)) * 32;
+static_assert(T5_MMAW < T5_EPI0 || T5_MMAW == T5_EPI0 + 3, "warp roles");
 constexpr int T5_MAX_NG = 10;       // N_s <= 80
 constexpr int T5_BLK_A = 64 * 16 * 2;  // bytes per k-step of A (M = 64)
 
-struct T5Z {
+constexpr int T5_BAR_BYTES = 128;  // mbarriers, TMEM slot, scale bits (rounded up)
+constexpr int T5_SMEM_MAX = 227 * 1024;  // opt-in shared memory per CTA on sm_100
+struct __align__(16) T5Z {
   float z[3][8 * T5_MAX_NG];  // ax * zs[s][c] (FP32), 0 past N_s
 };
 
@@ -115,8 +125,23 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 
 // hi/lo FP16 sigmoids 2^12 / (1 + 2^x), x = (ax z_s) . u + bx, for sample groups [G0, G1),
 // stored as 16-byte vectors (8 samples) at column groups g (hi) and NG + g (lo)
+#ifndef T5_NAMED
+#define T5_NAMED 1
+#endif
+#ifndef T5_EPI_SLEEP
+#define T5_EPI_SLEEP 256
+#endif
+#ifndef T5_MMA_SLEEP
+#define T5_MMA_SLEEP 20
+#endif
+#ifndef T5_PREPASS_W
+#define T5_PREPASS_W 0
+#endif
+#ifndef T5_SLEEPWAIT
+#define T5_SLEEPWAIT 1
+#endif
 #ifndef T5_XPAIR
-#define T5_XPAIR 0
+#define T5_XPAIR 1
 #endif
 #ifndef T5_SPLIT2
 #define T5_SPLIT2 1
@@ -135,6 +160,39 @@ __device__ __forceinline__ void t5_split2(float x0, float x1, uint32_t& hi, uint
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
+// polling with a sleep between probes (the epilogue waits ~7 000 cycles between flushes)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, unsigned ns) {
+#if T5_SLEEPWAIT
+  (void)ns;
+  mbar_wait_sleep(bar, parity);
+#else
+  while (!mbar_try(bar, parity)) __nanosleep(ns);
+#endif
+}
+// named barriers: the producers arrive (no wait) and the MMA warp blocks in hardware
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 template <int NG, int G0, int G1>
 __device__ __forceinline__ void t5_sigmoids(const T5Z& Z, float ux, float uy, float uz, float bx, uint32_t bdst) {
 #pragma unroll
@@ -155,7 +213,12 @@ __device__ __forceinline__ void t5_sigmoids(const T5Z& Z, float ux, float uy, fl
 #endif
       float y0, y1;  // 2^-12 (1 + 2^x) for both, one FFMA2
       unpack2(ffma2(pack2(ex2_approx(x0), ex2_approx(x1)), splat2(0x1p-12f), splat2(0x1p-12f)), y0, y1);
-      t5_split2(rcp_approx(y0), rcp_approx(y1), hv[p], lv[p]);
+      // one reciprocal for both sigmoids: r = 1 / (y0 y1), sg0 = y1 r, sg1 = y0 r (the host
+      // launches this kernel only when x <= 60, so y0 y1 <= 2^98 stays finite; y >= 2^-12)
+      const float r = rcp_approx(y0 * y1);
+      float sg0, sg1;
+      unpack2(fmul2(pack2(y1, y0), splat2(r)), sg0, sg1);
+      t5_split2(sg0, sg1, hv[p], lv[p]);
     }
     sts128(bdst + g * 128, hv[0], hv[1], hv[2], hv[3]);
     sts128(bdst + (NG + g) * 128, lv[0], lv[1], lv[2], lv[3]);
@@ -165,8 +228,8 @@ __device__ __forceinline__ void t5_sigmoids(const T5Z& Z, float ux, float uy, fl
 template <int NG, bool HAS_MASK>
 __global__ void __launch_bounds__(T5_THREADS, 1)
 k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v0, int64_t v1, int ns,
-             const PairGate gate, float inv_s2, float bx, const __grid_constant__ T5Z Z, double* __restrict__ out64,
-             float* __restrict__ out32) {
+             const PairGate gate, int use_gbits, float inv_s2, float bx, const __grid_constant__ T5Z Z,
+             double* __restrict__ out64, float* __restrict__ out32) {
   constexpr int NCOL = 16 * NG;                 // TMEM columns (and B rows) per voxel
   constexpr int BLK_B = NCOL * 16 * 2;          // bytes per k-step of B
   constexpr int STAGE_A = T5_KS * T5_BLK_A;     // bytes of one voxel's A tile
@@ -175,15 +238,20 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   constexpr int OFF_ACC = OFF_B + T5_STAGES * T5_VOX * STAGE_B;
   constexpr int ACC_V = 8 * NG * 21;            // doubles per voxel
   constexpr int OFF_BAR = OFF_ACC + T5_VOX * ACC_V * 8;
-  constexpr int G_SPLIT = NG / 2;               // sample groups of half 0 (which also computes the entries)
+  // sample-group boundaries of the parts; part 0 also computes the 21 entries (~ 13 samples of work)
+  constexpr int G1 = T5_PARTS == 1 ? NG : T5_PARTS == 2 ? NG / 2 : (2 * NG + 4) / 9;
+  constexpr int G2 = T5_PARTS == 2 ? NG : G1 + (NG - G1) * 3 / 7;
   extern __shared__ __align__(1024) unsigned char smem[];
   double* acc = reinterpret_cast<double*>(smem + OFF_ACC);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* empty = full + T5_STAGES;
-  uint64_t* ffull = empty + T5_STAGES;
-  uint64_t* fempty = ffull + T5_VOX;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fempty + T5_VOX);
+  uint64_t* ffull = empty + T5_STAGES;  // [2] accumulator buffer b holds a finished span
+  uint64_t* fempty = ffull + 2;         // [2] the epilogue has drained buffer b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fempty + 2);
   int* sbits = reinterpret_cast<int*>(tmem_slot + 1);
+  // masked builds: the pre-pass evaluates each pair's matchability gate once and keeps the
+  // answers as bits ([voxel][n_pad / 32] words) for the main loop (when they fit)
+  uint32_t* gbits = reinterpret_cast<uint32_t*>(smem + OFF_BAR + T5_BAR_BYTES);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int64_t vbase = v0 + (int64_t)blockIdx.x * T5_VOX;
   const int ntiles = (int)(n_pad / T5_TILE);
@@ -195,19 +263,19 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       mbar_init(&full[s], T5_PWARPS);
       mbar_init(&empty[s], 1);
     }
-    for (int j = 0; j < T5_VOX; ++j) {
-      mbar_init(&ffull[j], 1);
-      mbar_init(&fempty[j], 3);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ffull[b], 1);
+      mbar_init(&fempty[b], 3);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();  // sbits zeroed before the pre-pass's atomicMax
-  if (warp == 15) {
+  if (warp == T5_MMAW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   // producers: voxel centre, then the pre-pass bound on max |E| of their voxel
-  const int pj = warp >> 2, ph = (warp >> 1) & 1, pk = ((warp & 1) << 5) | lane;
+  const int pj = warp / (2 * T5_PARTS), ph = (warp >> 1) % T5_PARTS, pk = ((warp & 1) << 5) | lane;
   const int64_t pv = vbase + pj;
   const bool pvok = warp < T5_PWARPS && pv < v1;
   float ch[3] = {0.f, 0.f, 0.f}, cl[3] = {0.f, 0.f, 0.f};
@@ -215,22 +283,44 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     voxel_split(src, pvok ? pv : v0, ch, cl);
     float mx = 0.f;
     if (pvok) {
-      // n_pad is a multiple of 256: 4 independent landmarks per step (loads in flight together)
-      for (int64_t i0 = (ph << 6) | pk; i0 < n_pad; i0 += 512) {
+      // max over landmarks of (1 + |p|^2) / n^2 as a fraction bn / bd (no division per landmark);
+      // n^2 from the same hi/lo difference as pair_prologue, the same skip rule
+      float bn = 0.f, bd = 1.f;
+      constexpr int PT = 64 * T5_PARTS;  // pre-pass threads per voxel
+      for (int64_t i0 = ph * 64 + pk; i0 < n_pad; i0 += 4 * PT) {
         float4 a[4], b[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int64_t i = i0 + 128 * u;
+          const int64_t i = i0 + PT * u;
           a[u] = i < n_pad ? lm[2 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
           b[u] = i < n_pad ? lm[2 * i + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (HAS_MASK && b[u].w != 0.f && !gate_keep(gate, pv, i0 + 128 * u)) b[u].w = 0.f;
+          if (HAS_MASK && b[u].w != 0.f && !gate_keep(gate, pv, i0 + PT * u)) b[u].w = 0.f;
+          if (HAS_MASK && use_gbits) {  // warp = 32 consecutive landmarks: one word
+            const unsigned wbits = __ballot_sync(0xffffffffu, b[u].w != 0.f);
+            if (lane == 0) gbits[pj * (n_pad >> 5) + ((i0 + PT * u) >> 5)] = wbits;
+          }
+#if T5_PREPASS_W
           const PairF q = pair_prologue(a[u], b[u], ch, cl, inv_s2);
           mx = fmaxf(mx, fmaf(a[u].w, 2.0f * q.w, 2.0f * q.w));  // >= 2 max|E| (|c2| <= |p|)
+          continue;
+#endif
+          const float dx = __fadd_rn(__fsub_rn(a[u].x, ch[0]), __fsub_rn(b[u].x, cl[0]));
+          const float dy = __fadd_rn(__fsub_rn(a[u].y, ch[1]), __fsub_rn(b[u].y, cl[1]));
+          const float dz = __fadd_rn(__fsub_rn(a[u].z, ch[2]), __fsub_rn(b[u].z, cl[2]));
+          const float n2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+          const float num = 1.0f + a[u].w;
+          if (n2 > 1e-30f && b[u].w != 0.f && num * bd > bn * n2) {
+            bn = num;
+            bd = n2;
+          }
         }
       }
+      // 2 w (1 + |p|^2) with w = inv_s2 / n^2: >= 2 max|E| (|c2| <= |p|); the factor 2 also
+      // covers the rounding of w = inv_s2 rsqrt(n^2)^2 in the build
+      if (!T5_PREPASS_W) mx = bn > 0.f ? 2.0f * inv_s2 * __fdiv_rn(bn, bd) : 0.f;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -246,12 +336,17 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     const int ex = ((bits >> 23) & 0xff) - 127;
     return __int_as_float(min(254, max(1, 127 + 13 - ex)) << 23);
   };
-  auto span_end = [&](int j, int tt) { return ((tt + j * T5_FLUSH / T5_VOX) % T5_FLUSH) == T5_FLUSH - 1 || tt == ntiles - 1; };
+  // FP32 accumulation spans: tiles [8k, 8k + 8) for every voxel (so a voxel's rounding does
+  // not depend on which CTA, slab or centre list it lands in).  Span k accumulates in TMEM
+  // buffer k & 1: an M = 64 MMA writes D rows to lanes 0-15 of each sub-partition, or to
+  // lanes 16-31 with lane offset 16 in the D address (measured), so both buffers share the
+  // voxel's 16 NG columns and the epilogue drains one while the tensor pipe fills the other.
+  auto span_end = [&](int tt) { return (tt % T5_FLUSH) == T5_FLUSH - 1 || tt == ntiles - 1; };
   const uint32_t sbase = smem_u32(smem);
 
   if (warp < T5_PWARPS) {
     // ───────────── producers ─────────────
-    const float sj = voxel_scale(pj);
+    const float inv_s2_s = inv_s2 * voxel_scale(pj);  // exact: a power of two
     const uint32_t kofs_a = (pk >> 4) * T5_BLK_A + ((pk >> 3) & 1) * 1024 + (pk & 7) * 16;
     const uint32_t kofs_b = (pk >> 4) * BLK_B + ((pk >> 3) & 1) * (256 * NG) + (pk & 7) * 16;
     float4 na = lm[2 * pk], nb = lm[2 * pk + 1];
@@ -265,8 +360,13 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         nb = lm[2 * ni + 1];
       }
       if (!pvok) b.w = 0.f;
-      if (HAS_MASK && b.w != 0.f && !gate_keep(gate, pv, (int64_t)tt * T5_TILE + pk)) b.w = 0.f;
-      const PairF q = pair_prologue(a, b, ch, cl, inv_s2);
+      if (HAS_MASK && b.w != 0.f) {
+        const int64_t i = (int64_t)tt * T5_TILE + pk;
+        const bool keep = use_gbits ? ((gbits[pj * (n_pad >> 5) + (i >> 5)] >> (i & 31)) & 1u) != 0
+                                    : gate_keep(gate, pv, i);
+        if (!keep) b.w = 0.f;
+      }
+      const PairF q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
       if (tt >= T5_STAGES) mbar_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
       const uint32_t adst = sbase + (s * T5_VOX + pj) * STAGE_A + kofs_a;
       const uint32_t bdst = sbase + OFF_B + (s * T5_VOX + pj) * STAGE_B + kofs_b;
@@ -278,69 +378,71 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         for (int gi = 0; gi < 3; ++gi) {
           uint32_t hv[4], lv[4];
 #pragma unroll
-          for (int p = 0; p < 4; ++p) t5_split2(e[8 * gi + 2 * p] * sj, e[8 * gi + 2 * p + 1] * sj, hv[p], lv[p]);
+          for (int p = 0; p < 4; ++p) t5_split2(e[8 * gi + 2 * p], e[8 * gi + 2 * p + 1], hv[p], lv[p]);
           sts128(adst + (2 * gi) * 128, hv[0], hv[1], hv[2], hv[3]);
           sts128(adst + (2 * gi + 1) * 128, lv[0], lv[1], lv[2], lv[3]);
         }
-        t5_sigmoids<NG, 0, G_SPLIT>(Z, q.ux, q.uy, q.uz, bx, bdst);
+        t5_sigmoids<NG, 0, G1>(Z, q.ux, q.uy, q.uz, bx, bdst);
+      } else if (T5_PARTS == 2 || ph == 1) {
+        t5_sigmoids<NG, G1, G2>(Z, q.ux, q.uy, q.uz, bx, bdst);
       } else {
-        t5_sigmoids<NG, G_SPLIT, NG>(Z, q.ux, q.uy, q.uz, bx, bdst);
+        t5_sigmoids<NG, G2, NG>(Z, q.ux, q.uy, q.uz, bx, bdst);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
+#if T5_NAMED
+      named_arrive(1 + s, (T5_PWARPS + 1) * 32);  // stage s written (the MMA warp syncs on it)
+#else
       if (lane == 0) mbar_arrive(&full[s]);
+#endif
     }
-  } else if (warp == 15) {
+  } else if (warp == T5_MMAW) {
     // ───────────── MMA issue (one thread) ─────────────
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc = t5_idesc<NG>();
-      bool started[T5_VOX], pending[T5_VOX];
-      uint32_t fph[T5_VOX];
-#pragma unroll
-      for (int j = 0; j < T5_VOX; ++j) {
-        started[j] = pending[j] = false;
-        fph[j] = 0;
-      }
       for (int tt = 0; tt < ntiles; ++tt) {
         const int s = tt % T5_STAGES;
-        mbar_wait(&full[s], (tt / T5_STAGES) & 1);
+        const int k = tt / T5_FLUSH, b = k & 1;
+        __syncwarp();
+#if T5_NAMED
+        named_sync(1 + s, (T5_PWARPS + 1) * 32);  // all 32 lanes (bar.sync is warp-aligned)
+#else
+        mbar_wait_backoff(&full[s], (tt / T5_STAGES) & 1, T5_MMA_SLEEP);
+#endif
         tc_fence_after();
-#pragma unroll
-        for (int j = 0; j < T5_VOX; ++j) {
-          if (pending[j]) {  // the epilogue has to drain this accumulator first
-            mbar_wait(&fempty[j], fph[j]);
-            fph[j] ^= 1;
-            pending[j] = false;
-            started[j] = false;
+        if (lane == 0) {  // one thread issues
+          const bool first = tt % T5_FLUSH == 0;
+          if (first && k >= 2) {  // buffer b last held span k - 2: drained long ago, normally
+            mbar_wait_backoff(&fempty[b], ((k >> 1) - 1) & 1, T5_MMA_SLEEP);
             tc_fence_after();
           }
-          const uint32_t a0 = sbase + (s * T5_VOX + j) * STAGE_A;
-          const uint32_t b0 = sbase + OFF_B + (s * T5_VOX + j) * STAGE_B;
-          const uint32_t d = tmem + j * NCOL;
 #pragma unroll
-          for (int ks = 0; ks < T5_KS; ++ks) {
-            const uint64_t da = umma_desc(a0 + ks * T5_BLK_A, 1024, 128);
-            const uint64_t db = umma_desc(b0 + ks * BLK_B, 256 * NG, 128);
-            const uint32_t accf = (started[j] || ks > 0) ? 1u : 0u;
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-                         "l"(da), "l"(db), "r"(idesc), "r"(accf));
+          for (int j = 0; j < T5_VOX; ++j) {
+            const uint32_t a0 = sbase + (s * T5_VOX + j) * STAGE_A;
+            const uint32_t b0 = sbase + OFF_B + (s * T5_VOX + j) * STAGE_B;
+            const uint32_t d = tmem + ((uint32_t)(16 * b) << 16) + j * NCOL;
+#pragma unroll
+            for (int ks = 0; ks < T5_KS; ++ks) {
+              const uint64_t da = umma_desc(a0 + ks * T5_BLK_A, 1024, 128);
+              const uint64_t db = umma_desc(b0 + ks * BLK_B, 256 * NG, 128);
+              const uint32_t accf = (!first || ks > 0) ? 1u : 0u;
+              asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                           "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                           "l"(da), "l"(db), "r"(idesc), "r"(accf));
+            }
           }
-          started[j] = true;
-          if (span_end(j, tt)) {
+          if (span_end(tt))
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(&ffull[j]))
+                             smem_u32(&ffull[b]))
                          : "memory");
-            pending[j] = true;
-          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&empty[s]))
+                       : "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_u32(&empty[s]))
-                     : "memory");
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp >= T5_EPI0 && warp < T5_EPI0 + 3) {
     // ───────────── epilogue: TMEM -> FP64 sums (warps 12-14 = sub-partitions 0-2) ─────────────
     // 16x32bx2 loads: lane L < 16 reads D row 16 sp + L, columns [0, H) of a sample block,
     // lane 16 + L the same row's columns [H, 2H) (H = 4 NG): the whole snapshot (hi and lo
@@ -350,34 +452,30 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     const int sp = warp & 3;
     const int L = lane & 15, part = L >> 3, e = 8 * sp + (L & 7), q = lane >> 4;
     const bool row_ok = e < 21;
-    uint32_t fph[T5_VOX] = {0, 0, 0};
-    double unscale[T5_VOX];
-#pragma unroll
-    for (int j = 0; j < T5_VOX; ++j) unscale[j] = 0x1p-12 / (double)voxel_scale(j);
-    for (int tt = 0; tt < ntiles; ++tt) {
-#pragma unroll
+    const int nspans = (ntiles + T5_FLUSH - 1) / T5_FLUSH;
+    for (int k = 0; k < nspans; ++k) {
+      const int b = k & 1;
+      mbar_wait_backoff(&ffull[b], (k >> 1) & 1, T5_EPI_SLEEP);
+      tc_fence_after();
+#pragma unroll 1
       for (int j = 0; j < T5_VOX; ++j) {
-        if (!span_end(j, tt)) continue;
-        mbar_wait(&ffull[j], fph[j]);
-        fph[j] ^= 1;
-        tc_fence_after();
-        const uint32_t row = tmem + ((uint32_t)(32 * sp) << 16) + j * NCOL;
+        const uint32_t row = tmem + ((uint32_t)(32 * sp + 16 * b) << 16) + j * NCOL;
         float hi[H], lo[H];
         tmem_ld_half<H>(row, hi);
         tmem_ld_half<H>(row + 8 * NG, lo);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&fempty[j]);
         double* aj = acc + j * ACC_V;
 #pragma unroll
         for (int i = 0; i < H; ++i) {
           float v = hi[i] + lo[i];
           v += __shfl_xor_sync(0xffffffffu, v, 8);  // + the other part's row (entry hi / lo)
           const int sm = q * H + i;
-          if ((i & 1) == part && row_ok && sm < ns) aj[sm * 21 + e] += (double)v * unscale[j];
+          if ((i & 1) == part && row_ok && sm < ns) aj[sm * 21 + e] += (double)v;  // unscaled (exact 2^k at the end)
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fempty[b]);
     }
   }
   tc_fence_before();
@@ -389,19 +487,19 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     const int j = i / per, r = i - j * per;
     const int64_t v = vbase + j;
     if (v >= v1) continue;
-    const double x = acc[j * ACC_V + r];
+    const double x = acc[j * ACC_V + r] * (0x1p-12 / (double)voxel_scale(j));  // exact power of two
     out64[(v - v0) * per + r] = x;
     if (out32) out32[(v - v0) * per + r] = (float)x;
   }
-  if (warp == 15) {
+  if (warp == T5_MMAW) {
     __syncwarp();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
 template <int NG>
-constexpr size_t t5_smem_bytes() {
+constexpr size_t t5_smem_bytes() {  // without the gate bits (T5_VOX * n_pad / 8 bytes more when used)
   return (size_t)T5_STAGES * T5_VOX * T5_KS * (T5_BLK_A + 16 * NG * 16 * 2) + (size_t)T5_VOX * 8 * NG * 21 * 8 +
-         (2 * T5_STAGES + 2 * T5_VOX) * 8 + 4 + 4 * T5_VOX;
+         T5_BAR_BYTES;
 }
 

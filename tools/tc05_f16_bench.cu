@@ -26,7 +26,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
 // element (r, k) of an R x 16 tile, K-major no swizzle: 8-row groups of 2 core matrices (8 x 8 halves)
 __host__ __device__ inline int koff(int r, int k) { return (r >> 3) * 128 + (k >> 3) * 64 + (r & 7) * 8 + (k & 7); }
 
-template <int M, int N>
+template <int M, int N, int DLANE = 0>
 __global__ void k_layout(const __half* A, const __half* B, float* D /*[128][N]*/) {
   __shared__ __align__(128) __half sa[128 * 16];
   __shared__ __align__(128) __half sb[256 * 16];
@@ -69,7 +69,7 @@ __global__ void k_layout(const __half* A, const __half* B, float* D /*[128][N]*/
   if (t == 0) {
     const uint64_t da = make_desc(smem_u32(sa), 128, 256), db = make_desc(smem_u32(sb), 128, 256);
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tb), "l"(da), "l"(db),
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tb + ((uint32_t)DLANE << 16)), "l"(da), "l"(db),
                  "r"(idesc_f16(M, N)), "r"(0));
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
   }
@@ -89,7 +89,7 @@ __global__ void k_layout(const __half* A, const __half* B, float* D /*[128][N]*/
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(256));
 }
 
-template <int M, int N>
+template <int M, int N, int DLANE = 0>
 int layout_test() {
   __half *hA = (__half*)malloc(2 * M * 16), *hB = (__half*)malloc(2 * N * 16);
   float* hD = (float*)malloc(4 * 128 * N);
@@ -100,12 +100,12 @@ int layout_test() {
   cudaMalloc(&dA, 2 * M * 16); cudaMalloc(&dB, 2 * N * 16); cudaMalloc(&dD, 4 * 128 * N);
   cudaMemcpy(dA, hA, 2 * M * 16, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, hB, 2 * N * 16, cudaMemcpyHostToDevice);
-  k_layout<M, N><<<1, 128>>>(dA, dB, dD);
+  k_layout<M, N, DLANE><<<1, 128>>>(dA, dB, dD);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(hD, dD, 4 * 128 * N, cudaMemcpyDeviceToHost);
   // for every row r of the product find the TMEM lane holding it
   int bad = 0;
-  printf("M=%d N=%d: %s; row -> lane:", M, N, cudaGetErrorString(e));
+  printf("M=%d N=%d dlane=%d: %s; row -> lane:", M, N, DLANE, cudaGetErrorString(e));
   for (int r = 0; r < M; ++r) {
     int found = -1;
     for (int lane = 0; lane < 128 && found < 0; ++lane) {
@@ -190,7 +190,8 @@ void rate(const char* name) {
   double flops = 2.0 * M * N * 16 * (double)iters * 148;
   printf("%-28s %s  %6.1f cycles/MMA  %7.1f TFLOP/s\n", name, cudaGetErrorString(e), (double)c / iters, flops / ms / 1e9);
 }
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) { layout_test<64, 144, 16>(); return 0; }
   int bad = layout_test<64, 144>() + layout_test<128, 144>() + layout_test<64, 48>();
   rate<64, 144, 3>("f16 SS M64 N144 acc3");
   rate<64, 144, 1>("f16 SS M64 N144 acc1");
