@@ -125,6 +125,9 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 
 // hi/lo FP16 sigmoids 2^12 / (1 + 2^x), x = (ax z_s) . u + bx, for sample groups [G0, G1),
 // stored as 16-byte vectors (8 samples) at column groups g (hi) and NG + g (lo)
+#ifndef T5_EPI_CHUNK
+#define T5_EPI_CHUNK 1
+#endif
 #ifndef T5_NAMED
 #define T5_NAMED 1
 #endif
@@ -460,11 +463,30 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
 #pragma unroll 1
       for (int j = 0; j < T5_VOX; ++j) {
         const uint32_t row = tmem + ((uint32_t)(32 * sp + 16 * b) << 16) + j * NCOL;
+        double* aj = acc + j * ACC_V;
+#if T5_EPI_CHUNK
+        // 4 columns per load pair: few registers (the buffer is not needed again for 8 tiles)
+#pragma unroll 1
+        for (int c0 = 0; c0 < H; c0 += 4) {
+          uint32_t hr[4], lr[4];
+          asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x4.b32 {%0,%1,%2,%3}, [%4], %5;"
+                       : "=r"(hr[0]), "=r"(hr[1]), "=r"(hr[2]), "=r"(hr[3]) : "r"(row + c0), "n"(H));
+          asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x4.b32 {%0,%1,%2,%3}, [%4], %5;"
+                       : "=r"(lr[0]), "=r"(lr[1]), "=r"(lr[2]), "=r"(lr[3]) : "r"(row + 8 * NG + c0), "n"(H));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float v = __uint_as_float(hr[i]) + __uint_as_float(lr[i]);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            const int sm = q * H + c0 + i;
+            if ((i & 1) == part && row_ok && sm < ns) aj[sm * 21 + e] += (double)v;
+          }
+        }
+#else
         float hi[H], lo[H];
         tmem_ld_half<H>(row, hi);
         tmem_ld_half<H>(row + 8 * NG, lo);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        double* aj = acc + j * ACC_V;
 #pragma unroll
         for (int i = 0; i < H; ++i) {
           float v = hi[i] + lo[i];
@@ -472,6 +494,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
           const int sm = q * H + i;
           if ((i & 1) == part && row_ok && sm < ns) aj[sm * 21 + e] += (double)v;  // unscaled (exact 2^k at the end)
         }
+#endif
       }
       tc_fence_before();
       __syncwarp();
