@@ -174,16 +174,6 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAITS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAITS_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000)
-      : "memory");
-}
 // polling with a sleep between probes (the epilogue waits ~7 000 cycles between flushes)
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, unsigned ns) {
 #if T5_SLEEPWAIT

@@ -11,6 +11,11 @@
 // residual is far from zero — the decision is then provably identical — and
 // evaluated exactly otherwise.  Visible landmarks are compacted through a
 // per-warp smem queue so the FP32 6x6 accumulation runs on full warps.
+// Spatial culling: landmarks are sorted in Morton order and cut into groups of 32 with a
+// bounding box each; a pose first evaluates its five affine visibility rows over each
+// group's box (lane = group, 32 groups per tile), so groups that are certainly outside
+// the view (most of them) are skipped and groups certainly inside go straight to the
+// 6x6 accumulation; only groups the frustum boundary crosses run the per-landmark test.
 #include "fif_common.cuh"
 #include "fif_linalg.cuh"
 
@@ -25,6 +30,14 @@ constexpr int PC_WARPS = 15;  // pose warps; + 1 producer warp = 4 warps per SM 
 constexpr int PC_TILE = PC_TILE_N;
 constexpr int PC_NBUF = 4096 / PC_TILE;  // 128 KB ring (hi + lo)
 constexpr int PC_QCAP = 64;
+#ifndef PC_SLEEPWAIT
+#define PC_SLEEPWAIT 1  // ring waits suspend in hardware instead of spinning
+#endif
+#if PC_SLEEPWAIT
+#define PC_WAIT mbar_wait_sleep
+#else
+#define PC_WAIT mbar_wait
+#endif
 // pre-test image-border rows as FFMA2 pairs (landmark coordinates broadcast): config 3
 // 73.6 -> 70.4 ms, bit-identical decisions (FFMA2 rounds each lane like FFMA)
 #ifndef PC_PACKED
@@ -104,23 +117,78 @@ __device__ __forceinline__ void fim21(float dx, float dy, float dz, float px, fl
 __constant__ int kPR[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
 __constant__ int kPC[21] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5};
 
-// Landmark tables: hi[i] = {p_hi.xyz, |p_hi|_1}, lo[i] = {p_lo.xyz, 0}, p = p_hi + p_lo;
-// *p1max = max_i |p_hi|_1 (float bits, for the pre-test margins).
-__global__ void k_pc_prep(const double* __restrict__ pts, int64_t n, float4* __restrict__ tab,
-                          unsigned* __restrict__ p1max) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// Landmark tables in Morton order (slot k holds landmark i = order[k]): hi[k] = {p_hi.xyz,
+// |p_hi|_1}, lo[k] = {p_lo.xyz, i as int bits}, p = p_hi + p_lo; *p1max = max |p_hi|_1
+// (float bits, for the pre-test margins).
+__global__ void k_pc_prep(const double* __restrict__ pts, int64_t n, const int32_t* __restrict__ order,
+                          float4* __restrict__ tab, unsigned* __restrict__ p1max) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   float l1 = 0.f;
-  if (i < n) {
+  if (k < n) {
+    const int64_t i = order ? (int64_t)order[k] : k;
     float hx, lx, hy, ly, hz, lz;
     split_f32(pts[3 * i], hx, lx);
     split_f32(pts[3 * i + 1], hy, ly);
     split_f32(pts[3 * i + 2], hz, lz);
     l1 = fabsf(hx) + fabsf(hy) + fabsf(hz);
-    tab[i] = make_float4(hx, hy, hz, l1);
-    tab[n + i] = make_float4(lx, ly, lz, 0.f);
+    tab[k] = make_float4(hx, hy, hz, l1);
+    tab[n + k] = make_float4(lx, ly, lz, __int_as_float((int)i));
   }
   const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(l1));  // non-negative floats order as ints
   if ((threadIdx.x & 31) == 0) atomicMax(p1max, m);
+}
+
+// Box of each group of 32 consecutive table slots (over p_hi): centre c and a half
+// extent e rounded up, so every p_hi of the group lies in [c - e, c + e].
+__global__ void k_pc_groups(const float4* __restrict__ tab, int64_t n, float4* __restrict__ gbox) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g * 32 >= n) return;
+  float mn[3] = {3.0e38f, 3.0e38f, 3.0e38f}, mx[3] = {-3.0e38f, -3.0e38f, -3.0e38f};
+  const int64_t end = min(n, g * 32 + 32);
+  for (int64_t k = g * 32; k < end; ++k) {
+    const float4 p = tab[k];
+    mn[0] = fminf(mn[0], p.x), mx[0] = fmaxf(mx[0], p.x);
+    mn[1] = fminf(mn[1], p.y), mx[1] = fmaxf(mx[1], p.y);
+    mn[2] = fminf(mn[2], p.z), mx[2] = fmaxf(mx[2], p.z);
+  }
+  float c[3], e[3];
+  for (int a = 0; a < 3; ++a) {
+    c[a] = 0.5f * (mn[a] + mx[a]);
+    e[a] = fmaxf(__fsub_ru(mx[a], c[a]), __fsub_ru(c[a], mn[a]));
+  }
+  gbox[2 * g] = make_float4(c[0], c[1], c[2], 0.f);
+  gbox[2 * g + 1] = make_float4(e[0], e[1], e[2], 0.f);
+}
+
+// 30-bit Morton key of each landmark over the landmarks' bounding box (part: k_pc_bbox)
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+__global__ void k_pc_mkeys(const double* __restrict__ pts, int64_t n, const double* __restrict__ part, int nparts,
+                           uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
+  __shared__ double box[6];
+  if (threadIdx.x < 6) {
+    const bool is_lo = threadIdx.x < 3;
+    double v = is_lo ? 1e300 : -1e300;
+    for (int b = 0; b < nparts; ++b) v = is_lo ? fmin(v, part[b * 6 + threadIdx.x]) : fmax(v, part[b * 6 + threadIdx.x]);
+    box[threadIdx.x] = v;
+  }
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t c[3];
+  for (int a = 0; a < 3; ++a) {
+    const double ext = box[3 + a] - box[a];
+    const double f = ext > 0 ? (pts[3 * i + a] - box[a]) / ext * 1024.0 : 0.0;
+    c[a] = (uint32_t)fmin(fmax(f, 0.0), 1023.0);
+  }
+  keys[i] = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
+  idx[i] = (int32_t)i;
 }
 
 // FP32 pre-test with rigorous margins, branch-free.  Every quantity the reference
@@ -144,6 +212,25 @@ struct PoseAff {
   f32x2 w12[3], w34[3], c12, c34;  // image-border rows (1, 2) and (3, 4) as FP32x2 pairs
 #endif
 };
+// Group box test.  h_k over the box {c +- e}: h_k(c) +- sum_i |w_ki| e_i.  h_k(c) carries
+// at most ~1.2 of FP32 error (|c|_1 <= 3 max_i |p_i|_1 against the margin's max |p|_1), the
+// extent term 3 roundings (covered by the 1 + 2^-20 factor), so min_k > 3 proves every
+// landmark's exact row value > 1 (all five conditions hold: certainly visible) and any
+// row's max < -1 proves that row fails for every landmark (certainly invisible: for
+// zc > 0 the failed image-border row rejects it, for zc <= 0 the first test does).
+// Returns +1 / -1 / 0 (mixed).
+__device__ __forceinline__ int pc_boxtest(const PoseAff& A, float4 c, float4 e) {
+  float mn = 3.0e38f, mxmin = 3.0e38f;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const float hc = fmaf(A.w[k][0], c.x, fmaf(A.w[k][1], c.y, fmaf(A.w[k][2], c.z, A.c[k])));
+    const float ex = fmaf(fabsf(A.w[k][0]), e.x, fmaf(fabsf(A.w[k][1]), e.y, fabsf(A.w[k][2]) * e.z)) * 1.000001f;
+    mn = fminf(mn, hc - ex);
+    mxmin = fminf(mxmin, hc + ex);
+  }
+  return mn > 3.f ? 1 : (mxmin < -1.f ? -1 : 0);
+}
+
 __device__ __forceinline__ int pc_pretest(const PoseAff& A, float4 ph) {
   float h[5];
 #if PC_PACKED
@@ -169,16 +256,20 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
   return v;
 }
 
-template <bool MASK>
+constexpr int PC_GPT = PC_TILE / 32;  // landmark groups per tile (one per lane)
+static_assert(PC_GPT == 32, "the box test maps one group to each lane");
+template <bool MASK, bool CULL>
 __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double* __restrict__ rot, const double* __restrict__ tr,
                                                           int64_t nq, const double* __restrict__ pts,
-                                                          const float4* __restrict__ ptab, int64_t n, fif_camera cam,
+                                                          const float4* __restrict__ ptab, const float4* __restrict__ gbox,
+                                                          int64_t n, fif_camera cam,
                                                           const unsigned* __restrict__ p1max, float inv_s2, double* __restrict__ out,
                                                           uint8_t* __restrict__ mask, const int32_t* __restrict__ perm) {
   extern __shared__ float4 pcsm[];
   float4* ring_hi = pcsm;                                  // [PC_NBUF][PC_TILE]
-  float4* ring_lo = pcsm + PC_NBUF * PC_TILE;              // [PC_NBUF][PC_TILE]
-  float4* queues = pcsm + 2 * PC_NBUF * PC_TILE;           // [PC_WARPS][PC_QCAP][2]
+  float4* ring_lo = pcsm + PC_NBUF * PC_TILE;              // [PC_NBUF][PC_TILE] (w = original index bits)
+  float4* ring_box = pcsm + 2 * PC_NBUF * PC_TILE;         // [PC_NBUF][2 * PC_GPT] group centre / half extent
+  float4* queues = ring_box + PC_NBUF * 2 * PC_GPT;        // [PC_WARPS][PC_QCAP][2]
   uint64_t* full = reinterpret_cast<uint64_t*>(queues + PC_WARPS * PC_QCAP * 2);  // [PC_NBUF]
   uint64_t* empty = full + PC_NBUF;                                                 // [PC_NBUF]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -199,12 +290,15 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
       for (int64_t it = 0; it < npi; ++it)
         for (int64_t t = 0; t < ntiles; ++t, ++seq) {
           const int b = (int)(seq % PC_NBUF);
-          mbar_wait(&empty[b], (uint32_t)(((seq / PC_NBUF) & 1) ^ 1));
+          PC_WAIT(&empty[b], (uint32_t)(((seq / PC_NBUF) & 1) ^ 1));
           const int64_t base = t * PC_TILE;
-          const uint32_t bytes = (uint32_t)(min((int64_t)PC_TILE, n - base) * sizeof(float4));
-          mbar_expect_tx(&full[b], 2 * bytes);
+          const int cnt = (int)min((int64_t)PC_TILE, n - base);
+          const uint32_t bytes = (uint32_t)(cnt * sizeof(float4));
+          const uint32_t bbytes = CULL ? (uint32_t)(((cnt + 31) / 32) * 2 * sizeof(float4)) : 0u;
+          mbar_expect_tx(&full[b], 2 * bytes + bbytes);
           tma_bulk_g2s(ring_hi + b * PC_TILE, ptab + base, bytes, &full[b]);
           tma_bulk_g2s(ring_lo + b * PC_TILE, ptab + n + base, bytes, &full[b]);
+          if (CULL) tma_bulk_g2s(ring_box + b * 2 * PC_GPT, gbox + 2 * (base / 32), bbytes, &full[b]);
         }
     }
     return;
@@ -267,33 +361,61 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
       const int bsel = (int)(seq % PC_NBUF);
       const uint32_t tile_hi = smem_u32(ring_hi + bsel * PC_TILE) + 16u * lane;  // this lane's first landmark
       const uint32_t tile_lo = smem_u32(ring_lo + bsel * PC_TILE) + 16u * lane;
-      mbar_wait(&full[bsel], (uint32_t)((seq / PC_NBUF) & 1));
+      PC_WAIT(&full[bsel], (uint32_t)((seq / PC_NBUF) & 1));
       if (!has_pose) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[bsel]);
         continue;
       }
-      for (int j0 = 0; j0 < cnt; j0 += 32) {
-        const int j = j0 + lane;
+      // group decisions for this tile: lane g tests group g's box
+      unsigned todo = cnt >= PC_TILE ? 0xffffffffu : (1u << ((cnt + 31) >> 5)) - 1u;
+      unsigned allvis = 0u;
+      if (CULL) {
+        int dec = -1;
+        if (lane < (cnt + 31) >> 5) {
+          const uint32_t bx = smem_u32(ring_box + bsel * 2 * PC_GPT) + 32u * lane;
+          dec = pc_boxtest(A, lds128(bx), lds128(bx + 16u));
+        }
+        allvis = __ballot_sync(0xffffffffu, dec > 0);
+        todo &= ~__ballot_sync(0xffffffffu, dec < 0);
+      }
+      while (todo) {
+        const int g = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int j0 = 32 * g, j = j0 + lane;
+        if ((allvis >> g) & 1u) {  // every landmark of the group is visible: accumulate directly
+          if (j < cnt) {
+            const float4 ph = lds128(tile_hi + 16u * j0), pl = lds128(tile_lo + 16u * j0);
+            const float dx = (ph.x - thx) + (pl.x - tlx), dy = (ph.y - thy) + (pl.y - tly),
+                        dz = (ph.z - thz) + (pl.z - tlz);
+            float e[21];
+            fim21(dx, dy, dz, ph.x, ph.y, ph.z, inv_s2, e);
+#pragma unroll
+            for (int k = 0; k < 21; ++k) acc[k] += e[k];
+            if (MASK) mask[q * n + __float_as_int(pl.w)] = 1;
+          }
+          continue;
+        }
         bool vis = false;
-        float4 ph = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 ph = make_float4(0.f, 0.f, 0.f, 0.f), pl = ph;
         if (j < cnt) {
           ph = lds128(tile_hi + 16u * j0);
           const int pre = pc_pretest(A, ph);
           if (pre == 0) {  // within a margin: the reference's FP64 test (pose re-read: rare path)
-            const int64_t i = base + j;
+            pl = lds128(tile_lo + 16u * j0);
+            const int64_t i = __float_as_int(pl.w);  // original landmark index
             const double* R = rot + 9 * q;
             const PoseR P{R[0], R[1], R[2], R[3], R[4], R[5], R[6], R[7], R[8], tr[3 * q], tr[3 * q + 1], tr[3 * q + 2]};
             vis = pc_visible(P, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], cam, cxw, cyh);
           } else {
             vis = pre > 0;
           }
-          if (MASK) mask[q * n + base + j] = (uint8_t)vis;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, vis);
         if (vis) {
           // d = p - t, exact to ~1 ulp of |d| from the hi / lo parts
-          const float4 pl = lds128(tile_lo + 16u * j0);
+          pl = lds128(tile_lo + 16u * j0);
+          if (MASK) mask[q * n + __float_as_int(pl.w)] = 1;
           const float dx = (ph.x - thx) + (pl.x - tlx), dy = (ph.y - thy) + (pl.y - tly),
                       dz = (ph.z - thz) + (pl.z - tlz);
           const int slot = qn + __popc(bal & lt_mask);
@@ -478,19 +600,50 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
   int64_t cap = (int64_t)num_sms();  // persistent: one CTA (16 warps, ~190 KB smem) per SM
   unsigned blocks = (unsigned)(need < cap ? need : cap);
   const float inv_s2 = (float)(1.0 / (sigma * sigma));
+  // landmark tables in Morton order + group boxes: hi[n], lo[n], max |p|_1, boxes[2 ceil(n/32)]
+  const int64_t ngroups = (n_points + 31) / 32;
   float4* ptab = nullptr;
-  if (cudaMallocAsync(&ptab, sizeof(float4) * (2 * n_points + 1), st) != cudaSuccess) {  // hi[n], lo[n], max |p|_1
+  if (cudaMallocAsync(&ptab, sizeof(float4) * (2 * n_points + 1 + 2 * ngroups), st) != cudaSuccess) {
     set_error("fif_pc_fim: cudaMallocAsync failed");
     return FIF_ERR_CUDA;
   }
   unsigned* p1max = reinterpret_cast<unsigned*>(ptab + 2 * n_points);
+  float4* gbox = ptab + 2 * n_points + 1;
   cudaMemsetAsync(p1max, 0, sizeof(unsigned), st);
-  k_pc_prep<<<(unsigned)((n_points + 255) / 256), 256, 0, st>>>(d_points, n_points, ptab, p1max);
+  static const bool no_cull = getenv("FIF_PC_NOCULL") != nullptr;
+  int32_t* order = nullptr;
+  unsigned char* lbuf = nullptr;
+  if (n_points >= 64 && n_points < (int64_t)INT32_MAX) {
+    size_t temp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)n_points, 0, 30, st);
+    const size_t b4 = ((size_t)n_points * 4 + 255) & ~(size_t)255, bp = sizeof(double) * 6 * PK_BLOCKS;
+    if (cudaMallocAsync(&lbuf, 4 * b4 + bp + temp, st) != cudaSuccess) {
+      cudaFreeAsync(ptab, st);
+      set_error("fif_pc_fim: cudaMallocAsync (landmark order) failed");
+      return FIF_ERR_CUDA;
+    }
+    uint32_t* keys = reinterpret_cast<uint32_t*>(lbuf);
+    uint32_t* keys2 = reinterpret_cast<uint32_t*>(lbuf + b4);
+    int32_t* idx = reinterpret_cast<int32_t*>(lbuf + 2 * b4);
+    order = reinterpret_cast<int32_t*>(lbuf + 3 * b4);
+    double* part = reinterpret_cast<double*>(lbuf + 4 * b4);
+    k_pc_bbox<<<PK_BLOCKS, 256, 0, st>>>(d_points, n_points, part);
+    k_pc_mkeys<<<(unsigned)((n_points + 255) / 256), 256, 0, st>>>(d_points, n_points, part, PK_BLOCKS, keys, idx);
+    FIF_CHECK_LAUNCH("k_pc_mkeys");
+    cub::DeviceRadixSort::SortPairs(lbuf + 4 * b4 + bp, temp, keys, keys2, idx, order, (int)n_points, 0, 30, st);
+  }
+  k_pc_prep<<<(unsigned)((n_points + 255) / 256), 256, 0, st>>>(d_points, n_points, order, ptab, p1max);
   FIF_CHECK_LAUNCH("k_pc_prep");
-  const size_t smem = sizeof(float4) * (2 * PC_NBUF * PC_TILE + PC_WARPS * PC_QCAP * 2) + 2 * PC_NBUF * sizeof(uint64_t);
+  k_pc_groups<<<(unsigned)((ngroups + 127) / 128), 128, 0, st>>>(ptab, n_points, gbox);
+  FIF_CHECK_LAUNCH("k_pc_groups");
+  if (lbuf) cudaFreeAsync(lbuf, st);
+  if (d_mask) cudaMemsetAsync(d_mask, 0, (size_t)q * (size_t)n_points, st);  // the kernel writes the visible pairs
+  const size_t smem = sizeof(float4) * (2 * PC_NBUF * PC_TILE + PC_NBUF * 2 * PC_GPT + PC_WARPS * PC_QCAP * 2) +
+                      2 * PC_NBUF * sizeof(uint64_t);
   static std::atomic<uint64_t> attr{0};
   if (needs_setup(attr)) {
-    for (auto f : {k_pc_fim<true>, k_pc_fim<false>}) {
+    for (auto f : {k_pc_fim<true, true>, k_pc_fim<false, true>, k_pc_fim<true, false>, k_pc_fim<false, false>}) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
@@ -519,12 +672,12 @@ extern "C" int fif_pc_fim(const double* d_rot, const double* d_t, int64_t q, con
     FIF_CHECK_LAUNCH("k_pc_keys");
     cub::DeviceRadixSort::SortPairs(sbuf + 4 * b4 + bp, temp, keys, keys2, idx, perm, (int)q, 0, 19, st);
   }
-  if (d_mask)
-    k_pc_fim<true><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, p1max, inv_s2,
-                                                        d_out, d_mask, perm);
-  else
-    k_pc_fim<false><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, n_points, *cam, p1max, inv_s2,
-                                                         d_out, d_mask, perm);
+#define PC_LAUNCH(M, C)                                                                                       \
+  k_pc_fim<M, C><<<blocks, (PC_WARPS + 1) * 32, smem, st>>>(d_rot, d_t, q, d_points, ptab, gbox, n_points, *cam, p1max, \
+                                                            inv_s2, d_out, d_mask, perm)
+  if (d_mask) { if (no_cull) PC_LAUNCH(true, false); else PC_LAUNCH(true, true); }
+  else { if (no_cull) PC_LAUNCH(false, false); else PC_LAUNCH(false, true); }
+#undef PC_LAUNCH
   if (sbuf) cudaFreeAsync(sbuf, st);
   cudaFreeAsync(ptab, st);
   FIF_CHECK_LAUNCH("k_pc_fim");
