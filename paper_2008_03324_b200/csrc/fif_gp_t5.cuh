@@ -275,7 +275,12 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   if (warp < T5_PWARPS) {
     voxel_split(src, pvok ? pv : v0, ch, cl);
     float mx = 0.f;
+#ifdef T5_PROBE_NO_PREPASS  // timing probe only (wrong scale)
+    if (pvok) mx = 1.0e4f;
+    if (false) {
+#else
     if (pvok) {
+#endif
       // max over landmarks of (1 + |p|^2) / n^2 as a fraction bn / bd (no division per landmark);
       // n^2 from the same hi/lo difference as pair_prologue, the same skip rule
       float bn = 0.f, bd = 1.f;
