@@ -132,7 +132,10 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 #define T5_NAMED 1
 #endif
 #ifndef T5_EPI_SLEEP
-#define T5_EPI_SLEEP 256
+#define T5_EPI_SLEEP 2000
+#endif
+#ifndef T5_PROD_SLEEP
+#define T5_PROD_SLEEP 64
 #endif
 #ifndef T5_MMA_SLEEP
 #define T5_MMA_SLEEP 20
@@ -182,6 +185,11 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 #else
   while (!mbar_try(bar, parity)) __nanosleep(ns);
 #endif
+}
+// plain polling with a fixed sleep between probes (the suspending try_wait re-probes every
+// few dozen cycles, which at 3 waiting warps cost ~4 % of the kernel's issue slots)
+__device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity, unsigned ns) {
+  while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
 // named barriers: the producers arrive (no wait) and the MMA warp blocks in hardware
 __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -365,7 +373,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         if (!keep) b.w = 0.f;
       }
       const PairF q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
-      if (tt >= T5_STAGES) mbar_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
+      if (tt >= T5_STAGES) mbar_wait_poll(&empty[s], ((tt / T5_STAGES) - 1) & 1, T5_PROD_SLEEP);
       const uint32_t adst = sbase + (s * T5_VOX + pj) * STAGE_A + kofs_a;
       const uint32_t bdst = sbase + OFF_B + (s * T5_VOX + pj) * STAGE_B + kofs_b;
       if (ph == 0) {
@@ -453,7 +461,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     const int nspans = (ntiles + T5_FLUSH - 1) / T5_FLUSH;
     for (int k = 0; k < nspans; ++k) {
       const int b = k & 1;
-      mbar_wait_backoff(&ffull[b], (k >> 1) & 1, T5_EPI_SLEEP);
+      mbar_wait_poll(&ffull[b], (k >> 1) & 1, T5_EPI_SLEEP);
       tc_fence_after();
 #pragma unroll 1
       for (int j = 0; j < T5_VOX; ++j) {
