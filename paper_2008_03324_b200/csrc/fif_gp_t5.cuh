@@ -140,9 +140,6 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 #ifndef T5_MMA_SLEEP
 #define T5_MMA_SLEEP 20
 #endif
-#ifndef T5_PREPASS_W
-#define T5_PREPASS_W 0
-#endif
 #ifndef T5_SLEEPWAIT
 #define T5_SLEEPWAIT 1
 #endif
@@ -282,55 +279,82 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   float ch[3] = {0.f, 0.f, 0.f}, cl[3] = {0.f, 0.f, 0.f};
   if (warp < T5_PWARPS) {
     voxel_split(src, pvok ? pv : v0, ch, cl);
-    float mx = 0.f;
-#ifdef T5_PROBE_NO_PREPASS  // timing probe only (wrong scale)
-    if (pvok) mx = 1.0e4f;
-    if (false) {
-#else
-    if (pvok) {
-#endif
-      // max over landmarks of (1 + |p|^2) / n^2 as a fraction bn / bd (no division per landmark);
-      // n^2 from the same hi/lo difference as pair_prologue, the same skip rule
-      float bn = 0.f, bd = 1.f;
-      constexpr int PT = 64 * T5_PARTS;  // pre-pass threads per voxel
-      for (int64_t i0 = ph * 64 + pk; i0 < n_pad; i0 += 4 * PT) {
-        float4 a[4], b[4];
+    // Pre-pass: the voxel's bound 2 w (1 + |p|^2) >= 2 max|E| (|c2| <= |p|; the factor 2 also
+    // covers the rounding of w = inv_s2 rsqrt(n^2)^2 in the build), w = inv_s2 / n^2, as
+    // the fraction bn / bd = max (1 + |p|^2) / n^2 (no division per landmark); n^2 from the
+    // same hi/lo difference as pair_prologue, the same skip rule.
+    auto frac_update = [&](float4 a, float4 b, const float* c_h, const float* c_l, float& bn, float& bd) {
+      const float dx = __fadd_rn(__fsub_rn(a.x, c_h[0]), __fsub_rn(b.x, c_l[0]));
+      const float dy = __fadd_rn(__fsub_rn(a.y, c_h[1]), __fsub_rn(b.y, c_l[1]));
+      const float dz = __fadd_rn(__fsub_rn(a.z, c_h[2]), __fsub_rn(b.z, c_l[2]));
+      const float n2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      const float num = 1.0f + a.w;
+      if (n2 > 1e-30f && b.w != 0.f && num * bd > bn * n2) {
+        bn = num;
+        bd = n2;
+      }
+    };
+    if (!HAS_MASK) {
+      // unmasked: each producer thread loads a landmark once for all three voxels (a third
+      // of the L2 traffic of per-voxel scans; the pre-pass is L2-bandwidth-bound)
+      float vh[T5_VOX][3], vl[T5_VOX][3], bn[T5_VOX], bd[T5_VOX];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+      for (int j = 0; j < T5_VOX; ++j) {
+        voxel_split(src, vbase + j < v1 ? vbase + j : v0, vh[j], vl[j]);
+        bn[j] = 0.f;
+        bd[j] = 1.f;
+      }
+      constexpr int PT = T5_PWARPS * 32;
+      for (int64_t i0 = warp * 32 + lane; i0 < n_pad; i0 += 2 * PT) {
+        float4 a[2], b[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
           const int64_t i = i0 + PT * u;
           a[u] = i < n_pad ? lm[2 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
           b[u] = i < n_pad ? lm[2 * i + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (HAS_MASK && b[u].w != 0.f && !gate_keep(gate, pv, i0 + PT * u)) b[u].w = 0.f;
-          if (HAS_MASK && use_gbits) {  // warp = 32 consecutive landmarks: one word
-            const unsigned wbits = __ballot_sync(0xffffffffu, b[u].w != 0.f);
-            if (lane == 0) gbits[pj * (n_pad >> 5) + ((i0 + PT * u) >> 5)] = wbits;
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int j = 0; j < T5_VOX; ++j) frac_update(a[u], b[u], vh[j], vl[j], bn[j], bd[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < T5_VOX; ++j) {
+        float mx = (vbase + j < v1 && bn[j] > 0.f) ? 2.0f * inv_s2 * __fdiv_rn(bn[j], bd[j]) : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) atomicMax(&sbits[j], __float_as_int(mx));
+      }
+    } else {
+      // masked: the voxel's own threads evaluate each pair's gate once (kept as bits)
+      float mx = 0.f;
+      if (pvok) {
+        float bn = 0.f, bd = 1.f;
+        constexpr int PT = 64 * T5_PARTS;  // pre-pass threads per voxel
+        for (int64_t i0 = ph * 64 + pk; i0 < n_pad; i0 += 4 * PT) {
+          float4 a[4], b[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + PT * u;
+            a[u] = i < n_pad ? lm[2 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            b[u] = i < n_pad ? lm[2 * i + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-#if T5_PREPASS_W
-          const PairF q = pair_prologue(a[u], b[u], ch, cl, inv_s2);
-          mx = fmaxf(mx, fmaf(a[u].w, 2.0f * q.w, 2.0f * q.w));  // >= 2 max|E| (|c2| <= |p|)
-          continue;
-#endif
-          const float dx = __fadd_rn(__fsub_rn(a[u].x, ch[0]), __fsub_rn(b[u].x, cl[0]));
-          const float dy = __fadd_rn(__fsub_rn(a[u].y, ch[1]), __fsub_rn(b[u].y, cl[1]));
-          const float dz = __fadd_rn(__fsub_rn(a[u].z, ch[2]), __fsub_rn(b[u].z, cl[2]));
-          const float n2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-          const float num = 1.0f + a[u].w;
-          if (n2 > 1e-30f && b[u].w != 0.f && num * bd > bn * n2) {
-            bn = num;
-            bd = n2;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (b[u].w != 0.f && !gate_keep(gate, pv, i0 + PT * u)) b[u].w = 0.f;
+            if (use_gbits) {  // warp = 32 consecutive landmarks: one word
+              const unsigned wbits = __ballot_sync(0xffffffffu, b[u].w != 0.f);
+              if (lane == 0) gbits[pj * (n_pad >> 5) + ((i0 + PT * u) >> 5)] = wbits;
+            }
+            frac_update(a[u], b[u], ch, cl, bn, bd);
           }
         }
+        mx = bn > 0.f ? 2.0f * inv_s2 * __fdiv_rn(bn, bd) : 0.f;
       }
-      // 2 w (1 + |p|^2) with w = inv_s2 / n^2: >= 2 max|E| (|c2| <= |p|); the factor 2 also
-      // covers the rounding of w = inv_s2 rsqrt(n^2)^2 in the build
-      if (!T5_PREPASS_W) mx = bn > 0.f ? 2.0f * inv_s2 * __fdiv_rn(bn, bd) : 0.f;
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) atomicMax(&sbits[pj], __float_as_int(mx));
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) atomicMax(&sbits[pj], __float_as_int(mx));
+    }
   }
   tc_fence_before();
   __syncthreads();
