@@ -1588,8 +1588,8 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
     // tcgen05 path: one tcgen05.mma (M=64, N=16 NG, K=16) per voxel per 16 landmarks, TMEM accumulators
     const int ng = (ns + 7) / 8;
     T5Z z{};
-    for (int sidx = 0; sidx < ns; ++sidx)
-      for (int c = 0; c < 3; ++c) z.z[c][sidx] = (float)(ax * model->zs_host[3 * sidx + c]);
+    for (int sidx = 0; sidx < ns; ++sidx)  // sample s at slot s ^ 1 (pairs swapped: t5_sigmoids)
+      for (int c = 0; c < 3; ++c) z.z[c][sidx ^ 1] = (float)(ax * model->zs_host[3 * sidx + c]);
     const unsigned blocks5 = (unsigned)((rows + T5_VOX - 1) / T5_VOX);
     int rc = FIF_OK;
 #define T5_CASE(NG)                                                                                         \

@@ -53,7 +53,7 @@ constexpr int T5_BLK_A = 64 * 16 * 2;  // bytes per k-step of A (M = 64)
 constexpr int T5_BAR_BYTES = 128;  // mbarriers, TMEM slot, scale bits (rounded up)
 constexpr int T5_SMEM_MAX = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 struct __align__(16) T5Z {
-  float z[3][8 * T5_MAX_NG];  // ax * zs[s][c] (FP32), 0 past N_s
+  float z[3][8 * T5_MAX_NG];  // ax * zs[s ^ 1][c] (FP32; pairs swapped, see t5_sigmoids), 0 past N_s
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -146,11 +146,30 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 #ifndef T5_XPAIR
 #define T5_XPAIR 1
 #endif
+#ifndef T5_SPLIT_TRUNC
+#define T5_SPLIT_TRUNC 1
+#endif
 #ifndef T5_SPLIT2
 #define T5_SPLIT2 1
 #endif
-// FP16 hi + lo of two FP32 values; T5_SPLIT2: residuals as one packed FP32x2 subtraction
+// FP16 hi + lo of two FP32 values.  T5_SPLIT_TRUNC: hi = x with its 13 low mantissa bits
+// cleared (exactly representable in FP16 wherever FP16 is normal), lo = x - hi exact in
+// FP32, both converted once -- the converted halves feed only the 16-byte operand stores,
+// so they are allocated straight into the store's register quad (the round-to-nearest
+// variant converts hi back to FP32 for the residual and needs register moves to build the
+// quad).  |x - hi - lo16| <= 2^-21 |x| (2^-22 with round-to-nearest hi); below FP16's
+// normal range both keep the absolute error <= 2^-25 (in scaled units).
+// T5_SPLIT2: residuals as one packed FP32x2 subtraction.
 __device__ __forceinline__ void t5_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+#if T5_SPLIT_TRUNC
+  const float h0 = __uint_as_float(__float_as_uint(x0) & 0xFFFFE000u);
+  const float h1 = __uint_as_float(__float_as_uint(x1) & 0xFFFFE000u);
+  float d0, d1;
+  unpack2(fsub2(pack2(x0, x1), pack2(h0, h1)), d0, d1);
+  const __half2 h = __floats2half2_rn(h0, h1), l = __floats2half2_rn(d0, d1);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+#else
   const __half2 h = __floats2half2_rn(x0, x1);
   const float2 b = __half22float2(h);
 #if T5_SPLIT2
@@ -162,6 +181,7 @@ __device__ __forceinline__ void t5_split2(float x0, float x1, uint32_t& hi, uint
 #endif
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
+#endif
 }
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -211,11 +231,13 @@ __device__ __forceinline__ void t5_sigmoids(const T5Z& Z, float ux, float uy, fl
 #endif
       float y0, y1;  // 2^-12 (1 + 2^x) for both, one FFMA2
       unpack2(ffma2(pack2(ex2_approx(x0), ex2_approx(x1)), splat2(0x1p-12f), splat2(0x1p-12f)), y0, y1);
-      // one reciprocal for both sigmoids: r = 1 / (y0 y1), sg0 = y1 r, sg1 = y0 r (the host
-      // launches this kernel only when x <= 60, so y0 y1 <= 2^98 stays finite; y >= 2^-12)
+      // one reciprocal for both sigmoids: r = 1 / (y0 y1), 1 / y1 = y0 r, 1 / y0 = y1 r (the
+      // host launches this kernel only when x <= 60, so y0 y1 <= 2^98 stays finite; y >= 2^-12).
+      // The host stores each sample pair's directions swapped in Z (x0 belongs to sample
+      // s0 + 1), so (y0 r, y1 r) is (sigma(s0), sigma(s0 + 1)) in place: no register swap.
       const float r = rcp_approx(y0 * y1);
       float sg0, sg1;
-      unpack2(fmul2(pack2(y1, y0), splat2(r)), sg0, sg1);
+      unpack2(fmul2(pack2(y0, y1), splat2(r)), sg0, sg1);
       t5_split2(sg0, sg1, hv[p], lv[p]);
     }
     sts128(bdst + g * 128, hv[0], hv[1], hv[2], hv[3]);
