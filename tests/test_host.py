@@ -141,7 +141,7 @@ def test_c_abi_exports_every_declared_symbol():
     L = _lib.load()
     for name in declared:
         assert hasattr(L, name)
-    assert L.fif_abi_version() == 1
+    assert L.fif_abi_version() == 2
     assert L.fif_build_scratch_bytes(1000) >= 1000 * 32
 
 
