@@ -1596,7 +1596,8 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
   case NG: {                                                                                                \
     constexpr size_t sm = t5_smem_bytes<NG>();                                                              \
     const size_t gb = (size_t)T5_VOX * (n_pad / 8);                                                         \
-    const int use_gb = has_mask && sm + gb <= T5_SMEM_MAX;                                                  \
+    static const bool no_gb = getenv("FIF_T5_NO_GATE_BITS") != nullptr;                                     \
+    const int use_gb = has_mask && !no_gb && sm + gb <= T5_SMEM_MAX;                                        \
     static std::atomic<uint64_t> attr{0};                                                                   \
     if (needs_setup(attr)) {                                                                                \
       cudaFuncSetAttribute(k_gp_info_t5<NG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, T5_SMEM_MAX); \

@@ -364,9 +364,10 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (b[u].w != 0.f && !gate_keep(gate, pv, i0 + PT * u)) b[u].w = 0.f;
-            if (use_gbits) {  // warp = 32 consecutive landmarks: one word
+            if (use_gbits) {  // warp = 32 consecutive landmarks: one word (none past n_pad: the
+                              // next voxel's words follow)
               const unsigned wbits = __ballot_sync(0xffffffffu, b[u].w != 0.f);
-              if (lane == 0) gbits[pj * (n_pad >> 5) + ((i0 + PT * u) >> 5)] = wbits;
+              if (lane == 0 && i0 + PT * u < n_pad) gbits[pj * (n_pad >> 5) + ((i0 + PT * u) >> 5)] = wbits;
             }
             frac_update(a[u], b[u], ch, cl, bn, bd);
           }

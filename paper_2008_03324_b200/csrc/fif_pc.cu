@@ -28,7 +28,10 @@ constexpr int PC_WARPS = 15;  // pose warps; + 1 producer warp = 4 warps per SM 
 #define PC_TILE_N 1024
 #endif
 constexpr int PC_TILE = PC_TILE_N;
-constexpr int PC_NBUF = 4096 / PC_TILE;  // 128 KB ring (hi + lo)
+#ifndef PC_RING_LM
+#define PC_RING_LM 4096
+#endif
+constexpr int PC_NBUF = PC_RING_LM / PC_TILE;  // 128 KB ring (hi + lo) at 4096 landmarks
 constexpr int PC_QCAP = 64;
 #ifndef PC_SLEEPWAIT
 #define PC_SLEEPWAIT 1  // ring waits suspend in hardware instead of spinning
@@ -257,7 +260,7 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
 }
 
 constexpr int PC_GPT = PC_TILE / 32;  // landmark groups per tile (one per lane)
-static_assert(PC_GPT == 32, "the box test maps one group to each lane");
+static_assert(PC_GPT <= 32 && PC_TILE % 32 == 0, "the box test maps one group to each lane");
 template <bool MASK, bool CULL>
 __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double* __restrict__ rot, const double* __restrict__ tr,
                                                           int64_t nq, const double* __restrict__ pts,
@@ -368,11 +371,12 @@ __global__ void __launch_bounds__((PC_WARPS + 1) * 32, 1) k_pc_fim(const double*
         continue;
       }
       // group decisions for this tile: lane g tests group g's box
-      unsigned todo = cnt >= PC_TILE ? 0xffffffffu : (1u << ((cnt + 31) >> 5)) - 1u;
+      const int ngr = (cnt + 31) >> 5;
+      unsigned todo = ngr >= 32 ? 0xffffffffu : (1u << ngr) - 1u;
       unsigned allvis = 0u;
       if (CULL) {
         int dec = -1;
-        if (lane < (cnt + 31) >> 5) {
+        if (lane < ngr) {
           const uint32_t bx = smem_u32(ring_box + bsel * 2 * PC_GPT) + 32u * lane;
           dec = pc_boxtest(A, lds128(bx), lds128(bx + 16u));
         }

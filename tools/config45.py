@@ -95,6 +95,8 @@ if a.full:
     print(f"config4 GP-70 info, whole grid: {grid.voxel_count * N:.3e} pairs in {t:.1f} s = "
           f"{grid.voxel_count * N / t:.3e} pairs/s; field {f.memory_stats()['device_bytes'] / 1e9:.1f} GB on device",
           flush=True)
+    _, t_tab = timed(lambda: f.trace_table())  # one-time FP64 trace table (first trace query builds it)
+    print(f"config5: FP64 trace table of the config-4 field built in {t_tab * 1e3:.1f} ms (once per field)", flush=True)
     qrng = np.random.default_rng(4)
     chunk = 1 << 20
     batches = chunk // 64
