@@ -125,6 +125,9 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 
 // hi/lo FP16 sigmoids 2^12 / (1 + 2^x), x = (ax z_s) . u + bx, for sample groups [G0, G1),
 // stored as 16-byte vectors (8 samples) at column groups g (hi) and NG + g (lo)
+#ifndef T5_ROTATE_ROLES
+#define T5_ROTATE_ROLES 1
+#endif
 #ifndef T5_EPI_CHUNK
 #define T5_EPI_CHUNK 1
 #endif
@@ -295,7 +298,15 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   // producers: voxel centre, then the pre-pass bound on max |E| of their voxel
-  const int pj = warp / (2 * T5_PARTS), ph = (warp >> 1) % T5_PARTS, pk = ((warp & 1) << 5) | lane;
+  // producer warp w: voxel pj = w / (2 PARTS); its role r (sample part, landmark half) is
+  // rotated by the voxel so each SM sub-partition (w % 4) mixes heavy part-0 warps (entries +
+  // their samples) with light ones instead of holding the same role for all three voxels
+#if T5_ROTATE_ROLES
+  const int prole = ((warp % (2 * T5_PARTS)) + warp / (2 * T5_PARTS)) % (2 * T5_PARTS);
+#else
+  const int prole = warp % (2 * T5_PARTS);
+#endif
+  const int pj = warp / (2 * T5_PARTS), ph = prole >> 1, pk = ((prole & 1) << 5) | lane;
   const int64_t pv = vbase + pj;
   const bool pvok = warp < T5_PWARPS && pv < v1;
   float ch[3] = {0.f, 0.f, 0.f}, cl[3] = {0.f, 0.f, 0.f};
