@@ -1740,11 +1740,13 @@ extern "C" int fif_build_matched(int factor_kind, const fif_model* model, const 
 
 extern "C" int fif_export_reference(int factor_kind, const fif_model* model, const double* d_in64, int64_t rows,
                                     double* d_out, void* stream) {
-  FIF_CHECK_ARG(model != nullptr && d_in64 != nullptr && d_out != nullptr, "fif_export_reference: NULL argument");
+  FIF_CHECK_ARG(model != nullptr, "fif_export_reference: NULL model");
+  FIF_CHECK_ARG(rows >= 0, "fif_export_reference: rows < 0");
+  if (rows == 0) return FIF_OK;  // an empty field (no occupied voxel) exports nothing
+  FIF_CHECK_ARG(d_in64 != nullptr && d_out != nullptr, "fif_export_reference: NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
   const bool trace = factor_kind == FIF_KIND_TRACE;
   const int nv = model->kind == FIF_MODEL_QUAD ? 10 : model->n_v;
-  if (rows == 0) return FIF_OK;
   const double* src = d_in64;
   double* tmp = nullptr;
   if (model->kind == FIF_MODEL_GP) {

@@ -32,10 +32,16 @@
 #pragma once
 // (included inside namespace fif)
 
-constexpr int T5_VOX = 3;           // voxels per CTA (TMEM: 3 x 16 NG <= 480 of 512 columns)
+#ifndef T5_VOX_N
+#define T5_VOX_N 3                  // voxels per CTA (TMEM: 3 x 16 NG <= 480 of 512 columns)
+#endif
+#ifndef T5_STAGES_N
+#define T5_STAGES_N 2
+#endif
+constexpr int T5_VOX = T5_VOX_N;
 constexpr int T5_TILE = 64;         // landmarks per pipeline stage
 constexpr int T5_KS = T5_TILE / 16; // MMAs per voxel per stage
-constexpr int T5_STAGES = 2;
+constexpr int T5_STAGES = T5_STAGES_N;
 constexpr int T5_FLUSH = 8;         // FP32 accumulation span: 8 tiles = 512 landmarks
 #ifndef T5_PARTS
 #define T5_PARTS 2                  // sample parts per (voxel, landmark) pair: one thread each
@@ -51,6 +57,11 @@ constexpr int T5_MAX_NG = 10;       // N_s <= 80
 constexpr int T5_BLK_A = 64 * 16 * 2;  // bytes per k-step of A (M = 64)
 
 constexpr int T5_BAR_BYTES = 128;  // mbarriers, TMEM slot, scale bits (rounded up)
+// PARTS = 4: part 0 shares each pair's bearing with parts 1-3 through shared memory
+// ([stage][voxel][landmark] float4, after the barriers) and a named barrier per
+// (voxel, landmark half, stage): ids 1 + T5_STAGES ...
+constexpr int T5_USH_BYTES = T5_PARTS >= 3 ? T5_STAGES * T5_VOX * T5_TILE * 16 : 0;
+static_assert(1 + T5_STAGES + (T5_PARTS >= 3 ? 2 * T5_VOX * T5_STAGES : 0) <= 16, "named barrier ids");
 constexpr int T5_SMEM_MAX = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 struct __align__(16) T5Z {
   float z[3][8 * T5_MAX_NG];  // ax * zs[s ^ 1][c] (FP32; pairs swapped, see t5_sigmoids), 0 past N_s
@@ -262,8 +273,11 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   constexpr int ACC_V = 8 * NG * 21;            // doubles per voxel
   constexpr int OFF_BAR = OFF_ACC + T5_VOX * ACC_V * 8;
   // sample-group boundaries of the parts; part 0 also computes the 21 entries (~ 13 samples of work)
-  constexpr int G1 = T5_PARTS == 1 ? NG : T5_PARTS == 2 ? NG / 2 : (2 * NG + 4) / 9;
-  constexpr int G2 = T5_PARTS == 2 ? NG : G1 + (NG - G1) * 3 / 7;
+  // (PARTS = 4: part 0's entries cost ~1.75 sample groups; the rest split over parts 1-3)
+  constexpr int G1 = T5_PARTS == 1 ? NG : T5_PARTS == 2 ? NG / 2 : T5_PARTS == 3 ? (2 * NG + 4) / 9
+                                                                   : (NG >= 6 ? (NG - 5 + 2) / 4 : 0);
+  constexpr int G2 = T5_PARTS == 2 ? NG : T5_PARTS == 3 ? G1 + (NG - G1) * 3 / 7 : G1 + (NG - G1 + 2) / 3;
+  constexpr int G3 = T5_PARTS == 4 ? G2 + (NG - G2 + 1) / 2 : NG;
   extern __shared__ __align__(1024) unsigned char smem[];
   double* acc = reinterpret_cast<double*>(smem + OFF_ACC);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -274,7 +288,8 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   int* sbits = reinterpret_cast<int*>(tmem_slot + 1);
   // masked builds: the pre-pass evaluates each pair's matchability gate once and keeps the
   // answers as bits ([voxel][n_pad / 32] words) for the main loop (when they fit)
-  uint32_t* gbits = reinterpret_cast<uint32_t*>(smem + OFF_BAR + T5_BAR_BYTES);
+  float4* ush = reinterpret_cast<float4*>(smem + OFF_BAR + T5_BAR_BYTES);  // PARTS = 4 bearing share
+  uint32_t* gbits = reinterpret_cast<uint32_t*>(smem + OFF_BAR + T5_BAR_BYTES + T5_USH_BYTES);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int64_t vbase = v0 + (int64_t)blockIdx.x * T5_VOX;
   const int ntiles = (int)(n_pad / T5_TILE);
@@ -430,8 +445,23 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
                                     : gate_keep(gate, pv, i);
         if (!keep) b.w = 0.f;
       }
-      const PairF q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
+      PairF q;
+      if (T5_PARTS < 4 || ph == 0) q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
       if (tt >= T5_STAGES) mbar_wait_poll(&empty[s], ((tt / T5_STAGES) - 1) & 1, T5_PROD_SLEEP);
+      if (T5_PARTS == 4) {  // part 0 hands its bearing to parts 1-3 (the slot is free: its last
+                            // readers finished the tile whose MMA freed this stage)
+        const int bid = 1 + T5_STAGES + ((pj * 2 + (pk >> 5)) * T5_STAGES + s);
+        float4* slot = ush + (s * T5_VOX + pj) * T5_TILE + pk;
+        if (ph == 0) {
+          *slot = make_float4(q.ux, q.uy, q.uz, 0.f);
+          __syncwarp();
+          named_arrive(bid, 128);
+        } else {
+          named_sync(bid, 128);
+          const float4 u4 = *slot;
+          q.ux = u4.x, q.uy = u4.y, q.uz = u4.z, q.w = 0.f;
+        }
+      }
       const uint32_t adst = sbase + (s * T5_VOX + pj) * STAGE_A + kofs_a;
       const uint32_t bdst = sbase + OFF_B + (s * T5_VOX + pj) * STAGE_B + kofs_b;
       if (ph == 0) {
@@ -449,8 +479,10 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         t5_sigmoids<NG, 0, G1>(Z, q.ux, q.uy, q.uz, bx, bdst);
       } else if (T5_PARTS == 2 || ph == 1) {
         t5_sigmoids<NG, G1, G2>(Z, q.ux, q.uy, q.uz, bx, bdst);
+      } else if (T5_PARTS == 3 || ph == 2) {
+        t5_sigmoids<NG, G2, G3>(Z, q.ux, q.uy, q.uz, bx, bdst);
       } else {
-        t5_sigmoids<NG, G2, NG>(Z, q.ux, q.uy, q.uz, bx, bdst);
+        t5_sigmoids<NG, G3, NG>(Z, q.ux, q.uy, q.uz, bx, bdst);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -584,6 +616,6 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
 template <int NG>
 constexpr size_t t5_smem_bytes() {  // without the gate bits (T5_VOX * n_pad / 8 bytes more when used)
   return (size_t)T5_STAGES * T5_VOX * T5_KS * (T5_BLK_A + 16 * NG * 16 * 2) + (size_t)T5_VOX * 8 * NG * 21 * 8 +
-         T5_BAR_BYTES;
+         T5_BAR_BYTES + T5_USH_BYTES;
 }
 

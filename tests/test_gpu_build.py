@@ -210,6 +210,19 @@ def test_serialize_roundtrip(models, small_grid, g_small, tmp_path):
         # quad: FP64 rows round-trip exactly; GP: S = K F is re-rounded to the FP32 query copy
         tol = 1e-12 if mname == "quad" else 1e-6
         assert np.abs(a - b).max() <= tol * np.abs(a).max()
+    # a field with no rows (empty landmark set, or matchability rejecting every voxel) is a
+    # valid FIF1 file, as the reference writes it: it round-trips
+    for mname in ("quad", "gp30"):
+        for kind in ("trace", "info"):
+            e = F.Field.build(np.zeros((0, 3)), small_grid, models[mname], kind)
+            pe = tmp_path / f"empty_{mname}_{kind}.fif"
+            e.serialize(pe)
+            ge = F.Field.deserialize(pe)
+            assert ge.rows == 0 and (ge.slots == -1).all()
+            fims, ok = ge.query_fim_batch(g_small["positions"][:4], g_small["rotations"][:4], "trilinear") \
+                if kind == "info" else (None, None)
+            if kind == "info":
+                assert np.all(fims == 0)
     with pytest.raises(F.BadMagic):
         bad = tmp_path / "bad.fif"
         bad.write_bytes(b"XXXX" + b"\0" * 64)
