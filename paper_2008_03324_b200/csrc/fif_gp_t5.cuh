@@ -60,8 +60,11 @@ constexpr int T5_BAR_BYTES = 128;  // mbarriers, TMEM slot, scale bits (rounded 
 // PARTS = 4: part 0 shares each pair's bearing with parts 1-3 through shared memory
 // ([stage][voxel][landmark] float4, after the barriers) and a named barrier per
 // (voxel, landmark half, stage): ids 1 + T5_STAGES ...
-constexpr int T5_USH_BYTES = T5_PARTS >= 3 ? T5_STAGES * T5_VOX * T5_TILE * 16 : 0;
-static_assert(1 + T5_STAGES + (T5_PARTS >= 3 ? 2 * T5_VOX * T5_STAGES : 0) <= 16, "named barrier ids");
+#ifndef T5_SHARE_U
+#define T5_SHARE_U (T5_PARTS >= 4)  // part 0 computes each pair's bearing once for all parts
+#endif
+constexpr int T5_USH_BYTES = T5_SHARE_U ? T5_STAGES * T5_VOX * T5_TILE * 16 : 0;
+static_assert(1 + T5_STAGES + (T5_SHARE_U ? 2 * T5_VOX * T5_STAGES : 0) <= 16, "named barrier ids");
 constexpr int T5_SMEM_MAX = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 struct __align__(16) T5Z {
   float z[3][8 * T5_MAX_NG];  // ax * zs[s ^ 1][c] (FP32; pairs swapped, see t5_sigmoids), 0 past N_s
@@ -446,18 +449,18 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         if (!keep) b.w = 0.f;
       }
       PairF q;
-      if (T5_PARTS < 4 || ph == 0) q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
+      if (!T5_SHARE_U || ph == 0) q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
       if (tt >= T5_STAGES) mbar_wait_poll(&empty[s], ((tt / T5_STAGES) - 1) & 1, T5_PROD_SLEEP);
-      if (T5_PARTS == 4) {  // part 0 hands its bearing to parts 1-3 (the slot is free: its last
+      if (T5_SHARE_U) {  // part 0 hands its bearing to the other parts (the slot is free: its last
                             // readers finished the tile whose MMA freed this stage)
         const int bid = 1 + T5_STAGES + ((pj * 2 + (pk >> 5)) * T5_STAGES + s);
         float4* slot = ush + (s * T5_VOX + pj) * T5_TILE + pk;
         if (ph == 0) {
           *slot = make_float4(q.ux, q.uy, q.uz, 0.f);
           __syncwarp();
-          named_arrive(bid, 128);
+          named_arrive(bid, 32 * T5_PARTS);
         } else {
-          named_sync(bid, 128);
+          named_sync(bid, 32 * T5_PARTS);
           const float4 u4 = *slot;
           q.ux = u4.x, q.uy = u4.y, q.uz = u4.z, q.w = 0.f;
         }
