@@ -1583,13 +1583,13 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
                                                            model->zs, gate, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
   } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32 | FIF_BUILD_H16)) && model->zs_host != nullptr &&
-             ns <= 8 * T5_MAX_NG && bx + fabs(ax) <= 60.0) {
-    // (x = (ax zs) . u + bx <= bx + |ax| <= 60 keeps the paired sigmoid reciprocal finite)
+             ns <= 8 * T5_MAX_NG && bx + fabs(ax) <= T5_XMAX) {
+    // (x = (ax zs) . u + bx <= bx + |ax| <= T5_XMAX keeps the shared sigmoid reciprocal finite)
     // tcgen05 path: one tcgen05.mma (M=64, N=16 NG, K=16) per voxel per 16 landmarks, TMEM accumulators
     const int ng = (ns + 7) / 8;
     T5Z z{};
-    for (int sidx = 0; sidx < ns; ++sidx)  // sample s at slot s ^ 1 (pairs swapped: t5_sigmoids)
-      for (int c = 0; c < 3; ++c) z.z[c][sidx ^ 1] = (float)(ax * model->zs_host[3 * sidx + c]);
+    for (int sidx = 0; sidx < ns; ++sidx)  // (pair sigmoids: sample s at slot s ^ 1, see t5_sigmoids)
+      for (int c = 0; c < 3; ++c) z.z[c][T5_QUAD ? sidx : sidx ^ 1] = (float)(ax * model->zs_host[3 * sidx + c]);
     const unsigned blocks5 = (unsigned)((rows + T5_VOX - 1) / T5_VOX);
     int rc = FIF_OK;
 #define T5_CASE(NG)                                                                                         \

@@ -47,12 +47,25 @@ constexpr int T5_FLUSH = 8;         // FP32 accumulation span: 8 tiles = 512 lan
 #define T5_PARTS 2                  // sample parts per (voxel, landmark) pair: one thread each
 #endif
 constexpr int T5_PWARPS = T5_VOX * T5_PARTS * 2;  // producer warps: voxels x parts x 2 landmark halves
+// T5_DECOUPLE: the producer work is split by pipe.  The T5_PWARPS "sigmoid" warps compute
+// only the (MUFU-heavy) sigmoids; T5_EWARPS "entry" warps, thread = (voxel, landmark), run
+// one tile ahead: landmark load, the pair's bearing (handed to the sigmoid warps through a
+// 2-slot shared-memory ring), the 21 entries and their A-tile stores (no MUFU).  Sharing an
+// SM sub-partition, the two kinds overlap instead of meeting the XU pipe in lock step.
+#ifndef T5_DECOUPLE
+#define T5_DECOUPLE 0  // measured slower (139.3 vs 120.6 ms): DESIGN 8b
+#endif
+constexpr int T5_EWARPS = T5_DECOUPLE ? T5_VOX * 2 : 0;
 // warp roles after the producers: 3 epilogue warps whose warp % 4 = 0, 1, 2 (the TMEM
-// sub-partitions holding D rows 0-47) and one MMA warp
+// sub-partitions holding D rows 0-47) and one MMA warp, then the entry warps
 constexpr int T5_EPI0 = (T5_PWARPS % 4 == 0) ? T5_PWARPS : ((T5_PWARPS + 1 + 3) / 4) * 4;
 constexpr int T5_MMAW = (T5_PWARPS % 4 == 0) ? T5_PWARPS + 3 : T5_PWARPS;
-constexpr int T5_THREADS = (T5_EPI0 + 3 + (T5_MMAW > T5_EPI0 ? 1 : 0)) * 32;
+constexpr int T5_E0 = T5_EPI0 + 3 + (T5_MMAW > T5_EPI0 ? 1 : 0);  // first entry warp
+constexpr int T5_THREADS = (T5_E0 + T5_EWARPS) * 32;
 static_assert(T5_MMAW < T5_EPI0 || T5_MMAW == T5_EPI0 + 3, "warp roles");
+static_assert(!T5_DECOUPLE || T5_PARTS == 2, "decoupled producers: 2 sample parts");
+constexpr int T5_NFULL = (T5_PWARPS + T5_EWARPS + 1) * 32;  // stage-full named barrier: writers + MMA warp
+constexpr int T5_NU = (T5_PWARPS + T5_EWARPS) * 32;         // bearing-ring named barriers
 constexpr int T5_MAX_NG = 10;       // N_s <= 80
 constexpr int T5_BLK_A = 64 * 16 * 2;  // bytes per k-step of A (M = 64)
 
@@ -61,13 +74,15 @@ constexpr int T5_BAR_BYTES = 128;  // mbarriers, TMEM slot, scale bits (rounded 
 // ([stage][voxel][landmark] float4, after the barriers) and a named barrier per
 // (voxel, landmark half, stage): ids 1 + T5_STAGES ...
 #ifndef T5_SHARE_U
-#define T5_SHARE_U (T5_PARTS >= 4)  // part 0 computes each pair's bearing once for all parts
+#define T5_SHARE_U (T5_PARTS >= 4 && !T5_DECOUPLE)  // part 0 computes each pair's bearing once for all parts
 #endif
-constexpr int T5_USH_BYTES = T5_SHARE_U ? T5_STAGES * T5_VOX * T5_TILE * 16 : 0;
+static_assert(!(T5_SHARE_U && T5_DECOUPLE), "T5_SHARE_U and T5_DECOUPLE are exclusive");
+// bearing ring: [stage][voxel][landmark] float4 (SHARE_U: per pipeline stage; DECOUPLE: 2 slots)
+constexpr int T5_USH_BYTES = T5_SHARE_U ? T5_STAGES * T5_VOX * T5_TILE * 16 : T5_DECOUPLE ? 2 * T5_VOX * T5_TILE * 16 : 0;
 static_assert(1 + T5_STAGES + (T5_SHARE_U ? 2 * T5_VOX * T5_STAGES : 0) <= 16, "named barrier ids");
 constexpr int T5_SMEM_MAX = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 struct __align__(16) T5Z {
-  float z[3][8 * T5_MAX_NG];  // ax * zs[s ^ 1][c] (FP32; pairs swapped, see t5_sigmoids), 0 past N_s
+  float z[3][8 * T5_MAX_NG];  // ax * zs[s][c] (T5_QUAD; else zs[s ^ 1][c], pairs swapped), FP32, 0 past N_s
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -225,11 +240,84 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 __device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity, unsigned ns) {
   while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
+#ifndef T5_PROD_WAIT
+#define T5_PROD_WAIT 0  // producers' stage-empty wait: 0 = poll + T5_PROD_SLEEP ns, 1 = suspending try_wait, 2 = spin
+#endif
+__device__ __forceinline__ void t5_prod_wait(uint64_t* bar, uint32_t parity) {
+#if T5_PROD_WAIT == 1
+  mbar_wait_sleep(bar, parity);
+#elif T5_PROD_WAIT == 2
+  while (!mbar_try(bar, parity)) {
+  }
+#else
+  mbar_wait_poll(bar, parity, T5_PROD_SLEEP);
+#endif
+}
 // named barriers: the producers arrive (no wait) and the MMA warp blocks in hardware
 __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// T5_QUAD: one MUFU reciprocal per FOUR sigmoids.  With y_i = 2^-12 (1 + 2^x_i) (pairs
+// (y0, y2) and (y1, y3) from two FFMA2), (y01, y23) = (y0 y1, y2 y3) is one FMUL2, r =
+// 1 / (y01 y23), (a, b) = (y23 r, y01 r) one FMUL2, and the sigmoids 1 / y_i are
+// (y1 a, y3 b) = (s0, s2) and (y0 a, y2 b) = (s1, s3), two FMUL2: 5 issue slots and one
+// reciprocal per 4 samples instead of 4 and two (1.25 instead of 1.5 XU ops per sample).
+// The product of four y stays finite for x <= 42 (y <= 2^31); the host selects this
+// kernel only then.  Z holds the sample directions in order (no pair swap).
+#ifndef T5_QUAD
+#define T5_QUAD 0  // measured slower (123.0 vs 120.7 ms: the XU pipe is not what binds): DESIGN 8b
+#endif
+constexpr double T5_XMAX = T5_QUAD ? 42.0 : 60.0;  // host bound on bx + |ax|
+// FP16 hi + lo of four sigmoids held as the pairs (s0, s2) and (s1, s3): hi = truncated
+// (exact in FP16), lo = x - hi exact, residuals as two FADD2 on the pairs as they are
+__device__ __forceinline__ void t5_split4(f32x2 s02, f32x2 s13, uint32_t& h01, uint32_t& h23, uint32_t& l01,
+                                          uint32_t& l23) {
+  float s0, s1, s2, s3;
+  unpack2(s02, s0, s2);
+  unpack2(s13, s1, s3);
+  const float h0 = __uint_as_float(__float_as_uint(s0) & 0xFFFFE000u);
+  const float h1 = __uint_as_float(__float_as_uint(s1) & 0xFFFFE000u);
+  const float h2 = __uint_as_float(__float_as_uint(s2) & 0xFFFFE000u);
+  const float h3 = __uint_as_float(__float_as_uint(s3) & 0xFFFFE000u);
+  float d0, d1, d2, d3;
+  unpack2(fsub2(s02, pack2(h0, h2)), d0, d2);
+  unpack2(fsub2(s13, pack2(h1, h3)), d1, d3);
+  const __half2 a = __floats2half2_rn(h0, h1), b = __floats2half2_rn(h2, h3);
+  const __half2 c = __floats2half2_rn(d0, d1), d = __floats2half2_rn(d2, d3);
+  h01 = *reinterpret_cast<const uint32_t*>(&a);
+  h23 = *reinterpret_cast<const uint32_t*>(&b);
+  l01 = *reinterpret_cast<const uint32_t*>(&c);
+  l23 = *reinterpret_cast<const uint32_t*>(&d);
+}
 template <int NG, int G0, int G1>
 __device__ __forceinline__ void t5_sigmoids(const T5Z& Z, float ux, float uy, float uz, float bx, uint32_t bdst) {
+#if T5_QUAD
+#pragma unroll
+  for (int g = G0; g < G1; ++g) {
+    uint32_t hv[4], lv[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int s0 = 8 * g + 4 * q;
+      const f32x2 x01 = ffma2(splat2(ux), pack2(Z.z[0][s0], Z.z[0][s0 + 1]),
+                              ffma2(splat2(uy), pack2(Z.z[1][s0], Z.z[1][s0 + 1]),
+                                    ffma2(splat2(uz), pack2(Z.z[2][s0], Z.z[2][s0 + 1]), splat2(bx))));
+      const f32x2 x23 = ffma2(splat2(ux), pack2(Z.z[0][s0 + 2], Z.z[0][s0 + 3]),
+                              ffma2(splat2(uy), pack2(Z.z[1][s0 + 2], Z.z[1][s0 + 3]),
+                                    ffma2(splat2(uz), pack2(Z.z[2][s0 + 2], Z.z[2][s0 + 3]), splat2(bx))));
+      float x0, x1, x2, x3;
+      unpack2(x01, x0, x1);
+      unpack2(x23, x2, x3);
+      const f32x2 y02 = ffma2(pack2(ex2_approx(x0), ex2_approx(x2)), splat2(0x1p-12f), splat2(0x1p-12f));
+      const f32x2 y13 = ffma2(pack2(ex2_approx(x1), ex2_approx(x3)), splat2(0x1p-12f), splat2(0x1p-12f));
+      float p01, p23;
+      unpack2(fmul2(y02, y13), p01, p23);
+      const float r = rcp_approx(p01 * p23);
+      const f32x2 ab = fmul2(pack2(p23, p01), splat2(r));
+      t5_split4(fmul2(y13, ab), fmul2(y02, ab), hv[2 * q], hv[2 * q + 1], lv[2 * q], lv[2 * q + 1]);
+    }
+    sts128(bdst + g * 128, hv[0], hv[1], hv[2], hv[3]);
+    sts128(bdst + (NG + g) * 128, lv[0], lv[1], lv[2], lv[3]);
+  }
+#else
 #pragma unroll
   for (int g = G0; g < G1; ++g) {
     uint32_t hv[4], lv[4];
@@ -260,6 +348,7 @@ __device__ __forceinline__ void t5_sigmoids(const T5Z& Z, float ux, float uy, fl
     sts128(bdst + g * 128, hv[0], hv[1], hv[2], hv[3]);
     sts128(bdst + (NG + g) * 128, lv[0], lv[1], lv[2], lv[3]);
   }
+#endif
 }
 
 template <int NG, bool HAS_MASK>
@@ -426,7 +515,76 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   auto span_end = [&](int tt) { return (tt % T5_FLUSH) == T5_FLUSH - 1 || tt == ntiles - 1; };
   const uint32_t sbase = smem_u32(smem);
 
-  if (warp < T5_PWARPS) {
+  if (T5_DECOUPLE && warp < T5_PWARPS) {
+    // ───────────── sigmoid warps (decoupled producers) ─────────────
+    const uint32_t kofs_b = (pk >> 4) * BLK_B + ((pk >> 3) & 1) * (256 * NG) + (pk & 7) * 16;
+    for (int tt = 0; tt < ntiles; ++tt) {
+      const int s = tt % T5_STAGES, u = tt & 1;
+      named_sync(1 + T5_STAGES + u, T5_NU);  // the entry warps have written tile tt's bearings
+      const float4 u4 = ush[(u * T5_VOX + pj) * T5_TILE + pk];
+      named_arrive(3 + T5_STAGES + u, T5_NU);  // slot u may be refilled (tile tt + 2)
+      if (tt >= T5_STAGES) t5_prod_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
+      const uint32_t bdst = sbase + OFF_B + (s * T5_VOX + pj) * STAGE_B + kofs_b;
+      if (ph == 0)
+        t5_sigmoids<NG, 0, G1>(Z, u4.x, u4.y, u4.z, bx, bdst);
+      else
+        t5_sigmoids<NG, G1, NG>(Z, u4.x, u4.y, u4.z, bx, bdst);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      named_arrive(1 + s, T5_NFULL);  // stage s: this warp's B columns written
+    }
+  } else if (T5_DECOUPLE && warp >= T5_E0) {
+    // ───────────── entry warps: bearing, 21 entries, A tile (one tile ahead) ─────────────
+    const int ew = warp - T5_E0, ej = ew >> 1, ek = ((ew & 1) << 5) | lane;
+    const int64_t ev = vbase + ej;
+    const bool evok = ev < v1;
+    float ech[3], ecl[3];
+    voxel_split(src, evok ? ev : v0, ech, ecl);
+    const float inv_s2_s = inv_s2 * voxel_scale(ej);  // exact: a power of two
+    const uint32_t kofs_a = (ek >> 4) * T5_BLK_A + ((ek >> 3) & 1) * 1024 + (ek & 7) * 16;
+    float4 na = lm[2 * ek], nb = lm[2 * ek + 1];
+    for (int tt = 0; tt < ntiles; ++tt) {
+      const int s = tt % T5_STAGES, u = tt & 1;
+      const float4 a = na;
+      float4 b = nb;
+      if (tt + 1 < ntiles) {
+        const int64_t ni = (int64_t)(tt + 1) * T5_TILE + ek;
+        na = lm[2 * ni];
+        nb = lm[2 * ni + 1];
+      }
+      if (!evok) b.w = 0.f;
+      if (HAS_MASK && b.w != 0.f) {
+        const int64_t i = (int64_t)tt * T5_TILE + ek;
+        const bool keep = use_gbits ? ((gbits[ej * (n_pad >> 5) + (i >> 5)] >> (i & 31)) & 1u) != 0
+                                    : gate_keep(gate, ev, i);
+        if (!keep) b.w = 0.f;
+      }
+      const PairF q = pair_prologue(a, b, ech, ecl, inv_s2_s);  // w (and every entry) carries the voxel scale
+      if (tt >= 2) named_sync(3 + T5_STAGES + u, T5_NU);  // the sigmoid warps have read tile tt - 2
+      ush[(u * T5_VOX + ej) * T5_TILE + ek] = make_float4(q.ux, q.uy, q.uz, 0.f);
+      named_arrive(1 + T5_STAGES + u, T5_NU);
+      float e[24];
+      entries21(q, a, e);
+      e[21] = e[22] = e[23] = 0.f;
+      uint32_t hv[3][4], lv[3][4];
+#pragma unroll
+      for (int gi = 0; gi < 3; ++gi)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) t5_split2(e[8 * gi + 2 * p], e[8 * gi + 2 * p + 1], hv[gi][p], lv[gi][p]);
+      if (tt >= T5_STAGES) t5_prod_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
+      const uint32_t adst = sbase + (s * T5_VOX + ej) * STAGE_A + kofs_a;
+#pragma unroll
+      for (int gi = 0; gi < 3; ++gi) {
+        sts128(adst + (2 * gi) * 128, hv[gi][0], hv[gi][1], hv[gi][2], hv[gi][3]);
+        sts128(adst + (2 * gi + 1) * 128, lv[gi][0], lv[gi][1], lv[gi][2], lv[gi][3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      named_arrive(1 + s, T5_NFULL);  // stage s: this warp's A rows written
+    }
+    // consume the sigmoid warps' releases of the last two tiles (no barrier left half-arrived)
+    for (int tt = ntiles > 2 ? ntiles : 2; tt < ntiles + 2; ++tt) named_sync(3 + T5_STAGES + (tt & 1), T5_NU);
+  } else if (warp < T5_PWARPS) {
     // ───────────── producers ─────────────
     const float inv_s2_s = inv_s2 * voxel_scale(pj);  // exact: a power of two
     const uint32_t kofs_a = (pk >> 4) * T5_BLK_A + ((pk >> 3) & 1) * 1024 + (pk & 7) * 16;
@@ -450,7 +608,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       }
       PairF q;
       if (!T5_SHARE_U || ph == 0) q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
-      if (tt >= T5_STAGES) mbar_wait_poll(&empty[s], ((tt / T5_STAGES) - 1) & 1, T5_PROD_SLEEP);
+      if (tt >= T5_STAGES) t5_prod_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
       if (T5_SHARE_U) {  // part 0 hands its bearing to the other parts (the slot is free: its last
                             // readers finished the tile whose MMA freed this stage)
         const int bid = 1 + T5_STAGES + ((pj * 2 + (pk >> 5)) * T5_STAGES + s);
@@ -490,7 +648,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
 #if T5_NAMED
-      named_arrive(1 + s, (T5_PWARPS + 1) * 32);  // stage s written (the MMA warp syncs on it)
+      named_arrive(1 + s, T5_NFULL);  // stage s written (the MMA warp syncs on it)
 #else
       if (lane == 0) mbar_arrive(&full[s]);
 #endif
@@ -504,7 +662,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         const int k = tt / T5_FLUSH, b = k & 1;
         __syncwarp();
 #if T5_NAMED
-        named_sync(1 + s, (T5_PWARPS + 1) * 32);  // all 32 lanes (bar.sync is warp-aligned)
+        named_sync(1 + s, T5_NFULL);  // all 32 lanes (bar.sync is warp-aligned)
 #else
         mbar_wait_backoff(&full[s], (tt / T5_STAGES) & 1, T5_MMA_SLEEP);
 #endif
