@@ -371,12 +371,17 @@ def measure_e2e(args, F, FD, w2, grid, model, dev, stream, flush, world, rank, v
                 dist.barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            fld = F.Field.build(pts_host, grid, model, "info", device=dev, process_group=pg, replicate=False)
-            if export:
-                rows_dev = fld.export_reference()
-                host_out.copy_(rows_dev, non_blocking=True)
+            if export and world == 1:
+                # the reference's build returns host factors: z-slab chunks, each chunk's export
+                # and D2H overlapping the next chunk's build (Field.build(host_factors=True))
+                fld = F.Field.build(pts_host, grid, model, "info", device=dev, host_factors=True, host_out=host_out)
                 d2h = host_out.numel() * 8
             else:
+                fld = F.Field.build(pts_host, grid, model, "info", device=dev, process_group=pg, replicate=False)
+            if export and world > 1:
+                fld.export_reference_to(host_out)
+                d2h = host_out.numel() * 8
+            elif not export:
                 chk = fld.storage["f32"].sum(dtype=torch.float64).to("cpu", non_blocking=True)
                 d2h = 8
             b.record(stream)
@@ -392,8 +397,9 @@ def measure_e2e(args, F, FD, w2, grid, model, dev, stream, flush, world, rank, v
         tot_pairs = grid.voxel_count * w2.points.shape[0]
         res[export] = {"value": tot_pairs / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(pts_host.numel() * 8),
                        "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
-                       "path": ("Field.build(pinned host landmarks) -> device field -> export_reference (kinv @ S, "
-                                "reference layout FP64) -> D2H into pinned host memory" if export else
+                       "path": ("Field.build(pinned host landmarks, host_factors=True): z-slab chunks, each chunk's "
+                                "export_reference (kinv @ S, reference layout FP64) and D2H into pinned host memory "
+                                "overlapping the next chunk's build" if export else
                                 "Field.build(pinned host landmarks) -> device-resident field (the GPU queries' "
                                 "operand) -> D2H checksum")}
         del host_out

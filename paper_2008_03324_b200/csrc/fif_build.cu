@@ -1451,6 +1451,77 @@ __global__ void k_gp_apply_kinv(const double* __restrict__ S, int64_t rows, int 
   }
 }
 
+// Reference-layout export of GP rows (N_s <= 84): out = kinv @ S per voxel, expanded to the
+// reference's 36 entries per block in the same kernel (info) -- the GEMM kinv (N_s x N_s) x
+// [S_v0 | S_v1 | ...] over groups of voxels, FP64.  kinv is staged once per persistent CTA,
+// transposed (kT[g][k] = kinv[k][g]) so a thread's 28 consecutive k for one g are 14
+// broadcast LDS.128; thread = (column c = voxel-in-group x entry, k group of 28), 28 FP64
+// register accumulators, the same fma(kinv[k][g], S[g][e], acc) chain in g order as
+// k_gp_apply_kinv (bit-identical output).  Columns per CTA: 84 = 4 voxels x 21 (info) or
+// 84 voxels x 1 (trace).
+constexpr int GX_NC = 84, GX_KG = 28, GX_KS = 84;  // columns, k per thread group, kT row stride
+template <int W>
+__global__ void __launch_bounds__(256, 2) k_gp_export(const double* __restrict__ S, int64_t rows, int ns,
+                                                      const double* __restrict__ kinv, double* __restrict__ out) {
+  constexpr int VB = GX_NC / W;
+  extern __shared__ __align__(16) double gx_sm[];
+  double* kT = gx_sm;                   // [ns][GX_KS]
+  double* st = gx_sm + ns * GX_KS;      // [ns][GX_NC]
+  for (int i = threadIdx.x; i < ns * GX_KS; i += blockDim.x) {
+    const int g = i / GX_KS, k = i - g * GX_KS;
+    kT[i] = k < ns ? kinv[(int64_t)k * ns + g] : 0.0;
+  }
+  const int t = threadIdx.x, grp = t / GX_NC, c = t - grp * GX_NC, k0 = GX_KG * grp;
+  const int vb = c / W, e = c - vb * W;
+  int plo = 0, phi = 0;  // packed entry e -> (row, col) of the upper triangle
+  if (W == 21) {
+    int r = 0, rem = e;
+    while (rem >= 6 - r) rem -= 6 - r, ++r;
+    plo = r;
+    phi = r + rem;
+  }
+  const int64_t groups = (rows + VB - 1) / VB;
+  for (int64_t gi = blockIdx.x; gi < groups; gi += gridDim.x) {
+    const int64_t v0 = gi * VB;
+    const int nvb = (int)(rows - v0 < VB ? rows - v0 : VB);
+    __syncthreads();  // previous group's tile consumed (and kT written, first time)
+    for (int i = threadIdx.x; i < VB * ns * W; i += blockDim.x) {
+      const int b = i / (ns * W), r = i - b * (ns * W), g = r / W, ee = r - g * W;
+      st[g * GX_NC + b * W + ee] = b < nvb ? S[(v0 + b) * ns * W + r] : 0.0;
+    }
+    __syncthreads();
+    if (grp < 3 && k0 < ns && vb < nvb) {
+      double acc[GX_KG];
+#pragma unroll
+      for (int i = 0; i < GX_KG; ++i) acc[i] = 0.0;
+      for (int g = 0; g < ns; ++g) {
+        const double sv = st[g * GX_NC + c];
+        const double2* kp = reinterpret_cast<const double2*>(kT + g * GX_KS + k0);
+#pragma unroll
+        for (int i = 0; i < GX_KG / 2; ++i) {
+          const double2 kk = kp[i];
+          acc[2 * i] = fma(kk.x, sv, acc[2 * i]);
+          acc[2 * i + 1] = fma(kk.y, sv, acc[2 * i + 1]);
+        }
+      }
+      const int64_t v = v0 + vb;
+#pragma unroll
+      for (int i = 0; i < GX_KG; ++i) {
+        const int k = k0 + i;
+        if (k < ns) {
+          if (W == 21) {
+            double* o = out + (v * ns + k) * 36;
+            o[plo * 6 + phi] = acc[i];
+            if (plo != phi) o[phi * 6 + plo] = acc[i];
+          } else {
+            out[v * ns + k] = acc[i];
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace fif
 
 using namespace fif;
@@ -1752,6 +1823,26 @@ extern "C" int fif_export_reference(int factor_kind, const fif_model* model, con
   if (model->kind == FIF_MODEL_GP) {
     FIF_CHECK_ARG(model->kinv != nullptr, "fif_export_reference: GP model without kinv");
     const int W = trace ? 1 : 21;
+    if (nv <= GX_KS) {  // fused GEMM + expansion
+      const size_t smem = sizeof(double) * (size_t)nv * (GX_KS + GX_NC);
+      static std::atomic<uint64_t> gx_attr{0};
+      if (needs_setup(gx_attr)) {
+        cudaFuncSetAttribute(k_gp_export<21>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * GX_KS * (GX_KS + GX_NC)));
+        cudaFuncSetAttribute(k_gp_export<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * GX_KS * (GX_KS + GX_NC)));
+        mark_setup(gx_attr);
+      }
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t groups = (rows + GX_NC / W - 1) / (GX_NC / W);
+      const unsigned grid = (unsigned)std::min<int64_t>(groups, (int64_t)sms * 2);
+      if (trace)
+        k_gp_export<1><<<grid, 256, smem, st>>>(d_in64, rows, nv, model->kinv, d_out);
+      else
+        k_gp_export<21><<<grid, 256, smem, st>>>(d_in64, rows, nv, model->kinv, d_out);
+      FIF_CHECK_LAUNCH("k_gp_export");
+      return FIF_OK;
+    }
     double* dst = d_out;
     if (!trace) {
       if (cudaMallocAsync(&tmp, sizeof(double) * rows * nv * 21, st) != cudaSuccess) {

@@ -353,20 +353,26 @@ _GP_INFO_FLAGS = {"t5": 0, "h16": _lib.BUILD_H16, "tf32": _lib.BUILD_TF32, "simt
 def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, device: torch.device, grid=None,
                centers: torch.Tensor | None = None, v_begin: int = 0, v_end: int | None = None,
                mask: torch.Tensor | None = None, dmodel: _DeviceModel | None = None, f32_copy: bool = True,
-               exact: bool = False):
+               exact: bool = False, out64: torch.Tensor | None = None, out32: torch.Tensor | None = None,
+               scratch: torch.Tensor | None = None):
     """One fif_build launch: rows [v_begin, v_end) of the z-major grid (or of `centers`).
-    Returns (f64 rows (R, width_packed), f32 copy or None)."""
+    Returns (f64 rows (R, width_packed), f32 copy or None); out64 / out32 (contiguous row
+    ranges of a larger field) receive the rows when given."""
     dm = dmodel or _DeviceModel(model, device)
     n_v = 10 if isinstance(model, QuadraticVisibility) else model.n_v
     width = n_v if want_trace else n_v * 21
     if v_end is None:
         v_end = centers.shape[0] if centers is not None else int(np.prod(grid.dims))
     rows = v_end - v_begin
-    out64 = torch.empty((rows, width), dtype=torch.float64, device=device)
     gp = isinstance(model, GpVisibility)
-    out32 = torch.empty((rows, width), dtype=torch.float32, device=device) if (gp and f32_copy) else None
+    if out64 is None:
+        out64 = torch.empty((rows, width), dtype=torch.float64, device=device)
+        out32 = torch.empty((rows, width), dtype=torch.float32, device=device) if (gp and f32_copy) else None
+    assert out64.shape == (rows, width) and out64.is_contiguous()
+    assert out32 is None or (out32.shape == (rows, width) and out32.is_contiguous())
     n = points.shape[0]
-    scratch = torch.empty(int(_lib.load().fif_build_scratch_bytes(n)), dtype=torch.uint8, device=device)
+    if scratch is None:
+        scratch = torch.empty(int(_lib.load().fif_build_scratch_bytes(n)), dtype=torch.uint8, device=device)
     g = _lib.make_grid(grid.origin, grid.voxel_size, grid.dims) if grid is not None else None
     kind = _lib.KIND_TRACE if want_trace else _lib.KIND_INFO
     with torch.cuda.device(device):  # the library launches on the current device
@@ -400,6 +406,82 @@ def build_matched_rows(points: torch.Tensor, model, want_trace: bool, sigma: flo
                                                  _lib.ptr(scratch), _lib.ptr(out64), _lib.ptr(out32),
                                                  _device.stream_handle(device)), "fif_build_matched")
     return out64, out32
+
+
+def _host_rows(host_out, rows: int, width: int) -> torch.Tensor:
+    if host_out is None:
+        return torch.empty((rows, width), dtype=torch.float64).pin_memory()
+    if tuple(host_out.shape) != (rows, width) or host_out.dtype != torch.float64 or host_out.is_cuda:
+        raise ValueError(f"host_out must be a host float64 tensor of shape ({rows}, {width})")
+    return host_out
+
+
+def _export_chunks(field: "Field", host_out: torch.Tensor, chunks, before_export=None) -> None:
+    """Export each row range of `chunks` (device staging, two buffers) and copy it to
+    host_out on a side stream; before_export(i) runs on the compute stream first (the
+    pipelined build launches chunk i's rows there)."""
+    dev = field.device
+    if not chunks:
+        if before_export is not None:
+            before_export(-1)
+        return
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(device=dev)
+    cmax = max(b - a for a, b in chunks)
+    stage = [torch.empty((cmax, field.row_width), dtype=torch.float64, device=dev) for _ in range(2)]
+    freed = [None, None]
+    with torch.cuda.device(dev):
+        for i, (a, b) in enumerate(chunks):
+            if before_export is not None:
+                before_export(i)
+            buf = stage[i & 1]
+            if freed[i & 1] is not None:
+                comp.wait_event(freed[i & 1])  # the D2H of chunk i - 2 has drained this buffer
+            field._export_range(a, b, buf)
+            ready = torch.cuda.Event()
+            ready.record(comp)
+            copy.wait_event(ready)
+            with torch.cuda.stream(copy):
+                host_out[a:b].copy_(buf[: b - a], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(copy)
+            freed[i & 1] = done
+        comp.wait_stream(copy)
+        for t in stage:
+            t.record_stream(copy)
+
+
+# z-slab row chunks of a host_factors build (chunk i's export + D2H overlap chunk i + 1's build)
+HOST_EXPORT_CHUNKS = 8
+
+
+def _build_to_host(pts_dev, config, model, factor_kind, sigma, dev, exact, host_out) -> "Field":
+    """Dense build in z-slab row chunks; chunk i's export + D2H overlap chunk i + 1's build
+    (a voxel's rows do not depend on the chunking: fixed flush spans)."""
+    want_trace = factor_kind == "trace"
+    n_v = model.n_v
+    width = n_v if want_trace else n_v * 21
+    rows = config.voxel_count
+    gp = isinstance(model, GpVisibility)
+    s64 = torch.empty((rows, width), dtype=torch.float64, device=dev)
+    s32 = torch.empty((rows, width), dtype=torch.float32, device=dev) if gp else None
+    fld = Field(config, model, factor_kind, sigma, s64, s32, None, ALWAYS_MATCH, dense=True)
+    host_out = _host_rows(host_out, rows, fld.row_width)
+    per = -(-rows // max(1, HOST_EXPORT_CHUNKS))
+    chunks = [(a, min(rows, a + per)) for a in range(0, rows, per)]
+    scratch = torch.empty(int(_lib.load().fif_build_scratch_bytes(pts_dev.shape[0])), dtype=torch.uint8, device=dev)
+
+    def build_chunk(i):
+        if i < 0:
+            return
+        a, b = chunks[i]
+        build_rows(pts_dev, model, want_trace, sigma, dev, grid=config, v_begin=a, v_end=b, dmodel=fld._dm,
+                   exact=exact, out64=s64[a:b], out32=None if s32 is None else s32[a:b], scratch=scratch)
+
+    _export_chunks(fld, host_out, chunks, build_chunk)
+    torch.cuda.current_stream(dev).synchronize()  # the host factors are complete on return
+    fld._ref_cache = host_out.numpy()
+    return fld
 
 
 def device_centers(config: GridConfig, device: torch.device, order: int = 0) -> torch.Tensor:
@@ -478,6 +560,16 @@ class Field:
             self._ref_cache = _device.to_numpy(self.export_reference())
         return self._ref_cache
 
+    def export_reference_to(self, host_out: torch.Tensor | None = None, chunk_rows: int = 1 << 14) -> np.ndarray:
+        """All reference-layout rows into (pinned) host memory, chunk by chunk: the export
+        kernel of chunk i + 1 overlaps the D2H copy of chunk i (a side copy stream, two
+        device staging buffers).  Returns the host rows (also cached as `factors`)."""
+        host_out = _host_rows(host_out, self.rows, self.row_width)
+        _export_chunks(self, host_out, [(a, min(self.rows, a + chunk_rows)) for a in range(0, self.rows, chunk_rows)])
+        torch.cuda.current_stream(self.device).synchronize()  # the host rows are complete on return
+        self._ref_cache = host_out.numpy()
+        return self._ref_cache
+
     def export_reference(self, rows: torch.Tensor | np.ndarray | None = None) -> torch.Tensor:
         """Device tensor of reference-layout rows (all, or the given row indices)."""
         src = self._s64 if rows is None else self._s64[torch.as_tensor(rows, device=self.device, dtype=torch.long)]
@@ -489,6 +581,13 @@ class Field:
                                                         _device.stream_handle(self.device)), "fif_export_reference")
         return out
 
+    def _export_range(self, a: int, b: int, out: torch.Tensor) -> None:
+        kind = _lib.KIND_INFO if self._is_info else _lib.KIND_TRACE
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().fif_export_reference(kind, self._dm.c, _lib.ptr(self._s64[a:b]), b - a,
+                                                        _lib.ptr(out), _device.stream_handle(self.device)),
+                       "fif_export_reference")
+
     @property
     def storage(self) -> dict:
         return {"f64": self._s64, "f32": self._s32}
@@ -497,13 +596,18 @@ class Field:
     @staticmethod
     def build(landmarks, config, model, factor_kind: str = "info", matchability: Matchability = ALWAYS_MATCH,
               sigma: float = DEFAULT_SIGMA, parallel: bool = False, device=None, exact: bool = False,
-              process_group=None, replicate: bool = True) -> "Field":
+              process_group=None, replicate: bool = True, host_factors: bool = False,
+              host_out: torch.Tensor | None = None) -> "Field":
         """Build every voxel's factor on the GPU.  `parallel` is accepted for API
         compatibility (the GPU build is always parallel).  exact=True (quad model)
         reproduces the reference's FP64 operation order bit for bit.  With a torch.distributed
         `process_group` (one rank per GPU; the default group when it is the WORLD) the grid
         is built as z-slabs across the ranks (parallel.build_field): replicate=True returns the
-        whole field on every rank, replicate=False this rank's slab."""
+        whole field on every rank, replicate=False this rank's slab.
+        host_factors=True also hands back what the reference's build returns, the
+        reference-layout FP64 `factors` in host memory: the grid is built in z-slab chunks
+        and each chunk's export and D2H copy overlap the build of the next (`host_out`: an
+        optional pinned (rows, row_width) float64 buffer to fill)."""
         if process_group is not None:
             import torch.distributed as dist
 
@@ -532,6 +636,8 @@ class Field:
             return Field(config, model, factor_kind, sigma, empty64, empty64.float() if gp else None,
                          np.zeros((0, 3), np.int32), matchability, dense=False)
         pts_dev = _device.to_device_f64(points, dev, (3,))
+        if matchability.is_trivial and host_factors:
+            return _build_to_host(pts_dev, config, model, factor_kind, sigma, dev, exact, host_out)
         if matchability.is_trivial:
             s64, s32 = build_rows(pts_dev, model, want_trace, sigma, dev, grid=config, exact=exact)
             return Field(config, model, factor_kind, sigma, s64, s32, None, matchability, dense=True)

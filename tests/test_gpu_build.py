@@ -290,3 +290,26 @@ def test_sharp_sigmoids_stay_finite(oracle, g_small, models, small_grid, k_s, gp
         ref = oracle_field(oracle, m, cen, pts, kind)
         err = trace_rel_l2(mine, ref) if kind == "trace" else info_rel_fro(mine, ref)
         assert err.max() <= (TRACE_TOL if kind == "trace" else INFO_TOL), (kind, err.max())
+
+
+@pytest.mark.parametrize("mname,kind", [("gp30", "info"), ("gp70", "info"), ("quad", "info"), ("gp70", "trace")])
+def test_build_host_factors_pipelined(models, mname, kind):
+    """Field.build(host_factors=True): z-slab chunks whose export + D2H overlap the next
+    chunk's build return the same host factors (bit for bit) and device rows as the
+    one-launch build followed by export_reference; export_reference_to likewise."""
+    from paper_2008_03324_b200 import scenes as SC
+
+    w = SC.config1(0)
+    grid = F.GridConfig(*w.grid)
+    model = models[mname] if mname in models else F.build_gp_model(int(mname[2:]))
+    ref = F.Field.build(w.points, grid, model, kind)
+    want = ref.export_reference().cpu().numpy()
+    got = F.Field.build(w.points, grid, model, kind, host_factors=True)
+    assert got.factors.shape == want.shape and np.array_equal(got.factors, want)
+    assert torch.equal(got.storage["f64"], ref.storage["f64"])
+    host = torch.empty(want.shape, dtype=torch.float64).pin_memory()
+    again = F.Field.build(w.points, grid, model, kind, host_factors=True, host_out=host)
+    assert np.array_equal(host.numpy(), want) and again.factors.ctypes.data == host.numpy().ctypes.data
+    assert np.array_equal(ref.export_reference_to(chunk_rows=777), want)
+    with pytest.raises(ValueError):
+        F.Field.build(w.points, grid, model, kind, host_factors=True, host_out=torch.empty((3, 3), dtype=torch.float64))
