@@ -14,6 +14,7 @@
 // GP trace evaluates the sigmoid's cosine in FP64 (FP64 pipe is otherwise idle)
 // because the kinv epilogue amplifies S errors ~200x.
 #include <cstdarg>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 
@@ -1422,6 +1423,7 @@ k_gp_info_h16(const float4* __restrict__ lm, int64_t n_pad, int64_t n_real, VoxS
 }
 
 #include "fif_gp_t5.cuh"
+#include "fif_gp_t6.cuh"
 
 // ─────────────────────────── exports ───────────────────────────────────
 // Expand packed (rows, nv, 21) to the reference's (rows, nv*36).
@@ -1653,6 +1655,47 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
       k_gp_trace<false><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns,
                                                            model->zs, gate, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
+  } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32 | FIF_BUILD_H16 | FIF_BUILD_T5)) &&
+             model->zs_host != nullptr && !has_mask && ns > 8 && ns <= 8 * T6_MAX_NG && bx + fabs(ax) <= T5_XMAX &&
+             fabs(ax) <= 100.0 && fabs(bx - 12.0) <= 100.0 && !T5_QUAD) {
+    // tcgen05 path with the exponent arguments x' = (ax zs) . u on the tensor cores as well (one
+    // M=128 K=16 MMA per voxel per 64 landmarks) and the bias folded into the sigmoid:
+    // 2^-12 (1 + 2^(x' + bx)) = fma(2^x', 2^(bx - 12), 2^-12); |ax| <= 100 keeps 2^x' finite
+    const int ng = (ns + 7) / 8;
+    T6Z z;
+    t6_fill_z(z, model->zs_host, ns, ax, (8 * ng + 15) / 16 * 16);
+    const float cexp = (float)exp2(bx - 12.0);
+    const unsigned blocks6 = (unsigned)((rows + T5_VOX - 1) / T5_VOX);
+    int rc = FIF_OK;
+#define T6_LAUNCH(NG, SKIP)                                                                                  \
+  do {                                                                                                       \
+    constexpr int sm = T6Layout<NG>::BYTES;                                                                  \
+    static_assert(sm <= T5_SMEM_MAX, "k_gp_info_t6 shared memory");                                          \
+    static std::atomic<uint64_t> attr{0};                                                                    \
+    if (needs_setup(attr)) {                                                                                 \
+      cudaFuncSetAttribute(k_gp_info_t6<NG, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);         \
+      mark_setup(attr);                                                                                      \
+    }                                                                                                        \
+    k_gp_info_t6<NG, SKIP><<<blocks6, T5_THREADS, sm, st>>>(lm, n_pad, src, v_begin, v_end, ns, (float)inv_s2, \
+                                                            cexp, z, d_out64, d_out32);                      \
+  } while (0)
+  // (one trailing sample pair of padding, N_s <= 8 NG - 2, is skipped at compile time: N_s = 70)
+#define T6_CASE(NG)                              \
+  case NG:                                       \
+    if (ns <= 8 * NG - 2) T6_LAUNCH(NG, 1);      \
+    else T6_LAUNCH(NG, 0);                       \
+    break;
+    switch (ng) {
+      T6_CASE(2) T6_CASE(3) T6_CASE(4) T6_CASE(5) T6_CASE(6) T6_CASE(7) T6_CASE(8) T6_CASE(9)
+      default: rc = FIF_ERR_UNSUPPORTED;
+    }
+#undef T6_LAUNCH
+#undef T6_CASE
+    if (rc != FIF_OK) {
+      set_error("fif_build: N_s=%d unsupported by k_gp_info_t6", ns);
+      return rc;
+    }
+    FIF_CHECK_LAUNCH("k_gp_info_t6");
   } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32 | FIF_BUILD_H16)) && model->zs_host != nullptr &&
              ns <= 8 * T5_MAX_NG && bx + fabs(ax) <= T5_XMAX) {
     // (x = (ax zs) . u + bx <= bx + |ax| <= T5_XMAX keeps the shared sigmoid reciprocal finite)

@@ -346,8 +346,9 @@ _MASK_CHUNK_BYTES = 1 << 30
 # GP info kernel: "t5" (default; tcgen05.mma FP16 split with TMEM accumulators, N_s <= 80,
 # other N_s run "h16"), "h16" (mma.sync FP16 split, k16 per MMA), "tf32" (mma.sync TF32x3)
 # or "simt" (FP32 FFMA2); the alternatives are kept as cross-checks.
-GP_INFO_KERNEL = "t5"
-_GP_INFO_FLAGS = {"t5": 0, "h16": _lib.BUILD_H16, "tf32": _lib.BUILD_TF32, "simt": _lib.BUILD_SIMT}
+GP_INFO_KERNEL = "t6"
+_GP_INFO_FLAGS = {"t6": 0, "t5": _lib.BUILD_T5, "h16": _lib.BUILD_H16, "tf32": _lib.BUILD_TF32,
+                  "simt": _lib.BUILD_SIMT}
 
 
 def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, device: torch.device, grid=None,

@@ -1,4 +1,4 @@
-"""Config-2 GP-info build: tcgen05 kernel (t5) vs the mma.sync kernel (h16), timing and
+"""Config-2 GP-info build: tcgen05 kernels (t6, t5) vs the mma.sync kernel (h16), timing and
 precision against the C oracle on sampled voxels.  Usage: python tools/t5_probe.py [ns]"""
 import os
 import sys
@@ -40,7 +40,8 @@ sample = np.sort(rng.choice(V, 300, replace=False))
 cz = grid.centers()  # x-major reference order
 ref_rows = None
 res = {}
-for kern in ("t5", "h16"):
+KERNELS = tuple(os.environ.get("KERNELS", "t6,t5,h16").split(","))
+for kern in KERNELS:
     FD.GP_INFO_KERNEL = kern
     out = {}
 
@@ -63,5 +64,6 @@ for kern, r64 in res.items():
     refp = refp[:, :, iu[0], iu[1]].reshape(len(sample), -1)
     err = np.abs(mine - refp).max(1) / np.linalg.norm(refp, axis=1)
     print(f"{kern}: S max-entry / voxel-Frobenius over {len(sample)} voxels: max {err.max():.3e} median {np.median(err):.3e}")
-d = (res["t5"] - res["h16"]).abs().max().item() / res["h16"].abs().max().item()
-print(f"t5 vs h16 max abs diff / max: {d:.3e}")
+for kern in KERNELS[:-1]:
+    d = (res[kern] - res[KERNELS[-1]]).abs().max().item() / res[KERNELS[-1]].abs().max().item()
+    print(f"{kern} vs {KERNELS[-1]} max abs diff / max: {d:.3e}")
