@@ -54,8 +54,9 @@ extern "C" {
 #define FIF_BUILD_SIMT 2u   /* GP info: FP32 SIMT (FFMA2) kernel instead of the tensor-pipe kernel   */
 #define FIF_BUILD_TF32 4u   /* GP info: TF32x3 mma.sync kernel instead of the default tcgen05 one       */
 #define FIF_BUILD_H16 8u    /* GP info: FP16-split mma.sync kernel instead of the default tcgen05 one  */
-#define FIF_BUILD_T5 16u    /* GP info: k_gp_info_t5 (exponent arguments on the FMA pipe) instead of
-                               the default k_gp_info_t6 (exponent arguments on the tensor cores too) */
+#define FIF_BUILD_T6 16u    /* GP info: k_gp_info_t6 (sigmoid exponent arguments on the tensor cores as well;
+                               unmasked builds with 9 <= N_s <= 72, else the default kernel; measured slower
+                               than the default k_gp_info_t5: DESIGN 8b) */
 
 /* Axis-aligned voxel grid (field.py:45-98 GridConfig). */
 typedef struct fif_grid {

@@ -23,7 +23,7 @@ BUILD_EXACT = 1
 BUILD_SIMT = 2
 BUILD_TF32 = 4
 BUILD_H16 = 8
-BUILD_T5 = 16
+BUILD_T6 = 16
 METRIC_IDS = {"det": 0, "lmin": 1, "trace": 2}  # kernels.metric_id (kernels.py:602-608)
 
 EXPORTED = (

@@ -1655,7 +1655,7 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
       k_gp_trace<false><<<blocks_t, threads_t, smem, st>>>(d_points, n_points, src, v_begin, v_end, vbt, ns,
                                                            model->zs, gate, inv_s2, ax, bx, d_out64, d_out32);
     FIF_CHECK_LAUNCH("k_gp_trace");
-  } else if (!(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32 | FIF_BUILD_H16 | FIF_BUILD_T5)) &&
+  } else if ((build_flags & FIF_BUILD_T6) && !(build_flags & (FIF_BUILD_SIMT | FIF_BUILD_TF32 | FIF_BUILD_H16)) &&
              model->zs_host != nullptr && !has_mask && ns > 8 && ns <= 8 * T6_MAX_NG && bx + fabs(ax) <= T5_XMAX &&
              fabs(ax) <= 100.0 && fabs(bx - 12.0) <= 100.0 && !T5_QUAD) {
     // tcgen05 path with the exponent arguments x' = (ax zs) . u on the tensor cores as well (one

@@ -1,9 +1,10 @@
 // fif_gp_t6.cuh — GP info build on tcgen05 with the sigmoid exponent arguments ALSO on the
-// tensor cores.  Included by fif_build.cu after fif_gp_t5.cuh (shares its helpers).
+// tensor cores (FIF_BUILD_T6; a measured alternative to the default k_gp_info_t5, see the
+// result at the end).  Included by fif_build.cu after fif_gp_t5.cuh (shares its helpers).
 //
 // k_gp_info_t5 spends, per (pair, sample), 1.5 FFMA2 + a constant-bank load on the exponent
 // argument x = (ax z_s) . u + bx and computes every pair's bearing twice (once per sample
-// part): ~20 % of its issue slots, and it is issue-bound (70 % busy, XU 62 %).  Here
+// part): ~20 % of its issue slots.  Here
 //   X[l][s] = sum_c u_c(l) (ax z_s)_c                    (landmarks x 3) x (3 x samples)
 // is one more tcgen05.mma per (voxel, 64-landmark tile): kind::f16, M = 128, N = 16-aligned
 // 8 NG, K = 16, FP32 accumulate.  The K = 16 slots carry the FP16 splits u = uh + ul (22
@@ -12,32 +13,48 @@
 //   2^-12 (1 + 2^(x' + bx)) = fma(2^x', 2^(bx - 12), 2^-12).
 // Rows: A_x row 32 sp + lane belongs to the producer thread of TMEM sub-partition sp, so the
 // 64 landmarks of a tile appear twice (once per sample part) and each thread reads ITS x
-// values with one 32x32b tcgen05.ld of its own lane (32-48 columns) — no FFMA2, no constant
-// loads.  The pair's bearing for tile t + 1 is computed during tile t (after the X loads of
-// tile t are in registers), written K-major into the single A_x slot, and the MMA warp
-// issues X(t + 1) behind the S MMAs of tile t - 1; X(t + 1) has landed long before it is
-// read (one tile of slack), so X needs no double buffer.
+// values with one 32x32b tcgen05.ld of its own lane (32-40 columns) — no FFMA2, no constant
+// loads.  The pair's bearing for tile t + 1 is computed during tile t (while the X loads of
+// tile t are in flight), written K-major into the voxel's single A_x slot, and the MMA thread
+// issues X(t + 1) once the voxel's four warps have X(t) in registers.
 //
-// TMEM (512 columns): S accumulators 3 x XN, X 3 x XN (XN = 80 at N_s = 70).  To fit, the S
-// product drops the separate hi/lo sample columns of k_gp_info_t5: per k-step TWO N = 8 NG
-// MMAs accumulate into the same 48 D rows,
+// TMEM (512 columns): S accumulators 3 x XN, X 3 x XN (XN = 80 at N_s = 70): X cannot be
+// double-buffered.  To fit even that, the S product drops the separate hi/lo sample columns of
+// k_gp_info_t5: per k-step TWO N = 8 NG MMAs accumulate into the same 48 D rows,
 //   [E_lo; E_hi; 0] x vs_hi  and  [E_hi; 0; ...] x vs_lo
 // (A tile K-group = [lo0 lo1 lo2 hi0 hi1 hi2 Z Z Z] x 128 B; the second MMA's descriptor
 // starts at hi0, so its rows 24-47 read the zero groups and rows 48-63, never read back,
 // run into the next K-group), i.e. rows 0-23 = E_lo vs_hi + E_hi vs_lo, rows 24-47 = E_hi
-// vs_hi (lo x lo, <= 2^-22 relative, is dropped as in k_gp_info_h16).  The epilogue adds the
-// two row sets into the same FP64 sums in two phases separated by a named barrier.
-// Everything else (3 voxels per CTA, 64-landmark stages, 12 producer warps, lane-offset TMEM
-// double buffering of the S spans, FP16 hi + lo by truncation, one reciprocal per pair of
-// sigmoids, aligned 512-landmark FP32 spans) is k_gp_info_t5's.
+// vs_hi (lo x lo, <= 2^-22 relative, is dropped as in k_gp_info_h16).  The two rows of an
+// entry sit in different epilogue warps; the warps walk the voxels in rotated order so that
+// no FP64 cell has two writers at a time.
+// Every voxel is its own pipeline (own stages, mbarriers, X and S columns); one elected
+// thread polls the barriers and issues all MMAs (descriptors = loop-invariant low word +
+// constant, ~3 instructions per MMA).  3 voxels per CTA, 64-landmark stages, 12 producer
+// warps, lane-offset TMEM double buffering of the S spans, FP16 hi + lo by truncation, one
+// reciprocal per pair of sigmoids and aligned 512-landmark FP32 spans are k_gp_info_t5's.
+//
+// Result (config 2, GP-70, B200): same precision as t5 (max-entry / voxel-Frobenius 1.15e-6
+// vs 1.08e-6), 17 % fewer warp instructions, the sigmoid phase XU-saturated (1 220 cycles
+// per tile vs ~2 200), but 135.4 ms vs 120.6 ms: with one X buffer the chain "X(t) read ->
+// A_x(t + 1) -> barrier -> MMA thread -> in-order tensor queue -> X(t + 1) landed" (plus its
+// extra proxy fences) is exposed once per tile, and the producers wait ~20 % of their time
+// for X (profiles/r02_t6_*.txt, DESIGN 8b).
 #pragma once
 // (included inside namespace fif)
+
+#ifndef T6_DEBUG
+#define T6_DEBUG 0  // waits report their state and trap when nothing happens for a long time
+#endif
 
 #ifndef T6_G1_N
 #define T6_G1_N 1
 #define T6_G1_D 2
 #endif
 #define T6_G1(NG) ((NG) * T6_G1_N / T6_G1_D)  // sample groups of part 0 (which also computes the 21 entries)
+#ifndef T6_X_FIRST
+#define T6_X_FIRST 1
+#endif
 #ifndef T6_PROBE
 #define T6_PROBE 0  // timing probes (wrong results): 1 = no second S MMA, 2 = no FP64 adds in the epilogue,
                     // 3 = producers do not wait for X, 4 = empty epilogue, 5 = no S MMAs
@@ -47,8 +64,11 @@ constexpr int T6_BLK_A = 2 * T6_KG_A;   // bytes per k-step of A
 constexpr int T6_AX_BYTES = 128 * 32;   // A_x per voxel: 128 rows x K = 16 halves, K-major
 constexpr int T6_MAX_NG = 9;            // shared memory: N_s <= 72
 constexpr int T6_XN_MAX = 80;
-constexpr int T6_AXBAR = 1 + T5_STAGES; // named barrier: x(t) in registers, A_x(t + 1) written
-constexpr int T6_EPIBAR = 2 + T5_STAGES;
+constexpr int T6_EPIBAR = 1;            // named barrier of the three epilogue warps
+constexpr int T6_BAR_BYTES = 384;       // 30 mbarriers, TMEM slot, scale bits
+#ifndef T6_STAGGER_NS
+#define T6_STAGGER_NS 300  // start delay of voxel j's producers: j x this (de-phases the voxels' pipelines)
+#endif
 static_assert(T5_VOX == 3 && T5_PARTS == 2 && T5_STAGES == 2 && !T5_DECOUPLE && T5_PWARPS == 12,
               "k_gp_info_t6 is written for 3 voxels x 2 sample parts x 2 stages");
 
@@ -152,6 +172,22 @@ __device__ __forceinline__ float rcp_approx_v(float x) {
   asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// spin on an mbarrier phase; T6_DEBUG: report and trap instead of hanging
+__device__ __forceinline__ void t6_spin(uint64_t* bar, uint32_t parity, int tag, int a, int b) {
+#if T6_DEBUG
+  long long n = 0;
+  while (!mbar_try(bar, parity)) {
+    if (++n > 20000000) {
+      if ((threadIdx.x & 31) == 0) printf("t6 stuck tag %d block %d warp %d: %d %d\n", tag, blockIdx.x, threadIdx.x >> 5, a, b);
+      __trap();
+    }
+  }
+#else
+  (void)tag, (void)a, (void)b;
+  while (!mbar_try(bar, parity)) {
+  }
+#endif
+}
 #ifndef T6_PIPE
 #define T6_PIPE 1
 #endif
@@ -228,7 +264,7 @@ struct T6Layout {
   static constexpr int OFF_ACC = OFF_B + T5_STAGES * T5_VOX * STAGE_B;
   static constexpr int ACC_V = NCOL * 21;                // doubles per voxel
   static constexpr int OFF_BAR = OFF_ACC + T5_VOX * ACC_V * 8;
-  static constexpr int OFF_AX = OFF_BAR + T5_BAR_BYTES;
+  static constexpr int OFF_AX = OFF_BAR + T6_BAR_BYTES;
   static constexpr int OFF_BX = OFF_AX + T5_VOX * T6_AX_BYTES;
   static constexpr int BYTES = OFF_BX + XN * 32;
   static constexpr int XBASE = T5_VOX * XN;              // first X column
@@ -248,11 +284,15 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   static_assert(G1 >= 1 && G1 < NG, "both sample parts need at least one group");
   extern __shared__ __align__(1024) unsigned char smem[];
   double* acc = reinterpret_cast<double*>(smem + OFF_ACC);
-  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + OFF_BAR);  // [2] stage consumed by the S MMAs
-  uint64_t* ffull = empty + T5_STAGES;                            // [2] accumulator buffer b holds a finished span
-  uint64_t* fempty = ffull + 2;                                   // [2] the epilogue has drained buffer b
-  uint64_t* xfull = fempty + 2;                                   // X(t) has landed in TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
+  // Every voxel of the CTA is its own pipeline (4 producer warps, its stages, its X and S
+  // columns) with its own mbarriers, [voxel][stage / buffer]; the MMA thread polls them:
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);  // [3][2] stage written by the voxel's 4 warps
+  uint64_t* empty = full + T5_VOX * 2;                           // [3][2] stage consumed by the S MMAs
+  uint64_t* ffull = empty + T5_VOX * 2;                          // [3][2] accumulator buffer b holds a finished span
+  uint64_t* fempty = ffull + T5_VOX * 2;                         // [3][2] the epilogue has drained buffer b
+  uint64_t* axr = fempty + T5_VOX * 2;                           // [3] X(t - 1) read and A_x(t) written by the 4 warps
+  uint64_t* xfull = axr + T5_VOX;                                // [3] X(t) has landed in TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + T5_VOX);
   int* sbits = reinterpret_cast<int*>(tmem_slot + 1);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int64_t vbase = v0 + (int64_t)blockIdx.x * T5_VOX;
@@ -267,12 +307,16 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   }
   if (t < T5_VOX) sbits[t] = 0;
   if (t == 0) {
-    for (int s = 0; s < T5_STAGES; ++s) mbar_init(&empty[s], 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&ffull[b], 1);
-      mbar_init(&fempty[b], 3);
+    for (int i = 0; i < T5_VOX * 2; ++i) {
+      mbar_init(&full[i], 4);
+      mbar_init(&empty[i], 1);
+      mbar_init(&ffull[i], 1);
+      mbar_init(&fempty[i], 3);
     }
-    mbar_init(xfull, 1);
+    for (int j = 0; j < T5_VOX; ++j) {
+      mbar_init(&axr[j], 4);
+      mbar_init(&xfull[j], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros and B_x visible to the tensor core
@@ -378,8 +422,9 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       store_ax(q_cur);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      named_arrive(T6_AXBAR, T5_NFULL);
+      if (lane == 0) mbar_arrive(&axr[pj]);
     }
+    if (T6_STAGGER_NS > 0 && pj > 0) __nanosleep(pj * T6_STAGGER_NS);
     float4 na = a_cur, nb = make_float4(0.f, 0.f, 0.f, 0.f);
     if (ntiles > 1) {
       na = lm[2 * (T5_TILE + pk)];
@@ -390,9 +435,7 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       // this thread's exponent arguments of tile tt: one row of X(tt) (landed during tile tt - 1)
       constexpr int XR = 8 * (G1 > NG - G1 ? G1 : NG - G1);
       uint32_t xr[XR];
-      if (T6_PROBE != 3)
-        while (!mbar_try(xfull, tt & 1)) {
-        }
+      if (T6_PROBE != 3) t6_spin(&xfull[pj], tt & 1, 1, pj, tt);
       tc_fence_after();
       if (ph == 0)
         tmem_ld_row<8 * G1>(xaddr, xr);
@@ -410,13 +453,17 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
       __syncwarp();
-      named_arrive(T6_AXBAR, T5_NFULL);
+      if (lane == 0) mbar_arrive(&axr[pj]);
       if (tt + 2 < ntiles) {  // landmark of tile tt + 2: consumed after this tile's sigmoids
         const int64_t ni = (int64_t)(tt + 2) * T5_TILE + pk;
         na = lm[2 * ni];
         nb = lm[2 * ni + 1];
       }
-      if (tt >= T5_STAGES) t5_prod_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
+#if T6_DEBUG
+      if (tt >= T5_STAGES) t6_spin(&empty[pj * 2 + s], ((tt / T5_STAGES) - 1) & 1, 2, pj, tt);
+#else
+      if (tt >= T5_STAGES) t5_prod_wait(&empty[pj * 2 + s], ((tt / T5_STAGES) - 1) & 1);
+#endif
       const uint32_t adst = sbase + (s * T5_VOX + pj) * STAGE_A + kofs_a;
       const uint32_t bdst = sbase + OFF_B + (s * T5_VOX + pj) * STAGE_B + kofs_b;
       if (ph == 0) {
@@ -437,7 +484,7 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      named_arrive(1 + s, T5_NFULL);  // stage s written (the MMA warp syncs on it)
+      if (lane == 0) mbar_arrive(&full[pj * 2 + s]);  // this warp's share of the voxel's stage s is written
       a_cur = a_nxt;
       q_cur = q_nxt;
     }
@@ -457,57 +504,88 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     const uint32_t blo = (sb4 + (OFF_B >> 4)) | ((uint32_t)((256 * NG) >> 4) << 16);
     const uint32_t axlo = (sb4 + (OFF_AX >> 4)) | ((128u >> 4) << 16);
     const uint32_t bxlo = (sb4 + (OFF_BX >> 4)) | ((128u >> 4) << 16);
-    auto issue_x = [&]() {  // X(t) = A_x(t) (128 x 16) B_x^T (16 x XN) for the three voxels
-#pragma unroll
-      for (int j = 0; j < T5_VOX; ++j)
-        t6_mma_lo(tmem + XBASE + j * XN, axlo + j * (T6_AX_BYTES >> 4), bxlo, HI_X, idesc_x, 0u);
-      t6_commit(xfull);
+    auto issue_x = [&](auto voxel) {  // X(t) = A_x(t) (128 x 16) B_x^T (16 x XN) of one voxel
+      constexpr int J = decltype(voxel)::value;
+      t6_mma_lo(tmem + XBASE + J * XN, axlo + J * (T6_AX_BYTES >> 4), bxlo, HI_X, idesc_x, 0u);
+      t6_commit(&xfull[J]);
     };
-    auto issue_s = [&](auto stage, bool first, uint32_t dbase) {
-      constexpr int S = decltype(stage)::value;
+    auto issue_s = [&](auto voxel, auto stage, bool first, uint32_t d) {
+      constexpr int J = decltype(voxel)::value, S = decltype(stage)::value;
 #pragma unroll
-      for (int j = 0; j < T5_VOX; ++j) {
-        const uint32_t d = dbase + j * XN;
-#pragma unroll
-        for (int ks = 0; ks < T5_KS; ++ks) {
-          if (T6_PROBE == 5) continue;
-          const uint32_t a = alo + (uint32_t)(((S * T5_VOX + j) * STAGE_A + ks * T6_BLK_A) >> 4);
-          const uint32_t bb = blo + (uint32_t)(((S * T5_VOX + j) * STAGE_B + ks * BLK_B) >> 4);
-          // rows [E_lo; E_hi; 0] x vs_hi, then rows [E_hi; 0; ..] x vs_lo into the same D rows
-          t6_mma_lo(d, a, bb, HI_S, idesc_s, (ks > 0 || !first) ? 1u : 0u);
+      for (int ks = 0; ks < T5_KS; ++ks) {
+        if (T6_PROBE == 5) continue;
+        const uint32_t a = alo + (uint32_t)(((S * T5_VOX + J) * STAGE_A + ks * T6_BLK_A) >> 4);
+        const uint32_t bb = blo + (uint32_t)(((S * T5_VOX + J) * STAGE_B + ks * BLK_B) >> 4);
+        // rows [E_lo; E_hi; 0] x vs_hi, then rows [E_hi; 0; ..] x vs_lo into the same D rows
+        t6_mma_lo(d, a, bb, HI_S, idesc_s, (ks > 0 || !first) ? 1u : 0u);
 #if T6_PROBE != 1  // (timing probe 1: without the second S MMA; wrong results)
-          t6_mma_lo(d, a + ((3 * 128) >> 4), bb + ((NG * 128) >> 4), HI_S, idesc_s, 1u);
+        t6_mma_lo(d, a + ((3 * 128) >> 4), bb + ((NG * 128) >> 4), HI_S, idesc_s, 1u);
 #endif
-        }
       }
     };
-    __syncwarp();
-    named_sync(T6_AXBAR, T5_NFULL);  // A_x(0) written
-    tc_fence_after();
-    if (t6_elect(lane)) issue_x();
-    for (int tt = 0; tt < ntiles; ++tt) {
-      const int s = tt % T5_STAGES;
-      const int k = tt / T5_FLUSH, b = k & 1;
-      __syncwarp();
-      named_sync(T6_AXBAR, T5_NFULL);  // X(tt) read by every producer, A_x(tt + 1) written
-      tc_fence_after();
-      if (tt + 1 < ntiles && t6_elect(lane)) issue_x();
-      __syncwarp();
-      named_sync(1 + s, T5_NFULL);  // tile tt's operands written
-      tc_fence_after();
-      if (t6_elect(lane)) {
-        const bool first = tt % T5_FLUSH == 0;
-        if (first && k >= 2) {  // buffer b last held span k - 2: drained long ago, normally
-          mbar_wait_backoff(&fempty[b], ((k >> 1) - 1) & 1, T5_MMA_SLEEP);
+    // One elected thread serves the three voxel pipelines round robin: X(t) of a voxel as soon
+    // as its producers have read X(t - 1) and written A_x(t), the S MMAs of a tile as soon as
+    // its stage is written.  xt / st: next tile whose X / S MMAs are to be issued.
+    if (t6_elect(lane)) {
+      int xt[T5_VOX], st[T5_VOX];
+#pragma unroll
+      for (int j = 0; j < T5_VOX; ++j) xt[j] = st[j] = 0;
+      int left = 2 * T5_VOX * ntiles;
+      auto serve = [&](auto voxel) {
+        constexpr int J = decltype(voxel)::value;
+        bool any = false;
+        if (xt[J] < ntiles && mbar_try(&axr[J], xt[J] & 1)) {
           tc_fence_after();
+          issue_x(voxel);
+          ++xt[J];
+          --left;
+          any = true;
         }
-        const uint32_t dbase = tmem + ((uint32_t)(16 * b) << 16);
-        if (s == 0)
-          issue_s(std::integral_constant<int, 0>{}, first, dbase);
-        else
-          issue_s(std::integral_constant<int, 1>{}, first, dbase);
-        if (span_end(tt)) t6_commit(&ffull[b]);
-        t6_commit(&empty[s]);
+        const int tt = st[J], s = tt & 1;
+        const int k = tt / T5_FLUSH, b = k & 1;
+        const bool first = tt % T5_FLUSH == 0;
+        // a span's first tile also needs its accumulator buffer drained (it last held span k - 2).
+        // Never block on that: the epilogue walks the voxels together, so a voxel that runs
+        // ahead must let this thread serve the others, or they would wait for each other.
+        // T6_X_FIRST: the S MMAs of tile tt are held back until X(tt + 2) is issued (its A_x is
+        // written ~P1 after tile tt's stage): otherwise every X queues behind a tile's worth of
+        // S MMAs in the in-order tensor pipe and the producers wait even longer for it
+        // (139.4 vs 135.5 ms).  Probing all barriers first and issuing every ready X before any
+        // S was slower (142.7 ms).
+        if (tt < ntiles && (!T6_X_FIRST || xt[J] >= tt + 3 || xt[J] >= ntiles) &&
+            mbar_try(&full[J * 2 + s], (tt >> 1) & 1) &&
+            (!first || k < 2 || mbar_try(&fempty[J * 2 + b], ((k >> 1) - 1) & 1))) {
+          tc_fence_after();
+          const uint32_t d = tmem + ((uint32_t)(16 * b) << 16) + J * XN;
+          if (s == 0)
+            issue_s(voxel, std::integral_constant<int, 0>{}, first, d);
+          else
+            issue_s(voxel, std::integral_constant<int, 1>{}, first, d);
+          if (span_end(tt)) t6_commit(&ffull[J * 2 + b]);
+          t6_commit(&empty[J * 2 + s]);
+          ++st[J];
+          --left;
+          any = true;
+        }
+        return any;
+      };
+#if T6_DEBUG
+      long long idle = 0;
+#endif
+      while (left > 0) {
+        const bool a0 = serve(std::integral_constant<int, 0>{});
+        const bool a1 = serve(std::integral_constant<int, 1>{});
+        const bool a2 = serve(std::integral_constant<int, 2>{});
+        if (!(a0 | a1 | a2)) __nanosleep(T5_MMA_SLEEP);
+#if T6_DEBUG
+        idle = (a0 | a1 | a2) ? 0 : idle + 1;
+        if (idle > 2000000) {
+          if (blockIdx.x == 0)
+            printf("t6 stuck: left %d ntiles %d xt %d %d %d st %d %d %d\n", left, ntiles, xt[0], xt[1], xt[2], st[0],
+                   st[1], st[2]);
+          __trap();
+        }
+#endif
       }
     }
     __syncwarp();
@@ -529,11 +607,15 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     const int nspans = (ntiles + T5_FLUSH - 1) / T5_FLUSH;
     for (int k = 0; k < nspans; ++k) {
       const int b = k & 1;
-      mbar_wait_poll(&ffull[b], (k >> 1) & 1, T5_EPI_SLEEP);
-      tc_fence_after();
 #pragma unroll 1
       for (int step = 0; step < T5_VOX; ++step) {
         const int j = (sp + step) % T5_VOX;
+#if T6_DEBUG
+        t6_spin(&ffull[j * 2 + b], (k >> 1) & 1, 4, j, k);
+#else
+        mbar_wait_poll(&ffull[j * 2 + b], (k >> 1) & 1, T5_EPI_SLEEP);
+#endif
+        tc_fence_after();
         const uint32_t radr = tmem + ((uint32_t)(32 * sp + 16 * b) << 16) + j * XN;
         double* aj = acc + j * ACC_V + e;
         if (T6_PROBE != 4) {
@@ -553,11 +635,11 @@ k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
             }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fempty[j * 2 + b]);
         named_sync(T6_EPIBAR, 96);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&fempty[b]);
     }
   }
   tc_fence_before();

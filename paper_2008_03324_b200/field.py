@@ -344,10 +344,11 @@ class _DeviceModel:
 _MASK_CHUNK_BYTES = 1 << 30
 
 # GP info kernel: "t5" (default; tcgen05.mma FP16 split with TMEM accumulators, N_s <= 80,
-# other N_s run "h16"), "h16" (mma.sync FP16 split, k16 per MMA), "tf32" (mma.sync TF32x3)
-# or "simt" (FP32 FFMA2); the alternatives are kept as cross-checks.
-GP_INFO_KERNEL = "t6"
-_GP_INFO_FLAGS = {"t6": 0, "t5": _lib.BUILD_T5, "h16": _lib.BUILD_H16, "tf32": _lib.BUILD_TF32,
+# other N_s run "h16"), "t6" (t5 with the sigmoid exponent arguments on the tensor cores too;
+# measured slower, kept as a cross-check), "h16" (mma.sync FP16 split, k16 per MMA), "tf32"
+# (mma.sync TF32x3) or "simt" (FP32 FFMA2); the alternatives are kept as cross-checks.
+GP_INFO_KERNEL = "t5"
+_GP_INFO_FLAGS = {"t5": 0, "t6": _lib.BUILD_T6, "h16": _lib.BUILD_H16, "tf32": _lib.BUILD_TF32,
                   "simt": _lib.BUILD_SIMT}
 
 
