@@ -175,6 +175,9 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 #ifndef T5_SLEEPWAIT
 #define T5_SLEEPWAIT 1
 #endif
+#ifndef T5_FAST_ISSUE
+#define T5_FAST_ISSUE 1
+#endif
 #ifndef T5_XPAIR
 #define T5_XPAIR 1
 #endif
@@ -655,8 +658,34 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     }
   } else if (warp == T5_MMAW) {
     // ───────────── MMA issue (one thread) ─────────────
+    // T5_FAST_ISSUE: the issuing thread is chosen by elect.sync (ptxas then keeps the operands
+    // in uniform registers instead of a per-instruction R2UR waterfall) and the shared memory
+    // descriptors are {loop-invariant low word + constant, constant high word} with the stage
+    // unrolled: ~3 instead of ~21 instructions per MMA (the stage's release, tcgen05.commit
+    // after the last MMA, is that much earlier).
     {
       constexpr uint32_t idesc = t5_idesc<NG>();
+#if T5_FAST_ISSUE
+      constexpr uint32_t HI = (128u >> 4) | (1u << 14);  // SBO = 128, descriptor version 1 (bit 46)
+      const uint32_t sb4 = sbase >> 4;                   // (< 2^14: shared memory is < 256 KB)
+      const uint32_t alo = sb4 | ((uint32_t)(1024 >> 4) << 16);
+      const uint32_t blo = (sb4 + (OFF_B >> 4)) | ((uint32_t)((256 * NG) >> 4) << 16);
+      auto issue = [&](auto stage, bool first, uint32_t dbase) {
+        constexpr int S = decltype(stage)::value;
+#pragma unroll
+        for (int j = 0; j < T5_VOX; ++j)
+#pragma unroll
+          for (int ks = 0; ks < T5_KS; ++ks) {
+            const uint32_t a = alo + (uint32_t)(((S * T5_VOX + j) * STAGE_A + ks * T5_BLK_A) >> 4);
+            const uint32_t b = blo + (uint32_t)(((S * T5_VOX + j) * STAGE_B + ks * BLK_B) >> 4);
+            const uint32_t accf = (!first || ks > 0) ? 1u : 0u;
+            asm volatile("{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+                         "mov.b64 da, {%1, %3};\n\tmov.b64 db, {%2, %3};\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, p;\n\t}" ::"r"(dbase + j * NCOL),
+                         "r"(a), "r"(b), "r"(HI), "r"(idesc), "r"(accf));
+          }
+      };
+#endif
       for (int tt = 0; tt < ntiles; ++tt) {
         const int s = tt % T5_STAGES;
         const int k = tt / T5_FLUSH, b = k & 1;
@@ -667,12 +696,28 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         mbar_wait_backoff(&full[s], (tt / T5_STAGES) & 1, T5_MMA_SLEEP);
 #endif
         tc_fence_after();
+#if T5_FAST_ISSUE
+        uint32_t elected;
+        asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(elected));
+        if (elected) {
+#else
         if (lane == 0) {  // one thread issues
+#endif
           const bool first = tt % T5_FLUSH == 0;
           if (first && k >= 2) {  // buffer b last held span k - 2: drained long ago, normally
             mbar_wait_backoff(&fempty[b], ((k >> 1) - 1) & 1, T5_MMA_SLEEP);
             tc_fence_after();
           }
+#if T5_FAST_ISSUE
+          static_assert(T5_STAGES <= 3, "stage unrolling");
+          const uint32_t dbase = tmem + ((uint32_t)(16 * b) << 16);
+          if (s == 0)
+            issue(std::integral_constant<int, 0>{}, first, dbase);
+          else if (s == 1)
+            issue(std::integral_constant<int, 1>{}, first, dbase);
+          else
+            issue(std::integral_constant<int, T5_STAGES - 1>{}, first, dbase);
+#else
 #pragma unroll
           for (int j = 0; j < T5_VOX; ++j) {
             const uint32_t a0 = sbase + (s * T5_VOX + j) * STAGE_A;
@@ -688,6 +733,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
                            "l"(da), "l"(db), "r"(idesc), "r"(accf));
             }
           }
+#endif
           if (span_end(tt))
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                              smem_u32(&ffull[b]))
