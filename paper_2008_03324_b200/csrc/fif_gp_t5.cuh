@@ -175,6 +175,9 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 #ifndef T5_SLEEPWAIT
 #define T5_SLEEPWAIT 1
 #endif
+#ifndef T5_PIPE_PROLOGUE
+#define T5_PIPE_PROLOGUE 0  // measured slower (121.0 vs 118.5 ms, 120 registers): DESIGN 8b
+#endif
 #ifndef T5_FAST_ISSUE
 #define T5_FAST_ISSUE 1
 #endif
@@ -592,6 +595,73 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     const float inv_s2_s = inv_s2 * voxel_scale(pj);  // exact: a power of two
     const uint32_t kofs_a = (pk >> 4) * T5_BLK_A + ((pk >> 3) & 1) * 1024 + (pk & 7) * 16;
     const uint32_t kofs_b = (pk >> 4) * BLK_B + ((pk >> 3) & 1) * (256 * NG) + (pk & 7) * 16;
+#if T5_PIPE_PROLOGUE && T5_PARTS == 2 && !T5_SHARE_U
+    // The pair prologue (landmark, gate, bearing: a dependent chain through rsqrt and its Newton
+    // step) of tile tt + 1 sits in the middle of tile tt's sigmoid stream, where ptxas
+    // interleaves it with independent work, instead of at the loop top where every warp of
+    // the scheduler waits on it at the same time.
+    auto prep = [&](int tile, float4 a, float4 b) {
+      if (!pvok) b.w = 0.f;
+      if (HAS_MASK && b.w != 0.f) {
+        const int64_t i = (int64_t)tile * T5_TILE + pk;
+        const bool keep = use_gbits ? ((gbits[pj * (n_pad >> 5) + (i >> 5)] >> (i & 31)) & 1u) != 0
+                                    : gate_keep(gate, pv, i);
+        if (!keep) b.w = 0.f;
+      }
+      return pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
+    };
+    float4 a_cur = lm[2 * pk];
+    PairF q_cur = prep(0, a_cur, lm[2 * pk + 1]);
+    float4 na = a_cur, nb = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ntiles > 1) {
+      na = lm[2 * (T5_TILE + pk)];
+      nb = lm[2 * (T5_TILE + pk) + 1];
+    }
+    for (int tt = 0; tt < ntiles; ++tt) {
+      const int s = tt % T5_STAGES;
+      if (tt >= T5_STAGES) t5_prod_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
+      const float4 a_nxt = na, b_nxt = nb;  // tile tt + 1's landmark (loaded during tile tt - 1)
+      if (tt + 2 < ntiles) {
+        const int64_t ni = (int64_t)(tt + 2) * T5_TILE + pk;
+        na = lm[2 * ni];
+        nb = lm[2 * ni + 1];
+      }
+      const uint32_t adst = sbase + (s * T5_VOX + pj) * STAGE_A + kofs_a;
+      const uint32_t bdst = sbase + OFF_B + (s * T5_VOX + pj) * STAGE_B + kofs_b;
+      PairF q_nxt = q_cur;
+      if (ph == 0) {
+        constexpr int GA = G1 / 2;
+        t5_sigmoids<NG, 0, GA>(Z, q_cur.ux, q_cur.uy, q_cur.uz, bx, bdst);
+        if (tt + 1 < ntiles) q_nxt = prep(tt + 1, a_nxt, b_nxt);
+        float e[24];
+        entries21(q_cur, a_cur, e);
+        e[21] = e[22] = e[23] = 0.f;
+#pragma unroll
+        for (int gi = 0; gi < 3; ++gi) {
+          uint32_t hv[4], lv[4];
+#pragma unroll
+          for (int p = 0; p < 4; ++p) t5_split2(e[8 * gi + 2 * p], e[8 * gi + 2 * p + 1], hv[p], lv[p]);
+          sts128(adst + (2 * gi) * 128, hv[0], hv[1], hv[2], hv[3]);
+          sts128(adst + (2 * gi + 1) * 128, lv[0], lv[1], lv[2], lv[3]);
+        }
+        t5_sigmoids<NG, GA, G1>(Z, q_cur.ux, q_cur.uy, q_cur.uz, bx, bdst);
+      } else {
+        constexpr int GB = G1 + (G2 - G1) / 2;
+        t5_sigmoids<NG, G1, GB>(Z, q_cur.ux, q_cur.uy, q_cur.uz, bx, bdst);
+        if (tt + 1 < ntiles) q_nxt = prep(tt + 1, a_nxt, b_nxt);
+        t5_sigmoids<NG, GB, G2>(Z, q_cur.ux, q_cur.uy, q_cur.uz, bx, bdst);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+#if T5_NAMED
+      named_arrive(1 + s, T5_NFULL);  // stage s written (the MMA warp syncs on it)
+#else
+      if (lane == 0) mbar_arrive(&full[s]);
+#endif
+      a_cur = a_nxt;
+      q_cur = q_nxt;
+    }
+#else
     float4 na = lm[2 * pk], nb = lm[2 * pk + 1];
     for (int tt = 0; tt < ntiles; ++tt) {
       const int s = tt % T5_STAGES;
@@ -656,6 +726,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       if (lane == 0) mbar_arrive(&full[s]);
 #endif
     }
+#endif  // T5_PIPE_PROLOGUE
   } else if (warp == T5_MMAW) {
     // ───────────── MMA issue (one thread) ─────────────
     // T5_FAST_ISSUE: the issuing thread is chosen by elect.sync (ptxas then keeps the operands
