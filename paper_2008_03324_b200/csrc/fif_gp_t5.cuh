@@ -69,7 +69,7 @@ constexpr int T5_NU = (T5_PWARPS + T5_EWARPS) * 32;         // bearing-ring name
 constexpr int T5_MAX_NG = 10;       // N_s <= 80
 constexpr int T5_BLK_A = 64 * 16 * 2;  // bytes per k-step of A (M = 64)
 
-constexpr int T5_BAR_BYTES = 128;  // mbarriers, TMEM slot, scale bits (rounded up)
+constexpr int T5_BAR_BYTES = 384;  // mbarriers (8 shared + 24 per-voxel), TMEM slot, scale bits (rounded up)
 // PARTS = 4: part 0 shares each pair's bearing with parts 1-3 through shared memory
 // ([stage][voxel][landmark] float4, after the barriers) and a named barrier per
 // (voxel, landmark half, stage): ids 1 + T5_STAGES ...
@@ -174,6 +174,19 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 #endif
 #ifndef T5_SLEEPWAIT
 #define T5_SLEEPWAIT 1
+#endif
+// T5_PERVOX: every voxel of the CTA is its own pipeline: its 4 producer warps, stages and
+// accumulator buffers have their own mbarriers ([voxel][stage / buffer]); the MMA thread
+// polls them and issues a voxel's MMAs as soon as ITS stage is written, and the voxels'
+// producers start T5_STAGGER_NS apart (the idea: one voxel's landmark load / prologue /
+// stage wait overlaps the others' XU-bound sigmoid phase instead of all 12 warps meeting
+// there).  Measured slower: 120.4 ms (stagger 300 or 600 ns), 121.1 ms (no stagger) vs
+// 118.5 ms with the shared named barriers, rows bit-identical.
+#ifndef T5_PERVOX
+#define T5_PERVOX 0
+#endif
+#ifndef T5_STAGGER_NS
+#define T5_STAGGER_NS 300
 #endif
 #ifndef T5_PIPE_PROLOGUE
 #define T5_PIPE_PROLOGUE 0  // measured slower (121.0 vs 118.5 ms, 120 registers): DESIGN 8b
@@ -384,6 +397,12 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
   uint64_t* fempty = ffull + 2;         // [2] the epilogue has drained buffer b
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fempty + 2);
   int* sbits = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* vfull = reinterpret_cast<uint64_t*>(smem + OFF_BAR + 128);  // T5_PERVOX: [voxel][stage]
+  uint64_t* vempty = vfull + T5_VOX * T5_STAGES;
+  uint64_t* vffull = vempty + T5_VOX * T5_STAGES;                        // [voxel][buffer]
+  uint64_t* vfempty = vffull + T5_VOX * 2;
+  static_assert(128 + 8 * (2 * T5_VOX * T5_STAGES + 4 * T5_VOX) <= T5_BAR_BYTES, "barrier bytes");
+  constexpr bool PERVOX = T5_PERVOX && T5_FAST_ISSUE && !T5_PIPE_PROLOGUE && !T5_DECOUPLE && !T5_SHARE_U;
   // masked builds: the pre-pass evaluates each pair's matchability gate once and keeps the
   // answers as bits ([voxel][n_pad / 32] words) for the main loop (when they fit)
   float4* ush = reinterpret_cast<float4*>(smem + OFF_BAR + T5_BAR_BYTES);  // PARTS = 4 bearing share
@@ -402,6 +421,14 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ffull[b], 1);
       mbar_init(&fempty[b], 3);
+    }
+    for (int i = 0; i < T5_VOX * T5_STAGES; ++i) {
+      mbar_init(&vfull[i], 2 * T5_PARTS);  // the voxel's producer warps
+      mbar_init(&vempty[i], 1);
+    }
+    for (int i = 0; i < T5_VOX * 2; ++i) {
+      mbar_init(&vffull[i], 1);
+      mbar_init(&vfempty[i], 3);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -663,6 +690,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     }
 #else
     float4 na = lm[2 * pk], nb = lm[2 * pk + 1];
+    if (PERVOX && T5_STAGGER_NS > 0 && pj > 0) __nanosleep(pj * T5_STAGGER_NS);
     for (int tt = 0; tt < ntiles; ++tt) {
       const int s = tt % T5_STAGES;
       const float4 a = na;
@@ -681,7 +709,8 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       }
       PairF q;
       if (!T5_SHARE_U || ph == 0) q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
-      if (tt >= T5_STAGES) t5_prod_wait(&empty[s], ((tt / T5_STAGES) - 1) & 1);
+      if (tt >= T5_STAGES)
+        t5_prod_wait(PERVOX ? &vempty[pj * T5_STAGES + s] : &empty[s], ((tt / T5_STAGES) - 1) & 1);
       if (T5_SHARE_U) {  // part 0 hands its bearing to the other parts (the slot is free: its last
                             // readers finished the tile whose MMA freed this stage)
         const int bid = 1 + T5_STAGES + ((pj * 2 + (pk >> 5)) * T5_STAGES + s);
@@ -720,11 +749,15 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
+      if (PERVOX) {
+        if (lane == 0) mbar_arrive(&vfull[pj * T5_STAGES + s]);  // this warp's share of the voxel's stage
+      } else {
 #if T5_NAMED
-      named_arrive(1 + s, T5_NFULL);  // stage s written (the MMA warp syncs on it)
+        named_arrive(1 + s, T5_NFULL);  // stage s written (the MMA warp syncs on it)
 #else
-      if (lane == 0) mbar_arrive(&full[s]);
+        if (lane == 0) mbar_arrive(&full[s]);
 #endif
+      }
     }
 #endif  // T5_PIPE_PROLOGUE
   } else if (warp == T5_MMAW) {
@@ -756,6 +789,66 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
                          "r"(a), "r"(b), "r"(HI), "r"(idesc), "r"(accf));
           }
       };
+#endif
+#if T5_FAST_ISSUE
+      if (PERVOX) {
+        // one elected thread serves the three voxel pipelines round robin: the MMAs of a
+        // voxel's tile as soon as its stage is written (and, for a span's first tile, its
+        // accumulator buffer drained: never blocking on that, the other voxels need service)
+        auto issue1 = [&](auto voxel, auto stage, bool first, uint32_t d) {
+          constexpr int J = decltype(voxel)::value, S = decltype(stage)::value;
+#pragma unroll
+          for (int ks = 0; ks < T5_KS; ++ks) {
+            const uint32_t a = alo + (uint32_t)(((S * T5_VOX + J) * STAGE_A + ks * T5_BLK_A) >> 4);
+            const uint32_t b = blo + (uint32_t)(((S * T5_VOX + J) * STAGE_B + ks * BLK_B) >> 4);
+            const uint32_t accf = (!first || ks > 0) ? 1u : 0u;
+            asm volatile("{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+                         "mov.b64 da, {%1, %3};\n\tmov.b64 db, {%2, %3};\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, p;\n\t}" ::"r"(d),
+                         "r"(a), "r"(b), "r"(HI), "r"(idesc), "r"(accf));
+          }
+        };
+        static_assert(!(T5_PERVOX && T5_FAST_ISSUE) || T5_STAGES == 2, "per-voxel pipelines: 2 stages");
+        uint32_t elected;
+        asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(elected));
+        if (elected) {
+          int st[T5_VOX];
+#pragma unroll
+          for (int j = 0; j < T5_VOX; ++j) st[j] = 0;
+          int left = T5_VOX * ntiles;
+          auto serve = [&](auto voxel) {
+            constexpr int J = decltype(voxel)::value;
+            const int tt = st[J], s = tt & 1;
+            const int k = tt / T5_FLUSH, b = k & 1;
+            const bool first = tt % T5_FLUSH == 0;
+            if (!(tt < ntiles && mbar_try(&vfull[J * T5_STAGES + s], (tt >> 1) & 1) &&
+                  (!first || k < 2 || mbar_try(&vfempty[J * 2 + b], ((k >> 1) - 1) & 1))))
+              return false;
+            tc_fence_after();
+            const uint32_t d = tmem + ((uint32_t)(16 * b) << 16) + J * NCOL;
+            if (s == 0)
+              issue1(voxel, std::integral_constant<int, 0>{}, first, d);
+            else
+              issue1(voxel, std::integral_constant<int, 1>{}, first, d);
+            if (span_end(tt))
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                               smem_u32(&vffull[J * 2 + b]))
+                           : "memory");
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&vempty[J * T5_STAGES + s]))
+                         : "memory");
+            ++st[J];
+            --left;
+            return true;
+          };
+          while (left > 0) {
+            bool any = serve(std::integral_constant<int, 0>{});
+            if constexpr (T5_VOX > 1) any |= serve(std::integral_constant<int, 1>{});
+            if constexpr (T5_VOX > 2) any |= serve(std::integral_constant<int, 2>{});
+            if (!any) __nanosleep(T5_MMA_SLEEP);
+          }
+        }
+      } else
 #endif
       for (int tt = 0; tt < ntiles; ++tt) {
         const int s = tt % T5_STAGES;
@@ -829,10 +922,16 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     const int nspans = (ntiles + T5_FLUSH - 1) / T5_FLUSH;
     for (int k = 0; k < nspans; ++k) {
       const int b = k & 1;
-      mbar_wait_poll(&ffull[b], (k >> 1) & 1, T5_EPI_SLEEP);
-      tc_fence_after();
+      if (!PERVOX) {
+        mbar_wait_poll(&ffull[b], (k >> 1) & 1, T5_EPI_SLEEP);
+        tc_fence_after();
+      }
 #pragma unroll 1
       for (int j = 0; j < T5_VOX; ++j) {
+        if (PERVOX) {
+          mbar_wait_poll(&vffull[j * 2 + b], (k >> 1) & 1, T5_EPI_SLEEP);
+          tc_fence_after();
+        }
         const uint32_t row = tmem + ((uint32_t)(32 * sp + 16 * b) << 16) + j * NCOL;
         double* aj = acc + j * ACC_V;
 #if T5_EPI_CHUNK
@@ -866,10 +965,17 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
           if ((i & 1) == part && row_ok && sm < ns) aj[sm * 21 + e] += (double)v;  // unscaled (exact 2^k at the end)
         }
 #endif
+        if (PERVOX) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&vfempty[j * 2 + b]);
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&fempty[b]);
+      if (!PERVOX) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fempty[b]);
+      }
     }
   }
   tc_fence_before();
