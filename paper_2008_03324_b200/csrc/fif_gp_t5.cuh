@@ -188,6 +188,9 @@ __device__ __forceinline__ void tmem_ld_half(uint32_t addr, float* v) {
 #ifndef T5_STAGGER_NS
 #define T5_STAGGER_NS 300
 #endif
+#ifndef T5_EARLY_PROBE
+#define T5_EARLY_PROBE 0  // measured slower (121.3 vs 118.5 ms): DESIGN 8b
+#endif
 #ifndef T5_PIPE_PROLOGUE
 #define T5_PIPE_PROLOGUE 0  // measured slower (121.0 vs 118.5 ms, 120 registers): DESIGN 8b
 #endif
@@ -656,10 +659,13 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       const uint32_t adst = sbase + (s * T5_VOX + pj) * STAGE_A + kofs_a;
       const uint32_t bdst = sbase + OFF_B + (s * T5_VOX + pj) * STAGE_B + kofs_b;
       PairF q_nxt = q_cur;
+      // (T5_PIPE_PROLOGUE == 2: after the tile's last store instead, where the sigmoid
+      // temporaries are dead and the stores' completion, which the proxy fence waits for,
+      // overlaps the prologue)
       if (ph == 0) {
-        constexpr int GA = G1 / 2;
+        constexpr int GA = T5_PIPE_PROLOGUE == 2 ? 0 : G1 / 2;
         t5_sigmoids<NG, 0, GA>(Z, q_cur.ux, q_cur.uy, q_cur.uz, bx, bdst);
-        if (tt + 1 < ntiles) q_nxt = prep(tt + 1, a_nxt, b_nxt);
+        if (T5_PIPE_PROLOGUE != 2 && tt + 1 < ntiles) q_nxt = prep(tt + 1, a_nxt, b_nxt);
         float e[24];
         entries21(q_cur, a_cur, e);
         e[21] = e[22] = e[23] = 0.f;
@@ -673,11 +679,12 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
         }
         t5_sigmoids<NG, GA, G1>(Z, q_cur.ux, q_cur.uy, q_cur.uz, bx, bdst);
       } else {
-        constexpr int GB = G1 + (G2 - G1) / 2;
+        constexpr int GB = T5_PIPE_PROLOGUE == 2 ? G1 : G1 + (G2 - G1) / 2;
         t5_sigmoids<NG, G1, GB>(Z, q_cur.ux, q_cur.uy, q_cur.uz, bx, bdst);
-        if (tt + 1 < ntiles) q_nxt = prep(tt + 1, a_nxt, b_nxt);
+        if (T5_PIPE_PROLOGUE != 2 && tt + 1 < ntiles) q_nxt = prep(tt + 1, a_nxt, b_nxt);
         t5_sigmoids<NG, GB, G2>(Z, q_cur.ux, q_cur.uy, q_cur.uz, bx, bdst);
       }
+      if (T5_PIPE_PROLOGUE == 2 && tt + 1 < ntiles) q_nxt = prep(tt + 1, a_nxt, b_nxt);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
 #if T5_NAMED
@@ -693,6 +700,12 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
     if (PERVOX && T5_STAGGER_NS > 0 && pj > 0) __nanosleep(pj * T5_STAGGER_NS);
     for (int tt = 0; tt < ntiles; ++tt) {
       const int s = tt % T5_STAGES;
+      // T5_EARLY_PROBE: the stage-empty barrier is probed before the pair prologue, so the
+      // probe's own latency (a try_wait takes ~100 cycles to answer even when the phase is
+      // complete) overlaps the prologue instead of following it
+      uint64_t* ebar = PERVOX ? &vempty[pj * T5_STAGES + s] : &empty[s];
+      bool stage_free = tt < T5_STAGES;
+      if (T5_EARLY_PROBE && tt >= T5_STAGES) stage_free = mbar_try(ebar, ((tt / T5_STAGES) - 1) & 1);
       const float4 a = na;
       float4 b = nb;
       if (tt + 1 < ntiles) {
@@ -709,8 +722,7 @@ k_gp_info_t5(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v
       }
       PairF q;
       if (!T5_SHARE_U || ph == 0) q = pair_prologue(a, b, ch, cl, inv_s2_s);  // w (and every entry) carries the voxel scale
-      if (tt >= T5_STAGES)
-        t5_prod_wait(PERVOX ? &vempty[pj * T5_STAGES + s] : &empty[s], ((tt / T5_STAGES) - 1) & 1);
+      if (!stage_free) t5_prod_wait(ebar, ((tt / T5_STAGES) - 1) & 1);
       if (T5_SHARE_U) {  // part 0 hands its bearing to the other parts (the slot is free: its last
                             // readers finished the tile whose MMA freed this stage)
         const int bid = 1 + T5_STAGES + ((pj * 2 + (pk >> 5)) * T5_STAGES + s);

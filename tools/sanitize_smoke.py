@@ -20,6 +20,11 @@ vd /= np.linalg.norm(vd, axis=1, keepdims=True)
 grid = F.GridConfig(np.array([-1.0, -1.0, 0.25]), 0.5, np.array([5, 4, 3]))
 quad, gp30, gp150 = F.build_quad_model(), F.build_gp_model(30), F.build_gp_model(150)
 fields = {}
+gp70 = F.build_gp_model(70)
+for kernel in ("t5", "t6"):  # tcgen05 builds (N_s = 30 and 70)
+    FD.GP_INFO_KERNEL = kernel
+    for model in (gp30, gp70):
+        F.Field.build(pts, grid, model, "info")
 for kernel in ("h16", "tf32", "simt"):
     FD.GP_INFO_KERNEL = kernel
     for model in (quad, gp30, gp150):
