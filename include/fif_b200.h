@@ -111,7 +111,9 @@ int64_t fif_build_scratch_bytes(int64_t n_points);
  *   S = sum_i vs_i (x) I_i is the pre-kinv factor (reference factor = kinv @ S).
  * Optional d_out32: the same array in float32 (the query operand for GP).
  * d_scratch: fif_build_scratch_bytes(n_points) bytes.  build_flags:
- * FIF_BUILD_EXACT (quad only) selects the bit-exact reference arithmetic.     */
+ * FIF_BUILD_EXACT (quad only) selects the bit-exact reference arithmetic; the
+ * FIF_BUILD_SIMT / TF32 / H16 / T6 flags select alternative GP info kernels (all
+ * within the same tolerance; 0 = the fastest, k_gp_info_t5).                  */
 int fif_build(int factor_kind, const fif_model* model, const double* d_points, int64_t n_points,
               const fif_grid* grid, const double* d_centers, int64_t v_begin, int64_t v_end,
               const uint8_t* d_mask, double sigma, uint32_t build_flags, void* d_scratch, double* d_out64,

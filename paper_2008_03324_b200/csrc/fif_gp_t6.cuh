@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
 k_gp_info_t6(const float4* __restrict__ lm, int64_t n_pad, VoxSrc src, int64_t v0, int64_t v1, int ns, float inv_s2,
              float cexp, const __grid_constant__ T6Z Z, double* __restrict__ out64, float* __restrict__ out32) {
   using LY = T6Layout<NG>;
-  constexpr int NCOL = LY::NCOL, XN = LY::XN, BLK_B = LY::BLK_B, STAGE_A = LY::STAGE_A, STAGE_B = LY::STAGE_B;
+  constexpr int XN = LY::XN, BLK_B = LY::BLK_B, STAGE_A = LY::STAGE_A, STAGE_B = LY::STAGE_B;
   constexpr int OFF_B = LY::OFF_B, OFF_ACC = LY::OFF_ACC, ACC_V = LY::ACC_V, OFF_BAR = LY::OFF_BAR;
   constexpr int OFF_AX = LY::OFF_AX, OFF_BX = LY::OFF_BX, XBASE = LY::XBASE;
   constexpr int G1 = T6_G1(NG);
