@@ -360,6 +360,12 @@ def build_rows(points: torch.Tensor, model, want_trace: bool, sigma: float, devi
     """One fif_build launch: rows [v_begin, v_end) of the z-major grid (or of `centers`).
     Returns (f64 rows (R, width_packed), f32 copy or None); out64 / out32 (contiguous row
     ranges of a larger field) receive the rows when given."""
+    # the C ABI reads plain double pointers: anything else would be reinterpreted silently
+    if points.dtype != torch.float64 or points.dim() != 2 or points.shape[1] != 3 or not points.is_contiguous():
+        raise TypeError(f"build_rows: points must be a contiguous (N, 3) float64 tensor, got {tuple(points.shape)} "
+                        f"{points.dtype}")
+    if centers is not None and (centers.dtype != torch.float64 or not centers.is_contiguous()):
+        raise TypeError(f"build_rows: centers must be a contiguous float64 tensor, got {centers.dtype}")
     dm = dmodel or _DeviceModel(model, device)
     n_v = 10 if isinstance(model, QuadraticVisibility) else model.n_v
     width = n_v if want_trace else n_v * 21
@@ -398,6 +404,9 @@ def build_matched_rows(points: torch.Tensor, model, want_trace: bool, sigma: flo
     out64 = torch.empty((rows, width), dtype=torch.float64, device=device)
     gp = isinstance(model, GpVisibility)
     out32 = torch.empty((rows, width), dtype=torch.float32, device=device) if (gp and f32_copy) else None
+    if points.dtype != torch.float64 or not points.is_contiguous() or centers.dtype != torch.float64 or \
+            not centers.is_contiguous():
+        raise TypeError("build_matched_rows: points and centers must be contiguous float64 tensors")
     scratch = torch.empty(int(_lib.load().fif_build_scratch_bytes(points.shape[0])), dtype=torch.uint8, device=device)
     m, vd, _keep = matchability.device_match(device, view_dirs)
     kind = _lib.KIND_TRACE if want_trace else _lib.KIND_INFO

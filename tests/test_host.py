@@ -180,3 +180,19 @@ def test_junction_basis_matches_reference():
     assert np.allclose(b.cost_matrix(4), g["R4"], rtol=1e-12, atol=1e-9)
     assert np.allclose(b.cost_matrix(2), g["R2"], rtol=1e-12, atol=1e-9)
     assert np.allclose(b.coeffs_from_derivs(g["D0"]), g["coeffs0"], rtol=1e-12, atol=1e-12)
+
+
+def test_build_rows_rejects_non_float64_tensors():
+    """The C ABI takes plain double pointers (include/fif_b200.h fif_build): a float32 landmark
+    tensor would be reinterpreted, so the host refuses it before any library call."""
+    import torch
+
+    from paper_2008_03324_b200 import field as FD
+
+    grid = F.GridConfig(np.zeros(3), 0.5, np.array([2, 2, 2]))
+    with pytest.raises(TypeError):
+        FD.build_rows(torch.zeros((4, 3), dtype=torch.float32), F.build_quad_model(), False, 1.0, torch.device("cpu"),
+                      grid=grid)
+    with pytest.raises(TypeError):
+        FD.build_rows(torch.zeros((3, 4), dtype=torch.float64).t(), F.build_quad_model(), False, 1.0,
+                      torch.device("cpu"), grid=grid)
