@@ -1636,6 +1636,7 @@ static int build_impl(int factor_kind, const fif_model* model, const double* d_p
     const int tpv = (ns + GT_G - 1) / GT_G;
     int vbt = GT_THREADS / tpv;
     if (vbt < 1) vbt = 1;
+    if (vbt > 32) vbt = 32;  // N_s <= 28: the pair records of more voxels would not fit the 96 KB opt-in below
     const int threads_t = ((vbt * tpv + 31) / 32) * 32;
     FIF_CHECK_ARG(threads_t <= GT_THREADS, "fif_build: N_s=%d too large for k_gp_trace", ns);
     const unsigned blocks_t = (unsigned)((rows + vbt - 1) / vbt);

@@ -313,3 +313,27 @@ def test_build_host_factors_pipelined(models, mname, kind):
     assert np.array_equal(ref.export_reference_to(chunk_rows=777), want)
     with pytest.raises(ValueError):
         F.Field.build(w.points, grid, model, kind, host_factors=True, host_out=torch.empty((3, 3), dtype=torch.float64))
+
+
+@pytest.mark.parametrize("ns", [4, 5, 9, 16, 20, 21, 28, 29])
+def test_small_sample_counts_trace_and_info(oracle, ns):
+    """GP fields with few samples (kernels.py:471-524 takes any N_s): the trace kernel packs
+    more voxels per CTA the fewer samples there are (N_s <= 20 once asked for more shared
+    memory than its opt-in: found by tools/soak_masked.py), the info build runs the small
+    tcgen05 / mma.sync instantiations; queries on both."""
+    rng = np.random.default_rng(100 + ns)
+    pts = rng.uniform([-3, -3, 0], [3, 3, 2], size=(300, 3))
+    grid = F.GridConfig(np.array([-1.0, -1.0, 0.0]), 0.5, np.array([4, 3, 2]))
+    m = F.build_gp_model(ns, length_scale=0.5)
+    for kind, tol in (("trace", 1e-5), ("info", 1e-4)):
+        f = F.Field.build(pts, grid, m, kind)
+        ref = oracle_field(oracle, m, grid.centers(), pts, kind)
+        mine = reference_order(f)
+        err = trace_rel_l2(mine, ref) if kind == "trace" else info_rel_fro(mine, ref)
+        assert err.max() <= tol, (kind, ns, err.max())
+        fm = F.Field.build(pts, grid, m, kind, matchability=F.Matchability(d_far=2.5))
+        refm = oracle_field(oracle, m, grid.centers(), pts, kind,
+                            mask=np.asarray(F.Matchability(d_far=2.5).mask(grid.centers(), pts), dtype=np.uint8))
+        idx = grid.linear_index(fm.occupied_index3)
+        errm = (trace_rel_l2 if kind == "trace" else info_rel_fro)(fm.factors, refm[idx])
+        assert errm.max() <= tol, (kind, ns, "masked", errm.max())
